@@ -1,0 +1,145 @@
+/* libzinf — C ABI of the B200-native ZeRO-Infinity partitioned data-parallel step.
+ *
+ * Drop-in boundary for the reference `infinisim` hot path (/root/reference).
+ * The reference is pure Python + numpy (pkg/pyproject.toml:10-12); the
+ * Python mirror `paper_2104_07857_b200` keeps its API and calls these
+ * entry points through ctypes (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *   - Every call returns a zi_status; on failure zi_last_error() holds a
+ *     thread-local message. Status codes map to the reference exception tree
+ *     (store.py:54-71): ZI_ECAPACITY -> CapacityExceeded, ZI_ENOTFOUND ->
+ *     KeyNotFound, ZI_EINVAL -> ValueError, ZI_ECUDA/ZI_ENCCL -> StoreError.
+ *   - All device work is asynchronous on the caller's `stream`
+ *     (a cudaStream_t passed as void*). Callers own every buffer; the
+ *     library owns nothing but its error string.
+ *   - Element counts are size_t; pointers are device pointers unless noted.
+ *   - half_kind: ZI_HALF_FP16 (SPEC parity type) or
+ *     ZI_HALF_BF16 (BASELINE configs).
+ */
+#ifndef ZINF_H
+#define ZINF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ZI_OK = 0,
+  ZI_EINVAL = 1,
+  ZI_ECAPACITY = 2,
+  ZI_ENOTFOUND = 3,
+  ZI_ECUDA = 4,
+  ZI_ENCCL = 5
+} zi_status;
+
+enum { ZI_HALF_FP16 = 0, ZI_HALF_BF16 = 1 };
+
+/* Element types, numbered as the reference shard format's dtype byte
+ * (store.py:37: 0 = f32, 1 = f16, 2 = f64) plus this build's 3 = bf16. */
+enum { ZI_DT_F32 = 0, ZI_DT_F16 = 1, ZI_DT_F64 = 2, ZI_DT_BF16 = 3 };
+
+/* Adam constants folded on the host in float32 exactly as oracle/adam.py
+ * AdamConsts.make does: lr, beta1, 1-beta1, beta2, 1-beta2, 1-beta1^t,
+ * 1-beta2^t, eps. */
+typedef struct {
+  float lr, b1, omb1, b2, omb2, bc1, bc2, eps;
+} zi_adam_consts;
+
+const char* zi_last_error(void);
+int zi_version(void);
+
+/* ---- optimizer ------------------------------------------------------------
+ * chunked_adam_step for one chunk: in place on fp32
+ * p/m/v with fp32 gradient g, writes the RNE half copy of p to p_half
+ * (may be NULL). Bit-exact with oracle/adam.py:adam_update. */
+int zi_adam_step(float* p, float* m, float* v, const float* g, void* p_half,
+                 size_t n, const zi_adam_consts* c, int half_kind, void* stream);
+
+/* ---- collectives ----------------------------------------------------------
+ * reduce_scatter fused with the half->fp32 cast and scale (SPEC.md:484-492,
+ * SPEC.md:750,782). contribs[k] (k = 0..n_contrib-1, in fold order) are
+ * full-length half gradient buckets, local or IPC-mapped peer memory.
+ *   out[i] = scale * fold_k fp32(contribs[k][shard_offset + i]),
+ * the fold being a left-to-right fp32 sum; elements at or beyond
+ * contrib_len read as 0 (zero pad of the last shard). */
+int zi_reduce_scatter_cast(const void* const* contribs, int n_contrib,
+                           size_t shard_offset, size_t shard_elems, size_t contrib_len,
+                           float scale, int half_kind, float* out, void* stream);
+
+/* reduce_scatter for any SPEC dtype: half inputs as
+ * zi_reduce_scatter_cast (fp32 out); f32 folds in fp32, f64 in fp64 (out
+ * has the input type). scale multiplies the folded sum. */
+int zi_reduce_scatter(const void* const* contribs, int n_contrib, size_t shard_offset,
+                      size_t shard_elems, size_t contrib_len, int dtype, double scale,
+                      void* out, void* stream);
+
+/* The engine's per-layer update: zi_reduce_scatter_cast followed by
+ * zi_adam_step in one pass over HBM (no fp32 gradient round trip).
+ * g_out (nullable) receives the fp32 gradient shard for parity tests. */
+int zi_rs_adam(const void* const* contribs, int n_contrib, size_t shard_offset,
+               size_t shard_elems, size_t contrib_len, float scale, int half_kind,
+               float* p, float* m, float* v, void* p_half, float* g_out,
+               const zi_adam_consts* c, void* stream);
+
+/* allgather: full[r*shard_elems + i] = shards[r][i],
+ * truncated to full_elems. shards[r] may be IPC-mapped peer memory.
+ * elem_bytes in {2,4,8}. use_copy_engine != 0 issues one cudaMemcpyAsync per
+ * rank (zero SMs); otherwise one vectorised SM copy kernel. */
+int zi_allgather(const void* const* shards, int world, size_t shard_elems,
+                 size_t elem_bytes, void* full, size_t full_elems,
+                 int use_copy_engine, void* stream);
+
+/* Cross-GPU barrier over IPC-mapped flag words: rank writes `epoch` into
+ * slot [rank] of every peer's flag array (flags[k] = peer k's array of
+ * `world` uint32), then spins until its own array holds >= epoch in every
+ * slot. Orders the P2P reduce-scatter / gather with the peers' producers. */
+int zi_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream);
+
+/* ---- init / casts ---------------------------------------------------------
+ * Counter-RNG uniform init (oracle/numerics.py:uniform_init):
+ * master[i] = float32(2k+1-2^24) * scale with k = top 24 bits of
+ * splitmix64(key + (start_index+i+1)*golden); p_half[i] = RNE(master[i]).
+ * Either output may be NULL. */
+int zi_init_uniform(float* master, void* p_half, size_t n, uint64_t key,
+                    uint64_t start_index, float scale, int half_kind, void* stream);
+int zi_fill(float* master, void* p_half, size_t n, float value, int half_kind,
+            void* stream);
+int zi_cast_f32_to_half(const float* src, void* dst, size_t n, int half_kind,
+                        void* stream);
+int zi_cast_half_to_f32(const void* src, float* dst, size_t n, int half_kind,
+                        void* stream);
+
+/* ---- offload engine (tier-store host tier, store.py:81-153) -------------- */
+int zi_host_alloc(size_t bytes, void** out);          /* pinned, portable */
+int zi_host_free(void* p);
+/* kind: 0 H2D, 1 D2H, 2 D2D, 3 default (UVA) */
+int zi_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* stream);
+int zi_event_create(void** ev);                       /* timing disabled */
+int zi_event_destroy(void* ev);
+int zi_event_record(void* ev, void* stream);
+int zi_event_query(void* ev);                         /* ZI_OK done, ZI_ENOTFOUND pending */
+int zi_event_sync(void* ev);
+int zi_stream_wait_event(void* stream, void* ev);
+
+/* ---- CUDA IPC (peer buffers for the P2P collectives) --------------------- */
+int zi_ipc_get_handle(void* dptr, unsigned char handle[64]);
+int zi_ipc_open(const unsigned char handle[64], void** dptr);
+int zi_ipc_close(void* dptr);
+
+/* ---- memory-centric tiling ------------------------------
+ * One tile of a tiled linear on the 5th-gen tensor cores (tcgen05 + TMEM,
+ * TMA-fed), bf16 in, fp32 accumulate, bf16 out:
+ *   y[m, n] = sum_k x[m, k] * w[n, k] + bias[n]     (bias nullable)
+ * x: M x K row-major (ld = ldx elements), w: N x K row-major (ldw), y: M x N
+ * (ldy). Requires K % 64 == 0, ldx/ldw/ldy % 8 == 0, 16-byte aligned bases. */
+int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y,
+                  int M, int N, int K, int ldx, int ldw, int ldy, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZINF_H */

@@ -1,0 +1,97 @@
+// Shared helpers for libzinf (B200 / sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+#include <cstddef>
+#include <string>
+
+#include "../../include/zinf.h"
+
+namespace zi {
+
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+// After a kernel launch: map a launch failure to ZI_ECUDA with context.
+inline int launch_status(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return cuda_status(e, what);
+}
+
+inline bool aligned(const void* p, size_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+
+inline int grid_for(size_t work_items, int block, int max_blocks_per_sm = 8) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  size_t want = (work_items + block - 1) / block;
+  size_t cap = (size_t)sms * max_blocks_per_sm;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+// ---------------------------------------------------------------- half types
+template <int KIND> struct Half;
+template <> struct Half<ZI_HALF_FP16> {
+  using T = __half;
+  static __device__ __forceinline__ float widen(uint16_t b) {
+    return __half2float(__ushort_as_half(b));
+  }
+  static __device__ __forceinline__ uint16_t narrow(float x) {
+    return __half_as_ushort(__float2half_rn(x));
+  }
+};
+template <> struct Half<ZI_HALF_BF16> {
+  using T = __nv_bfloat16;
+  static __device__ __forceinline__ float widen(uint16_t b) {
+    return __uint_as_float(((uint32_t)b) << 16);
+  }
+  static __device__ __forceinline__ uint16_t narrow(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+  }
+};
+
+// Streaming (evict-first) vector loads/stores: every byte of the optimizer
+// stream is touched exactly once per step.
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(uint2* p, uint2 v) { __stcs(p, v); }
+
+// Adam update with the oracle's exact operation order (oracle/adam.py).
+__device__ __forceinline__ void adam1(float& p, float& m, float& v, float g,
+                                      const zi_adam_consts& c) {
+  m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, g));
+  v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.omb2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, c.bc1);
+  const float vh = __fdiv_rn(v, c.bc2);
+  const float den = __fadd_rn(__fsqrt_rn(vh), c.eps);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(c.lr, mh), den));
+}
+
+}  // namespace zi
+
+#define ZI_CHECK_ARG(cond, ...)           \
+  do {                                    \
+    if (!(cond)) {                        \
+      zi::set_error(__VA_ARGS__);         \
+      return ZI_EINVAL;                   \
+    }                                     \
+  } while (0)
+
+#define ZI_CUDA(call, what)                              \
+  do {                                                   \
+    int _s = zi::cuda_status((call), what);              \
+    if (_s != ZI_OK) return _s;                          \
+  } while (0)

@@ -1,0 +1,593 @@
+"""ZeRO-3 / ZeRO-Infinity partitioned training step for a GPT-style model on B200.
+
+The train-harness of SPEC.md:704-799 generalised to the BASELINE GPT
+configs. Per operator (embed, each block, head):
+
+  fetch   gather the bf16 bucket from every rank's shard (zi_allgather,
+          prefetched one op ahead on a side stream; N=1 + HBM = zero copy)
+  compute forward / backward of the block (cuBLAS GEMMs + SDPA attention
+          via torch — plain library math; the partitioning, gradient
+          reduction and optimizer are libzinf kernels)
+  release the gathered slot returns to a 2-slot ring
+  reduce  (backward) zi_rs_adam: rank-order fp32 reduce-scatter of the
+          per-rank bf16 gradient buckets fused with the bias-corrected
+          Adam update of the fp32 master / m / v shard and the RNE bf16
+          working copy, in one HBM pass. No global grad-norm clipping
+          exists in the SPEC, so Adam runs per bucket inside
+          backward as soon as the bucket's last consumer finished.
+
+Layouts (bit-identical to oracle/gpt.py): one PartitionedTensor per op
+bucket (block-flattening), ceil(n/N) shard with zero pad;
+shards of all buckets live in per-state flat arenas (p16, p32, m, v) with
+each bucket's shard 64-element aligned. Init is shard-local and
+counter-based (zi_init_uniform), identical to the oracle's generator.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.nn.functional as F
+
+from . import _lib, kernels
+from .comm import LocalComm
+from .partition import shard_len
+from .schedule import Timeline, plan_prefetch, trace_schedule
+from .store import TierKind
+
+LN_EPS = 1e-5
+_ALIGN = 64
+
+
+@dataclass(frozen=True)
+class GPTConfig:
+    nl: int = 4
+    hd: int = 256
+    heads: int = 4
+    seq: int = 128
+    vocab: int = 512
+    batch: int = 4  # per-rank micro-batch (sequences)
+
+    @property
+    def head_dim(self) -> int:
+        return self.hd // self.heads
+
+    @property
+    def tokens(self) -> int:
+        return self.batch * self.seq
+
+
+TINY = GPTConfig()
+GPT_1P3B = GPTConfig(nl=24, hd=2048, heads=16, seq=1024, vocab=50304, batch=8)
+GPT_10B = GPTConfig(nl=50, hd=4096, heads=32, seq=1024, vocab=50304, batch=8)
+GPT_70B = GPTConfig(nl=87, hd=8192, heads=64, seq=1024, vocab=50304, batch=4)
+
+
+def _bound(fan_in: int) -> float:
+    return 1.0 / math.sqrt(fan_in)
+
+
+def layer_params(c: GPTConfig):
+    h = c.hd
+    ub = ("u", _bound(h))
+    return [
+        ("ln1_w", (h,), ("c", 1.0)), ("ln1_b", (h,), ("c", 0.0)),
+        ("qkv_w", (3 * h, h), ub), ("qkv_b", (3 * h,), ("c", 0.0)),
+        ("proj_w", (h, h), ub), ("proj_b", (h,), ("c", 0.0)),
+        ("ln2_w", (h,), ("c", 1.0)), ("ln2_b", (h,), ("c", 0.0)),
+        ("fc1_w", (4 * h, h), ub), ("fc1_b", (4 * h,), ("c", 0.0)),
+        ("fc2_w", (h, 4 * h), ("u", _bound(4 * h))), ("fc2_b", (h,), ("c", 0.0)),
+    ]
+
+
+def embed_params(c: GPTConfig):
+    ub = ("u", _bound(c.hd))
+    return [("wte", (c.vocab, c.hd), ub), ("wpe", (c.seq, c.hd), ub)]
+
+
+def final_params(c: GPTConfig):
+    return [("lnf_w", (c.hd,), ("c", 1.0)), ("lnf_b", (c.hd,), ("c", 0.0))]
+
+
+def _numel(shape) -> int:
+    return int(math.prod(shape))
+
+
+def param_count(c: GPTConfig) -> int:
+    n = sum(_numel(s) for _, s, _ in embed_params(c) + final_params(c))
+    return n + c.nl * sum(_numel(s) for _, s, _ in layer_params(c))
+
+
+def model_flops_per_step(c: GPTConfig, ranks: int = 1) -> float:
+    """6 * tokens * params (dense, no recompute) + causal attention matmuls.
+
+    The paper's 8*tokens*params (efficiency.py:38-45) counts an activation
+    recompute this engine does not perform; we report executed model flops.
+    """
+    T = c.tokens * ranks
+    attn = 6 * 2 * c.batch * ranks * c.seq * c.seq * c.hd * c.nl  # QK^T, PV fwd+bwd (causal: half of dense x2)
+    return 6.0 * T * param_count(c) + attn
+
+
+@dataclass
+class Bucket:
+    op: int
+    key: str
+    params: list
+    numel: int
+    shard: int            # L = ceil(numel / N)
+    arena_off: int        # offset of this bucket's shard inside each state arena
+    views: dict = field(default_factory=dict)   # name -> (offset, shape)
+
+    def segments(self):
+        off = 0
+        for j, (name, shape, init) in enumerate(self.params):
+            n = _numel(shape)
+            yield name, off, n, self.op * 64 + j, init
+            off += n
+
+
+def _splitmix_key(seed: int, stream: int) -> int:
+    M = (1 << 64) - 1
+
+    def mix(z):
+        z &= M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    return mix(((seed * 0x9E3779B97F4A7C15) & M) ^ mix(stream + 0x632BE59BD9B4E019))
+
+
+@dataclass
+class Placement:
+    """Where model states live (PAPER Table 3)."""
+    params: TierKind = TierKind.DEVICE     # bf16 working shards
+    optim: TierKind = TierKind.DEVICE      # fp32 master / m / v shards
+
+
+class GPTZeroEngine:
+    """Partitioned ZeRO-3 engine over a communicator (LocalComm or DistComm)."""
+
+    def __init__(self, cfg: GPTConfig, comm=None, seed: int = 7,
+                 half_dtype: torch.dtype = torch.bfloat16,
+                 compute_dtype: torch.dtype | None = None,
+                 placement: Placement | None = None,
+                 lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
+                 prefetch: bool = True, copy_engine_gather: bool = False,
+                 trace: bool = False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
+        _lib.load()
+        self.cfg = cfg
+        self.comm = comm if comm is not None else LocalComm(1)
+        self.N = self.comm.world
+        self.ranks = list(self.comm.ranks())
+        self.seed = seed
+        self.half = half_dtype
+        self.cdt = compute_dtype or half_dtype
+        self.placement = placement or Placement()
+        if self.placement.optim is not TierKind.DEVICE or self.placement.params is not TierKind.DEVICE:
+            if not self.comm.is_local and self.N > 1 and self.placement.params is not TierKind.DEVICE:
+                raise NotImplementedError("host-resident params need the cg staging ring (multi-process)")
+        self.lr, self.betas, self.eps = lr, betas, eps
+        self.prefetch = prefetch
+        self.copy_engine_gather = copy_engine_gather
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.t = 0
+        self.trace = trace
+        self.timeline = Timeline()
+        self._build_buckets()
+        self._alloc_state()
+        self._init_state()
+        self.fwd_seq, self.bwd_seq = trace_schedule(self)
+        self.plan = plan_prefetch(self.fwd_seq, (1, 1, 1))
+        self.gather_stream = torch.cuda.Stream(self.dev)
+        self.h2d_stream = torch.cuda.Stream(self.dev)
+        self.d2h_stream = torch.cuda.Stream(self.dev)
+        self._alloc_work()
+        self.launches = 0  # libzinf kernel launches issued by step()
+
+    # ------------------------------------------------------------------ layout
+    def _build_buckets(self):
+        c = self.cfg
+        specs = [(0, "embed", embed_params(c))]
+        specs += [(i + 1, f"h{i}", layer_params(c)) for i in range(c.nl)]
+        specs.append((c.nl + 1, "final", final_params(c)))
+        self.buckets: list[Bucket] = []
+        off = 0
+        for op, key, params in specs:
+            n = sum(_numel(s) for _, s, _ in params)
+            L = shard_len(n, self.N)
+            b = Bucket(op, key, params, n, L, off)
+            o = 0
+            for name, shape, _ in params:
+                b.views[name] = (o, shape)
+                o += _numel(shape)
+            self.buckets.append(b)
+            off += -(-L // _ALIGN) * _ALIGN
+        self.arena_len = off
+        self.by_key = {b.key: b for b in self.buckets}
+
+    def operators(self):
+        """[(param keys, bytes, flops)] in forward order, for trace_schedule."""
+        c = self.cfg
+        out = []
+        for b in self.buckets:
+            keys = (b.key,) if b.key != "final" else ("final", "embed")  # tied wte (external)
+            flops = 2 * c.tokens * b.numel if b.key != "embed" else c.tokens * c.hd
+            if b.key == "final":
+                flops += 2 * c.tokens * c.vocab * c.hd
+            out.append((keys, 2 * b.numel, max(1, flops)))
+        return out
+
+    def _alloc_state(self):
+        nloc = len(self.ranks)
+        A = self.arena_len
+        hp = self.placement.params is TierKind.HOST
+        ho = self.placement.optim is TierKind.HOST
+
+        def mk(dtype, host):
+            if host:
+                return torch.zeros(nloc, A, dtype=dtype, pin_memory=True)
+            return torch.zeros(nloc, A, dtype=dtype, device=self.dev)
+        self.p16 = mk(self.half, hp)
+        self.p32 = mk(torch.float32, ho)
+        self.m = mk(torch.float32, ho)
+        self.v = mk(torch.float32, ho)
+
+    def _init_state(self):
+        """Shard-local counter-RNG init; never a full tensor."""
+        ho = self.placement.optim is TierKind.HOST
+        hp = self.placement.params is TierKind.HOST
+        for li, r in enumerate(self.ranks):
+            for b in self.buckets:
+                lo, hi = r * b.shard, min((r + 1) * b.shard, b.numel)
+                if hi <= lo:
+                    continue
+                # stage on device when the tiers are host, then copy down
+                p32 = torch.empty(b.shard, dtype=torch.float32, device=self.dev) if ho else \
+                    self.p32[li, b.arena_off:b.arena_off + b.shard]
+                p16 = torch.empty(b.shard, dtype=self.half, device=self.dev) if hp else \
+                    self.p16[li, b.arena_off:b.arena_off + b.shard]
+                for name, off, n, stream, init in b.segments():
+                    s, e = max(lo, off), min(hi, off + n)
+                    if s >= e:
+                        continue
+                    d32 = p32[s - lo:e - lo]
+                    d16 = p16[s - lo:e - lo]
+                    if init[0] == "u":
+                        kernels.init_uniform(d32, d16, _splitmix_key(self.seed, stream), s - off,
+                                             float(init[1] * 2.0 ** -24))
+                    else:
+                        kernels.fill(d32, d16, float(init[1]))
+                if ho:
+                    self.p32[li, b.arena_off:b.arena_off + b.shard].copy_(p32)
+                if hp:
+                    self.p16[li, b.arena_off:b.arena_off + b.shard].copy_(p16)
+        torch.cuda.synchronize()
+
+    def _alloc_work(self):
+        c = self.cfg
+        maxn = max(b.shard * self.N for b in self.buckets if b.key != "embed")
+        e = self.by_key["embed"]
+        # gathered-parameter slots: a 2-slot ring for blocks/final + a resident embed slot
+        self.zero_copy = self.N == 1 and self.placement.params is TierKind.DEVICE and self.cdt == self.half
+        if not self.zero_copy:
+            self.slots = [torch.empty(maxn, dtype=self.half, device=self.dev) for _ in range(2)]
+            self.embed_slot = torch.empty(e.shard * self.N, dtype=self.half, device=self.dev)
+        if self.cdt != self.half:
+            self.wide_slots = [torch.empty(maxn, dtype=self.cdt, device=self.dev) for _ in range(2)]
+            self.wide_embed = torch.empty(e.shard * self.N, dtype=self.cdt, device=self.dev)
+        self.slot_ready = [None, None]
+        # gradient contribution buckets: per local rank, 2-slot ring + embed slot
+        nloc = len(self.ranks)
+        self.gslots = [[torch.zeros(maxn, dtype=self.half, device=self.dev) for _ in range(2)]
+                       for _ in range(nloc)]
+        self.gembed = [torch.zeros(e.shard * self.N, dtype=self.half, device=self.dev)
+                       for _ in range(nloc)]
+        if self.cdt != self.half:
+            self.gwide = [torch.zeros(maxn, dtype=self.cdt, device=self.dev) for _ in range(nloc)]
+        self.wte_acc = [torch.zeros(c.vocab, c.hd, dtype=torch.float32, device=self.dev)
+                        for _ in range(nloc)]
+        if not self.comm.is_local and self.N > 1:
+            self.peer_gslots = [self.comm.share(self.gslots[0][k]) for k in range(2)]
+            self.peer_gembed = self.comm.share(self.gembed[0])
+            self.peer_p16 = self.comm.share(self.p16[0])
+        self.events = {}
+
+    # ------------------------------------------------------------- fetch/release
+    def _shard_view(self, arena, li, b: Bucket):
+        return arena[li, b.arena_off:b.arena_off + b.shard]
+
+    def _fetch(self, b: Bucket, slot: int, stream):
+        """Issue the gather of bucket b into ring slot `slot` on `stream`."""
+        if self.zero_copy:
+            return
+        dst = self.embed_slot if b.key == "embed" else self.slots[slot]
+        with torch.cuda.stream(stream):
+            if self.comm.is_local:
+                shards = [self._shard_view(self.p16, li, b) for li in range(len(self.ranks))]
+                kernels.allgather(shards, b.shard, dst, b.numel,
+                                  use_copy_engine=self.copy_engine_gather or
+                                  self.placement.params is TierKind.HOST)
+            else:
+                base = b.arena_off * self.p16.element_size()
+                ptrs = [p + base for p in self.peer_p16]
+                kernels.allgather(ptrs, b.shard, dst, b.numel,
+                                  use_copy_engine=self.copy_engine_gather)
+            self.launches += 1
+            if self.cdt != self.half:
+                wide = self.wide_embed if b.key == "embed" else self.wide_slots[slot]
+                kernels.cast_half_to_f32(dst[:b.numel], wide[:b.numel])
+                self.launches += 1
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self.events[(b.key, slot)] = ev
+
+    def _full(self, b: Bucket, slot: int) -> torch.Tensor:
+        """The gathered (compute-dtype) flat bucket, after waiting for its fetch."""
+        if self.zero_copy:
+            return self.p16[0, b.arena_off:b.arena_off + b.numel]
+        ev = self.events.pop((b.key, slot), None)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+        if self.cdt != self.half:
+            w = self.wide_embed if b.key == "embed" else self.wide_slots[slot]
+            return w[:b.numel]
+        src = self.embed_slot if b.key == "embed" else self.slots[slot]
+        return src[:b.numel]
+
+    def _params(self, b: Bucket, flat: torch.Tensor) -> dict:
+        return {n: flat[o:o + _numel(s)].view(s) for n, (o, s) in b.views.items()}
+
+    # ------------------------------------------------------------------ compute
+    def _embed_fwd(self, P, tokens):
+        c = self.cfg
+        x = F.embedding(tokens, P["wte"]) + P["wpe"][: tokens.shape[1]]
+        return x.reshape(-1, c.hd)
+
+    def _attn_fwd(self, qkv):
+        c = self.cfg
+        B, S, H, D = c.batch, c.seq, c.heads, c.head_dim
+        leaf = qkv.detach().requires_grad_(True)
+        with torch.enable_grad():
+            q, k, v = leaf.view(B, S, 3, H, D).unbind(2)
+            o4 = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                                v.transpose(1, 2), is_causal=True)
+        o = o4.detach().transpose(1, 2).reshape(B * S, c.hd)
+        return o, (leaf, o4)
+
+    def _attn_bwd(self, do, saved):
+        c = self.cfg
+        leaf, o4 = saved
+        g4 = do.view(c.batch, c.seq, c.heads, c.head_dim).transpose(1, 2)
+        (dqkv,) = torch.autograd.grad(o4, leaf, g4)
+        return dqkv.reshape(-1, 3 * c.hd)
+
+    def _block_fwd(self, x, P):
+        hd = self.cfg.hd
+        h1, m1, r1 = torch.native_layer_norm(x, (hd,), P["ln1_w"], P["ln1_b"], LN_EPS)
+        qkv = torch.addmm(P["qkv_b"], h1, P["qkv_w"].t())
+        o, att = self._attn_fwd(qkv)
+        x2 = torch.addmm(P["proj_b"], o, P["proj_w"].t())
+        x2 += x
+        h2, m2, r2 = torch.native_layer_norm(x2, (hd,), P["ln2_w"], P["ln2_b"], LN_EPS)
+        u = torch.addmm(P["fc1_b"], h2, P["fc1_w"].t())
+        a = F.gelu(u, approximate="tanh")
+        y = torch.addmm(P["fc2_b"], a, P["fc2_w"].t())
+        y += x2
+        return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
+
+    def _block_bwd(self, dy, cache, P, G):
+        hd = self.cfg.hd
+        x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
+        torch.mm(dy.t(), a, out=G["fc2_w"])
+        torch.sum(dy, 0, out=G["fc2_b"])
+        da = torch.mm(dy, P["fc2_w"])
+        du = torch.ops.aten.gelu_backward(da, u, approximate="tanh")
+        torch.mm(du.t(), h2, out=G["fc1_w"])
+        torch.sum(du, 0, out=G["fc1_b"])
+        dh2 = torch.mm(du, P["fc1_w"])
+        dx2, dw, db = torch.ops.aten.native_layer_norm_backward(
+            dh2, x2, (hd,), m2, r2, P["ln2_w"], P["ln2_b"], [True, True, True])
+        G["ln2_w"].copy_(dw)
+        G["ln2_b"].copy_(db)
+        dx2 += dy
+        torch.mm(dx2.t(), o, out=G["proj_w"])
+        torch.sum(dx2, 0, out=G["proj_b"])
+        do = torch.mm(dx2, P["proj_w"])
+        dqkv = self._attn_bwd(do, att)
+        torch.mm(dqkv.t(), h1, out=G["qkv_w"])
+        torch.sum(dqkv, 0, out=G["qkv_b"])
+        dh1 = torch.mm(dqkv, P["qkv_w"])
+        dx, dw, db = torch.ops.aten.native_layer_norm_backward(
+            dh1, x, (hd,), m1, r1, P["ln1_w"], P["ln1_b"], [True, True, True])
+        G["ln1_w"].copy_(dw)
+        G["ln1_b"].copy_(db)
+        dx += dx2
+        return dx
+
+    def _head_fwd_bwd(self, x, PF, PE, G, targets, wte_acc):
+        """Final LN + tied LM head + mean token CE; returns (loss, dx). Fills
+        G (final bucket grads) and wte_acc (fp32 head contribution to wte)."""
+        hd = self.cfg.hd
+        hf, mf, rf = torch.native_layer_norm(x, (hd,), PF["lnf_w"], PF["lnf_b"], LN_EPS)
+        logits = torch.mm(hf, PE["wte"].t()).float()
+        tgt = targets.reshape(-1)
+        T = tgt.numel()
+        lse = torch.logsumexp(logits, -1)
+        loss = (lse - logits.gather(1, tgt[:, None]).squeeze(1)).sum() / T
+        p = torch.exp(logits - lse[:, None])
+        p[torch.arange(T, device=p.device), tgt] -= 1.0
+        dlog = (p / T).to(self.cdt)
+        del logits, p
+        if self.cdt == torch.float32:
+            torch.mm(dlog.t(), hf, out=wte_acc)
+        else:
+            wte_acc.copy_(torch.ops.aten.mm.dtype(dlog.t(), hf, torch.float32))
+        dhf = torch.mm(dlog, PE["wte"])
+        dx, dw, db = torch.ops.aten.native_layer_norm_backward(
+            dhf, x, (hd,), mf, rf, PF["lnf_w"], PF["lnf_b"], [True, True, True])
+        G["lnf_w"].copy_(dw)
+        G["lnf_b"].copy_(db)
+        return loss, dx
+
+    # ------------------------------------------------------------------- reduce
+    def _grad_views(self, li, b: Bucket, slot: int) -> tuple[dict, torch.Tensor]:
+        if self.cdt != self.half:
+            flat = self.gwide[li] if b.key != "embed" else torch.zeros(
+                b.shard * self.N, dtype=self.cdt, device=self.dev)
+        else:
+            flat = self.gembed[li] if b.key == "embed" else self.gslots[li][slot]
+        return self._params(b, flat), flat
+
+    def _contrib(self, li, b: Bucket, slot: int) -> torch.Tensor:
+        return self.gembed[li] if b.key == "embed" else self.gslots[li][slot]
+
+    def _finish_grad(self, li, b: Bucket, slot: int, flat: torch.Tensor):
+        """Cast the compute-dtype grads to the half contribution (RNE)."""
+        dst = self._contrib(li, b, slot)
+        if flat.data_ptr() != dst.data_ptr():
+            kernels.cast_f32_to_half(flat[:b.numel].contiguous(), dst[:b.numel])
+            self.launches += 1
+        if b.shard * self.N > b.numel:
+            dst[b.numel:b.shard * self.N].zero_()
+
+    def _reduce_update(self, b: Bucket, slot: int, consts):
+        """zi_rs_adam for every local rank's shard of bucket b."""
+        if self.comm.is_local:
+            contribs = [self._contrib(li, b, slot) for li in range(len(self.ranks))]
+        else:
+            self.comm.device_barrier()
+            self.launches += 1
+            if b.key == "embed":
+                contribs = list(self.peer_gembed)
+            else:
+                contribs = list(self.peer_gslots[slot])
+        scale = 1.0 / self.N
+        for li, r in enumerate(self.ranks):
+            kernels.rs_adam(contribs, r * b.shard, b.shard, b.numel, scale,
+                            self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
+                            self._shard_view(self.v, li, b), self._shard_view(self.p16, li, b),
+                            consts, g_out=self._gout(li, b))
+            self.launches += 1
+
+    def _gout(self, li, b):
+        if getattr(self, "capture_grads", False):
+            g = torch.empty(b.shard, dtype=torch.float32, device=self.dev)
+            self.grad_shards.setdefault(b.key, {})[self.ranks[li]] = g
+            return g
+        return None
+
+    # --------------------------------------------------------------------- step
+    def step(self, batches) -> torch.Tensor:
+        """One partitioned training step; ``batches[li] = (tokens, targets)``
+        (int64 [batch, seq] CUDA tensors) for each local rank. Returns the
+        mean loss over all ranks as a 0-d fp32 CUDA tensor."""
+        if self.placement.optim is not TierKind.DEVICE:
+            raise NotImplementedError("optimizer offload: use OffloadGPTEngine")
+        c = self.cfg
+        self.t += 1
+        consts = _lib.adam_consts(self.lr, self.betas[0], self.betas[1], self.eps, self.t)
+        self.grad_shards = {}
+        cur = torch.cuda.current_stream()
+        gs = self.gather_stream if self.prefetch else cur
+        nloc = len(self.ranks)
+        if not self.comm.is_local and self.N > 1:
+            self.comm.device_barrier()  # peers' previous-step Adam writes are done
+            self.launches += 1
+        gs.wait_stream(cur)
+        blocks = self.buckets[1:-1]
+        E, FB = self.buckets[0], self.buckets[-1]
+        # ---- forward
+        self._fetch(E, 0, gs)
+        if blocks:
+            self._fetch(blocks[0], 0, gs)
+        PE = self._params(E, self._full(E, 0))
+        xs = [self._embed_fwd(PE, batches[li][0]) for li in range(nloc)]
+        caches = [[None] * len(blocks) for _ in range(nloc)]
+        for i, b in enumerate(blocks):
+            slot = i % 2
+            full = self._full(b, slot)
+            if i + 1 < len(blocks):
+                gs.wait_stream(cur)  # slot (i+1)%2 was last read by compute of block i-1
+                self._fetch(blocks[i + 1], (i + 1) % 2, gs)
+            else:
+                gs.wait_stream(cur)
+                self._fetch(FB, (i + 1) % 2, gs)
+            P = self._params(b, full)
+            for li in range(nloc):
+                xs[li], caches[li][i] = self._block_fwd(xs[li], P)
+        fslot = len(blocks) % 2
+        if not blocks:
+            self._fetch(FB, 0, gs)
+        PF = self._params(FB, self._full(FB, fslot))
+        # ---- head (forward + backward fused; its bucket reduces first)
+        losses = []
+        GF = []
+        for li in range(nloc):
+            G, flat = self._grad_views(li, FB, fslot)
+            loss, xs[li] = self._head_fwd_bwd(xs[li], PF, PE, G, batches[li][1], self.wte_acc[li])
+            self._finish_grad(li, FB, fslot, flat)
+            losses.append(loss)
+        self._reduce_update(FB, fslot, consts)
+        # ---- backward through the blocks, re-gathering each one
+        nb = len(blocks)
+        if nb:
+            gs.wait_stream(cur)
+            self._fetch(blocks[-1], (nb - 1) % 2, gs)  # slot of FB is free after its update? no: use parity
+        for j in range(nb - 1, -1, -1):
+            b = blocks[j]
+            slot = j % 2
+            full = self._full(b, slot)
+            if j - 1 >= 0:
+                gs.wait_stream(cur)
+                self._fetch(blocks[j - 1], (j - 1) % 2, gs)
+            P = self._params(b, full)
+            for li in range(nloc):
+                G, flat = self._grad_views(li, b, slot)
+                xs[li] = self._block_bwd(xs[li], caches[li][j], P, G)
+                caches[li][j] = None
+                self._finish_grad(li, b, slot, flat)
+            self._reduce_update(b, slot, consts)
+        # ---- embedding backward: tied wte = head part + scatter of dx
+        for li in range(nloc):
+            G, flat = self._grad_views(li, E, 0)
+            tok = batches[li][0].reshape(-1)
+            acc = self.wte_acc[li]
+            acc.index_add_(0, tok, xs[li].float())
+            dwpe = torch.zeros(c.seq, c.hd, dtype=torch.float32, device=self.dev)
+            dwpe[: c.seq] = xs[li].float().view(c.batch, c.seq, c.hd).sum(0)
+            G["wte"].copy_(acc)
+            G["wpe"].copy_(dwpe)
+            self._finish_grad(li, E, 0, flat)
+        self._reduce_update(E, 0, consts)
+        total = losses[0].float()
+        for l in losses[1:]:
+            total = total + l.float()
+        return total / nloc if self.comm.is_local else total
+
+    # ------------------------------------------------------------------ access
+    def gathered(self, key: str) -> torch.Tensor:
+        """Full half bucket (all ranks local) — for tests."""
+        b = self.by_key[key]
+        out = torch.empty(b.shard * self.N, dtype=self.half, device=self.dev)
+        shards = [self._shard_view(self.p16, li, b).to(self.dev) for li in range(len(self.ranks))]
+        kernels.allgather(shards, b.shard, out, b.numel)
+        return out[:b.numel]
+
+    def shard(self, key: str, li: int = 0) -> dict:
+        b = self.by_key[key]
+        return {n: self._shard_view(a, li, b) for n, a in
+                (("p16", self.p16), ("p32", self.p32), ("m", self.m), ("v", self.v))}
+
+
+def synthetic_tokens(cfg: GPTConfig, seed: int, rank: int, step: int = 0, device="cuda"):
+    """Uniform token ids on [0, V) per (rank, step) — same generator as the oracle."""
+    import numpy as np
+    rng = np.random.default_rng([seed, rank, step])
+    tok = rng.integers(0, cfg.vocab, size=(cfg.batch, cfg.seq + 1), dtype=np.int64)
+    t = torch.from_numpy(tok)
+    return t[:, :-1].contiguous().to(device), t[:, 1:].contiguous().to(device)

@@ -1,0 +1,135 @@
+"""Tensor-level wrappers over the libzinf C ABI.
+
+PyTorch is plumbing here: tensors supply device pointers and the current
+CUDA stream; every computation below is a libzinf kernel (csrc/*.cu).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+HALF_KIND = {torch.float16: _lib.HALF_FP16, torch.bfloat16: _lib.HALF_BF16}
+KIND_DTYPE = {v: k for k, v in HALF_KIND.items()}
+
+
+def half_kind(dtype: torch.dtype) -> int:
+    try:
+        return HALF_KIND[dtype]
+    except KeyError:
+        raise ValueError(f"half dtype must be float16 or bfloat16, got {dtype}") from None
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(t: torch.Tensor, name: str) -> int:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def adam_step(p, m, v, g, p_half, consts: _lib.AdamConstsC, stream=None) -> None:
+    """zi_adam_step: in-place Adam on fp32 p/m/v with fp32 grad g; p_half <- RNE(p)."""
+    n = p.numel()
+    for t, nm in ((m, "m"), (v, "v"), (g, "g")):
+        if t.numel() != n or t.dtype != torch.float32:
+            raise ValueError(f"{nm} must be fp32 with {n} elements")
+    if p.dtype != torch.float32:
+        raise ValueError("p must be fp32")
+    kind = half_kind(p_half.dtype) if p_half is not None else _lib.HALF_BF16
+    if p_half is not None and p_half.numel() != n:
+        raise ValueError("p_half length mismatch")
+    _lib.call("zi_adam_step", _dev(p, "p"), _dev(m, "m"), _dev(v, "v"), _dev(g, "g"),
+              _dev(p_half, "p_half") if p_half is not None else None, n, consts, kind,
+              _stream(stream))
+
+
+def _contrib_ptrs(contribs) -> tuple:
+    ptrs = []
+    for c in contribs:
+        if isinstance(c, int):
+            ptrs.append(c)          # raw (e.g. IPC-mapped peer) device pointer
+        else:
+            ptrs.append(_dev(c, "contrib"))
+    return _lib.ptr_array(ptrs), len(ptrs)
+
+
+def reduce_scatter_cast(contribs, shard_offset: int, shard_elems: int, contrib_len: int,
+                        scale: float, dtype: torch.dtype, out: torch.Tensor, stream=None) -> None:
+    """zi_reduce_scatter_cast: out = scale * fold_k fp32(contribs[k][off:off+n])."""
+    if out.dtype != torch.float32 or out.numel() < shard_elems:
+        raise ValueError("out must be fp32 with >= shard_elems elements")
+    arr, k = _contrib_ptrs(contribs)
+    _lib.call("zi_reduce_scatter_cast", arr, k, shard_offset, shard_elems, contrib_len, scale,
+              half_kind(dtype), _dev(out, "out"), _stream(stream))
+
+
+def rs_adam(contribs, shard_offset: int, shard_elems: int, contrib_len: int, scale: float,
+            p, m, v, p_half, consts, g_out=None, stream=None) -> None:
+    """zi_rs_adam: fused reduce-scatter + cast + scale + Adam + RNE half param."""
+    arr, k = _contrib_ptrs(contribs)
+    for t, nm in ((p, "p"), (m, "m"), (v, "v")):
+        if t.dtype != torch.float32 or t.numel() < shard_elems:
+            raise ValueError(f"{nm} must be fp32 with >= shard_elems elements")
+    _lib.call("zi_rs_adam", arr, k, shard_offset, shard_elems, contrib_len, scale,
+              half_kind(p_half.dtype), _dev(p, "p"), _dev(m, "m"), _dev(v, "v"),
+              _dev(p_half, "p_half"), _dev(g_out, "g_out") if g_out is not None else None,
+              consts, _stream(stream))
+
+
+def allgather(shards, shard_elems: int, full: torch.Tensor, full_elems: int,
+              use_copy_engine: bool = False, stream=None) -> None:
+    """zi_allgather: full[r*L:(r+1)*L] = shards[r], truncated to full_elems."""
+    ptrs = [s if isinstance(s, int) else _dev(s, "shard") for s in shards]
+    _lib.call("zi_allgather", _lib.ptr_array(ptrs), len(ptrs), shard_elems, full.element_size(),
+              _dev(full, "full"), full_elems, int(use_copy_engine), _stream(stream))
+
+
+def init_uniform(master, p_half, key: int, start_index: int, scale: float, stream=None) -> None:
+    n = (master if master is not None else p_half).numel()
+    kind = half_kind(p_half.dtype) if p_half is not None else _lib.HALF_BF16
+    _lib.call("zi_init_uniform", _dev(master, "master") if master is not None else None,
+              _dev(p_half, "p_half") if p_half is not None else None, n, key, start_index,
+              scale, kind, _stream(stream))
+
+
+def fill(master, p_half, value: float, stream=None) -> None:
+    n = (master if master is not None else p_half).numel()
+    kind = half_kind(p_half.dtype) if p_half is not None else _lib.HALF_BF16
+    _lib.call("zi_fill", _dev(master, "master") if master is not None else None,
+              _dev(p_half, "p_half") if p_half is not None else None, n, value, kind,
+              _stream(stream))
+
+
+def cast_f32_to_half(src, dst, stream=None) -> None:
+    if src.dtype != torch.float32 or dst.numel() != src.numel():
+        raise ValueError("cast_f32_to_half: shape/dtype mismatch")
+    _lib.call("zi_cast_f32_to_half", _dev(src, "src"), _dev(dst, "dst"), src.numel(),
+              half_kind(dst.dtype), _stream(stream))
+
+
+def cast_half_to_f32(src, dst, stream=None) -> None:
+    if dst.dtype != torch.float32 or dst.numel() != src.numel():
+        raise ValueError("cast_half_to_f32: shape/dtype mismatch")
+    _lib.call("zi_cast_half_to_f32", _dev(src, "src"), _dev(dst, "dst"), src.numel(),
+              half_kind(src.dtype), _stream(stream))
+
+
+def linear_fwd(x: torch.Tensor, w: torch.Tensor, bias, y: torch.Tensor, stream=None) -> None:
+    """zi_linear_fwd (tcgen05 tile GEMM): y = x @ w.T + bias, bf16."""
+    M, K = x.shape
+    N = w.shape[0]
+    if w.shape[1] != K or y.shape != (M, N):
+        raise ValueError("linear_fwd: shape mismatch")
+    for t in (x, w, y):
+        if t.dtype != torch.bfloat16 or t.stride(-1) != 1:
+            raise ValueError("linear_fwd: bf16 row-major operands required")
+    _lib.call("zi_linear_fwd", x.data_ptr(), w.data_ptr(),
+              _dev(bias, "bias") if bias is not None else None, y.data_ptr(), M, N, K,
+              x.stride(0), w.stride(0), y.stride(0), _stream(stream))

@@ -1,0 +1,115 @@
+"""The partitioned GPT step on the GPU against the CPU oracle (oracle/gpt.py).
+
+Layout and init are bit-exact; gradients / loss within stated tolerances:
+fp32 compute (half params widened, as the SPEC harness computes)
+within 1e-5 on the loss and 1e-2 relative L2 on gradient shards (bucket
+grads are rounded to half before the reduce-scatter, so summation-order
+differences can flip single half ulps); bf16 compute within 2e-2 on the
+loss and 6e-2 on gradients (SURVEY.md §8c tolerance proposal).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gpt as og
+from oracle import numerics as nx
+from paper_2104_07857_b200 import gpt as eg
+from paper_2104_07857_b200.comm import LocalComm
+
+pytestmark = pytest.mark.gpu
+
+SMALL = eg.GPTConfig(nl=2, hd=128, heads=2, seq=64, vocab=256, batch=2)
+
+
+def ocfg(c):
+    return og.GPTConfig(c.nl, c.hd, c.heads, c.seq, c.vocab, c.batch)
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+
+
+def batches_for(c, world, step=0):
+    return [eg.synthetic_tokens(c, 7, r, step) for r in range(world)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+@pytest.mark.parametrize("half,kind", [(torch.bfloat16, nx.HALF_BF16), (torch.float16, nx.HALF_FP16)])
+def test_init_layout_bit_exact(world, half, kind):
+    eng = eg.GPTZeroEngine(SMALL, LocalComm(world), half_dtype=half)
+    st = og.init_partitioned(ocfg(SMALL), world, half_kind=kind)
+    for key in st.p16:
+        for r in range(world):
+            s = eng.shard(key, r)
+            assert np.array_equal(s["p32"].cpu().numpy(), st.p32[key][r]), (key, r)
+            got = s["p16"].cpu().view(torch.int16).numpy().view(np.uint16)
+            assert np.array_equal(got, st.p16[key][r]), (key, r)
+            assert not s["m"].any() and not s["v"].any()
+        full = eng.gathered(key).cpu().view(torch.int16).numpy().view(np.uint16)
+        want = nx.f32_to_half_bits(og.init_bucket_range(7, eng.by_key[key].op,
+                                                        og.buckets(ocfg(SMALL))[eng.by_key[key].op][2],
+                                                        0, st.full_len[key]), kind)
+        assert np.array_equal(full, want)
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_step_fp32_compute_matches_oracle(world):
+    torch.backends.cuda.matmul.allow_tf32 = False
+    eng = eg.GPTZeroEngine(SMALL, LocalComm(world), half_dtype=torch.float16,
+                           compute_dtype=torch.float32, lr=1e-3)
+    eng.capture_grads = True
+    st = og.init_partitioned(ocfg(SMALL), world, half_kind=nx.HALF_FP16)
+    for step in range(2):
+        bs = batches_for(SMALL, world, step)
+        loss = eng.step(bs).item()
+        oloss, gsh = og.train_step(st, [(t.cpu().numpy(), y.cpu().numpy()) for t, y in bs], lr=1e-3)
+        assert abs(loss - oloss) <= 1e-5 * abs(oloss), (step, loss, oloss)
+        for key in gsh:
+            for r in range(world):
+                g = eng.grad_shards[key][r].cpu().numpy()
+                assert rel(g, gsh[key][r]) < 1e-2, (step, key, r, rel(g, gsh[key][r]))
+        for key in st.p32:
+            for r in range(world):
+                p = eng.shard(key, r)["p32"].cpu().numpy()
+                assert np.abs(p - st.p32[key][r]).max() < 3e-3, key
+
+
+def test_step_bf16_matches_oracle():
+    world = 2
+    eng = eg.GPTZeroEngine(SMALL, LocalComm(world), lr=1e-3)
+    eng.capture_grads = True
+    st = og.init_partitioned(ocfg(SMALL), world, half_kind=nx.HALF_BF16)
+    bs = batches_for(SMALL, world)
+    loss = eng.step(bs).item()
+    oloss, gsh = og.train_step(st, [(t.cpu().numpy(), y.cpu().numpy()) for t, y in bs], lr=1e-3)
+    assert abs(loss - oloss) <= 2e-2 * abs(oloss)
+    for key in gsh:
+        for r in range(world):
+            assert rel(eng.grad_shards[key][r].cpu().numpy(), gsh[key][r]) < 6e-2, key
+
+
+def test_loss_decreases_and_world_sizes_agree():
+    c = SMALL
+    out = {}
+    for world in (1, 2):
+        eng = eg.GPTZeroEngine(c, LocalComm(world), lr=3e-3)
+        # same global data: rank r of world 2 == half of the world-1 batch is not
+        # needed here; compare loss trends only
+        losses = [eng.step(batches_for(c, world, 0)).item() for _ in range(8)]
+        assert losses[-1] < 0.8 * losses[0], losses
+        out[world] = losses
+    assert np.isfinite(out[1]).all() and np.isfinite(out[2]).all()
+
+
+def test_copy_engine_gather_same_result():
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, copy_engine_gather=True, prefetch=False)
+    bs = batches_for(SMALL, 2)
+    la, lb = a.step(bs).item(), b.step(bs).item()
+    assert abs(la - lb) <= 1e-6 * abs(la)   # atomics in attention/embedding bwd
+    for key in a.by_key:
+        torch.testing.assert_close(a.shard(key, 1)["p32"], b.shard(key, 1)["p32"],
+                                   rtol=0, atol=2e-5)
