@@ -34,6 +34,15 @@ def _dev(t: torch.Tensor, name: str) -> int:
     return t.data_ptr()
 
 
+def _dev_or_pinned(t: torch.Tensor, name: str) -> int:
+    """Device pointer of a CUDA tensor or of pinned host memory (UVA-addressable)."""
+    if t.is_cuda:
+        return _dev(t, name)
+    if not t.is_contiguous() or not t.is_pinned():
+        raise ValueError(f"{name} must be a CUDA tensor or contiguous pinned host memory")
+    return t.data_ptr()
+
+
 def adam_step(p, m, v, g, p_half, consts: _lib.AdamConstsC, stream=None) -> None:
     """zi_adam_step: in-place Adam on fp32 p/m/v with fp32 grad g; p_half <- RNE(p)."""
     n = p.numel()
@@ -86,7 +95,7 @@ def rs_adam(contribs, shard_offset: int, shard_elems: int, contrib_len: int, sca
 def allgather(shards, shard_elems: int, full: torch.Tensor, full_elems: int,
               use_copy_engine: bool = False, stream=None) -> None:
     """zi_allgather: full[r*L:(r+1)*L] = shards[r], truncated to full_elems."""
-    ptrs = [s if isinstance(s, int) else _dev(s, "shard") for s in shards]
+    ptrs = [s if isinstance(s, int) else _dev_or_pinned(s, "shard") for s in shards]
     _lib.call("zi_allgather", _lib.ptr_array(ptrs), len(ptrs), shard_elems, full.element_size(),
               _dev(full, "full"), full_elems, int(use_copy_engine), _stream(stream))
 
