@@ -18,7 +18,10 @@ import torch
 from paper_2104_07857_b200 import store as S
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
-REF_SRC = "/root/reference/pkg/src"
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# the reference source (build container) or its unmodified install in baseline/_ref
+REF_SRC = next((p for p in ("/root/reference/pkg/src", os.path.join(_ROOT, "baseline", "_ref"))
+                if os.path.isdir(os.path.join(p, "infinisim"))), "/nonexistent")
 
 
 def load_gold():
