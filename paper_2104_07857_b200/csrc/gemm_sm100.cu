@@ -23,7 +23,7 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;           // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;   // two 256-column fp32 accumulators
 constexpr int THREADS = 192;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 
@@ -121,6 +121,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
 }
 
+// Persistent tile order: groups of GROUP_M m-tiles sweep the n-tiles so the
+// ~148 tiles in flight share A row-blocks and B column-blocks in L2.
+constexpr int GROUP_M = 16;
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
+  const int per_group = GROUP_M * tiles_n;
+  const int g = t / per_group;
+  const int first = g * GROUP_M;
+  const int gm = min(tiles_m - first, GROUP_M);
+  const int r = t % per_group;
+  mt = first + r % gm;
+  nt = r / gm;
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
 linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __nv_bfloat16* __restrict__ bias, __nv_bfloat16* __restrict__ Y, int M,
@@ -132,19 +146,24 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + STAGES;      // [2] accumulator ready
+  uint64_t* tmem_empty = tmem_full + 2;      // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (K + BK - 1) / BK;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int ntiles = tiles_m * tiles_n;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -161,67 +180,94 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], STAGE_BYTES);
-        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
-        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, n0);
+      uint32_t it = 0;  // global k-block counter across tiles (ring position)
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, mt, nt);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], STAGE_BYTES);
+          tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, mt * BM);
+          tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, nt * BN);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      uint32_t it = 0, tcount = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+        const uint32_t acc = tcount & 1;
+        mbar_wait(&tmem_empty[acc], ((tcount >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_bf16(tmem, sdesc_kmajor_sw128(a0 + k * 32), sdesc_kmajor_sw128(b0 + k * 32), idesc,
-                    (kb | k) != 0);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d, sdesc_kmajor_sw128(a0 + k * 32), sdesc_kmajor_sw128(b0 + k * 32), idesc,
+                      (kb | k) != 0);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tmem_full[acc]);
       }
-      umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
     // epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 (= tile rows)
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int q = warp & 3;
-    const int row = m0 + q * 32 + lane;
     const bool vec_ok = (ldy % 8) == 0 && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+    uint32_t tcount = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+      int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, mt, nt);
+      const uint32_t acc = tcount & 1;
+      mbar_wait(&tmem_full[acc], (tcount >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = mt * BM + q * 32 + lane;
+      const int n0 = nt * BN;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c, r);
-      const int col0 = n0 + c;
-      if (row >= M || col0 >= N) continue;
-      float f[32];
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c, r);
+        const int col0 = n0 + c;
+        if (row >= M || col0 >= N) continue;
+        float f[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = col0 + j;
-        const float b = (bias != nullptr && col < N) ? __bfloat162float(bias[col]) : 0.f;
-        f[j] = __uint_as_float(r[j]) + b;
-      }
-      __nv_bfloat16* dst = Y + (size_t)row * ldy + col0;
-      if (vec_ok && col0 + 32 <= N) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          uint4 v;
-          v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
-          v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
-          v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
-          v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
-          reinterpret_cast<uint4*>(dst)[j] = v;
+        for (int j = 0; j < 32; ++j) {
+          const int col = col0 + j;
+          const float b = (bias != nullptr && col < N) ? __bfloat162float(bias[col]) : 0.f;
+          f[j] = __uint_as_float(r[j]) + b;
         }
-      } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) dst[j] = __float2bfloat16_rn(f[j]);
+        __nv_bfloat16* dst = Y + (size_t)row * ldy + col0;
+        if (vec_ok && col0 + 32 <= N) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 v;
+            v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
+            v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
+            v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
+            v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
+            reinterpret_cast<uint4*>(dst)[j] = v;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < N) dst[j] = __float2bfloat16_rn(f[j]);
+        }
       }
+      // accumulator drained: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc]))
+                     : "memory");
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -289,7 +335,14 @@ extern "C" int zi_linear_fwd(const void* x, const void* w, const void* bias, voi
                                  (int)SMEM_BYTES), "cudaFuncSetAttribute(smem)");
     attr = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  dim3 grid(ntiles < sms ? ntiles : sms);
   linear_fwd_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       ma, mb, static_cast<const __nv_bfloat16*>(bias), static_cast<__nv_bfloat16*>(y), M, N, K,
       ldy);

@@ -76,14 +76,22 @@ class _TileFetcher:
 
     def __init__(self, tl: TiledLinear, store: TierStore, comm, prefetch: bool):
         self.tl, self.store, self.comm, self.prefetch = tl, store, comm, prefetch
-        n = max((p.shard_len * p.world_size for p in tl.parts if p is not None), default=1)
+        n = max((p.shard_len * p.world_size for p in tl.parts
+                 if p is not None and not self._zero_copy(p)), default=1)
         self.slots = [torch.empty(n, dtype=tl.dtype, device=store.device) for _ in range(2)]
         self.stream = torch.cuda.Stream(store.device) if prefetch else None
         self.ready = {}
         self.peak_resident = 0
 
+    def _zero_copy(self, p: PartitionedTensor) -> bool:
+        # one rank holding the whole tile in HBM: the shard *is* the gathered tile
+        return p.world_size == 1 and p.tier is TierKind.DEVICE and \
+            (self.comm is None or self.comm.is_local)
+
     def issue(self, t: int) -> None:
         p: PartitionedTensor = self.tl.parts[t]
+        if self._zero_copy(p):
+            return
         slot = self.slots[t % 2]
         cur = torch.cuda.current_stream()
         if self.stream is None:
@@ -101,7 +109,11 @@ class _TileFetcher:
         if ev is not None:
             torch.cuda.current_stream().wait_event(ev)
         s, e = self.tl.rows[t]
-        flat = self.slots[t % 2]
+        p = self.tl.parts[t]
+        if self._zero_copy(p):
+            flat = self.store.tensor(p.shard_key(0), p.tier)
+        else:
+            flat = self.slots[t % 2]
         live = 2 if self.prefetch else 1
         self.peak_resident = max(self.peak_resident, live * self.tl.tile_bytes(t))
         n = (e - s) * self.tl.in_dim
