@@ -139,6 +139,18 @@ int zi_ipc_close(void* dptr);
 int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y,
                   int M, int N, int K, int ldx, int ldw, int ldy, void* stream);
 
+/* General tcgen05 GEMM behind the tiled linear's forward and backward:
+ *   D[m, n] = sum_k A(m, k) * B(n, k) (+ bias[n]) (+ D[m, n] if accumulate)
+ * A(m, k) = A[m*lda + k] (a_mn_major = 0) or A[k*lda + m] (a_mn_major = 1);
+ * B(n, k) = B[n*ldb + k] or B[k*ldb + n]. bf16 operands, fp32 accumulate;
+ * D is bf16 (d_f32 = 0) or fp32 (d_f32 = 1), row-major with ldd.
+ * Supported (a_mn, b_mn, d_f32, accumulate): (0,0,0,0) forward,
+ * (0,1,0,0) / (0,1,1,0) / (0,1,1,1) input gradient dx = dy W,
+ * (1,1,0,0) / (1,1,1,0) weight gradient dW = dy^T x, (0,0,1,0/1). */
+int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
+            const void* bias, void* D, int d_f32, int accumulate, int ldd,
+            int M, int N, int K, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

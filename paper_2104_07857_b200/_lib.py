@@ -64,6 +64,8 @@ SIGNATURES = {
     "zi_ipc_close": [c_void_p],
     "zi_linear_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                       c_int, c_void_p],
+    "zi_gemm": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
+                c_int, c_int, c_int, c_int, c_void_p],
 }
 _RESTYPE = {"zi_last_error": ctypes.c_char_p}
 

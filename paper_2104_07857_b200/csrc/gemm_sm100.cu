@@ -1,16 +1,24 @@
-// Memory-centric tiling GEMM on the 5th-gen tensor cores (PAPER §5.1.3).
+// Tiled-linear GEMMs on the 5th-gen tensor cores (PAPER §5.1.3).
 //
-// One tile of a tiled linear: y[m, n] = sum_k x[m, k] * w[n, k] + bias[n]
-// (bf16 in, fp32 accumulate in TMEM, bf16 out). Blackwell-native:
-//   * TMA (cp.async.bulk.tensor.2d) stages 128x64 A and 256x64 B tiles into
-//     a 4-deep shared-memory ring with 128-byte swizzle, completion signalled
-//     on mbarriers (expect_tx);
-//   * one elected thread issues tcgen05.mma.cta_group::1.kind::f16
-//     (M=128, N=256, K=16) with smem descriptors, accumulating in TMEM
-//     (256 fp32 columns); tcgen05.commit releases ring slots;
-//   * four epilogue warps drain TMEM with tcgen05.ld.32x32b, add the bias and
-//     store bf16.
-// Warp roles: 0 = TMA producer, 1 = TMEM allocator + MMA issuer, 2..5 = epilogue.
+//   D[m, n] = sum_k A(m, k) * B(n, k)  (+ bias[n])  (+ D if accumulating)
+//
+// A(m, k) is K-major (A[m*lda + k]) or M-major (A[k*lda + m]); B likewise
+// (B[n*ldb + k] or B[k*ldb + n]). That covers a linear's forward
+// y = x W^T + b (both K-major), its input gradient dx = dy W (B N-major) and
+// its weight gradient dW = dy^T x (both MN-major). bf16 operands, fp32
+// accumulation in TMEM, bf16 or fp32 output. Blackwell-native structure:
+//   * persistent CTAs (one per SM), tiles 128 x 256 visited in GROUP_M-row
+//     groups so the tiles in flight share A / B blocks in L2;
+//   * warp 0: TMA producer. cp.async.bulk.tensor.2d fills a 4-stage ring of
+//     128-byte-swizzled A / B tiles (K-major: box 64(k) x rows; MN-major:
+//     boxes of 64(mn) x 64(k)), completion via mbarrier expect_tx;
+//   * warp 1: TMEM allocator + the single MMA-issuing thread:
+//     tcgen05.mma.cta_group::1.kind::f16 M=128 N=256 K=16 from smem
+//     descriptors into one of two 256-column TMEM accumulators;
+//     tcgen05.commit frees ring slots and publishes finished accumulators;
+//   * warps 2..5: epilogue. tcgen05.ld.32x32b drains the accumulator (rows =
+//     TMEM lanes), adds bias / the existing output, stores, and hands the
+//     accumulator back, so the epilogue of tile i overlaps the mainloop of i+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -23,8 +31,10 @@ constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KiB
 constexpr int B_BYTES = BN * BK * 2;           // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 512;   // two 256-column fp32 accumulators
+constexpr int MN_BOX_BYTES = 64 * BK * 2;      // one 64(mn) x 64(k) MN-major box: 8 KiB
+constexpr int TMEM_COLS = 512;                 // two 256-column fp32 accumulators
 constexpr int THREADS = 192;
+constexpr int GROUP_M = 16;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -38,6 +48,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // Wait for the phase with the given parity to complete; traps after ~10 s
@@ -68,23 +82,24 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
-// K-major operand tile written by TMA with 128-byte swizzle: rows of 128 B,
-// 8-row (1024 B) swizzle atoms stacked along M/N. LBO unused (16 B), SBO =
-// 1024 B, descriptor version 1, layout SWIZZLE_128B (2).
-__device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
+// Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B, version 1.
+//  K-major : rows of 128 B (64 k), 8-row atoms -> SBO = 1024 B, LBO unused (16 B).
+//  MN-major: 128 B lines of 64 mn per k-row, 8 k-rows per atom -> SBO = 1024 B
+//            between k-groups, LBO = BK*128 B between 64-wide mn boxes.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr, uint32_t lbo_bytes) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
-  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)(1024 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(m >> 4) << 24);
+// Instruction descriptor, kind::f16: D fp32, A/B bf16; bit 15/16 = A/B MN-major.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -121,10 +136,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
 }
 
-// Persistent tile order: groups of GROUP_M m-tiles sweep the n-tiles so the
-// ~148 tiles in flight share A row-blocks and B column-blocks in L2.
-constexpr int GROUP_M = 16;
-
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
   const int per_group = GROUP_M * tiles_n;
   const int g = t / per_group;
@@ -135,10 +146,24 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nt = r / gm;
 }
 
+// One operand tile (rows = BM or BN, 64 k) into smem at dst.
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int k0, int r0) {
+  if (!MN) {
+    tma_load_2d(dst, map, bar, k0, r0);               // box {64 k, ROWS}
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS / 64; ++j)               // boxes {64 mn, 64 k}
+      tma_load_2d(dst + j * MN_BOX_BYTES, map, bar, r0 + 64 * j, k0);
+  }
+}
+
+template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
 __global__ void __launch_bounds__(THREADS, 1)
-linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const __nv_bfloat16* __restrict__ bias, __nv_bfloat16* __restrict__ Y, int M,
-                  int N, int K, int ldy) {
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __nv_bfloat16* __restrict__ bias, void* __restrict__ Dout, int M, int N, int K,
+            int ldd) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -189,14 +214,18 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], STAGE_BYTES);
-          tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, mt * BM);
-          tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], kb * BK, nt * BN);
+          load_operand<A_MN, BM>(sA + s * A_BYTES, &tmA, &full[s], kb * BK, mt * BM);
+          load_operand<B_MN, BN>(sB + s * B_BYTES, &tmB, &full[s], kb * BK, nt * BN);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      // per 16-deep k step: K-major advances 32 B inside the swizzle atom,
+      // MN-major advances two 8-row k-groups (2 KiB)
+      constexpr uint32_t kstep = 32;
+      constexpr uint32_t kstep_mn = 2 * 1024;
       uint32_t it = 0, tcount = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
         const uint32_t acc = tcount & 1;
@@ -210,9 +239,13 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t a0 = smem_u32(sA + s * A_BYTES), b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(d, sdesc_kmajor_sw128(a0 + k * 32), sdesc_kmajor_sw128(b0 + k * 32), idesc,
-                      (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = A_MN ? sdesc_sw128(a0 + k * kstep_mn, MN_BOX_BYTES)
+                                     : sdesc_sw128(a0 + k * kstep, 16);
+            const uint64_t db = B_MN ? sdesc_sw128(b0 + k * kstep_mn, MN_BOX_BYTES)
+                                     : sdesc_sw128(b0 + k * kstep, 16);
+            umma_bf16(d, da, db, idesc, (kb | k) != 0);
+          }
           umma_commit(&empty[s]);
         }
         umma_commit(&tmem_full[acc]);
@@ -222,7 +255,8 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   } else {
     // epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 (= tile rows)
     const int q = warp & 3;
-    const bool vec_ok = (ldy % 8) == 0 && ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+    constexpr int OB = OUT_F32 ? 4 : 2;
+    const bool vec_ok = (ldd % 8) == 0 && ((reinterpret_cast<uintptr_t>(Dout) & 15) == 0);
     uint32_t tcount = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
       int mt, nt;
@@ -245,29 +279,53 @@ linear_fwd_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
           const float b = (bias != nullptr && col < N) ? __bfloat162float(bias[col]) : 0.f;
           f[j] = __uint_as_float(r[j]) + b;
         }
-        __nv_bfloat16* dst = Y + (size_t)row * ldy + col0;
-        if (vec_ok && col0 + 32 <= N) {
+        uint8_t* dst = static_cast<uint8_t*>(Dout) + ((size_t)row * ldd + col0) * OB;
+        const bool full_vec = vec_ok && col0 + 32 <= N;
+        if (OUT_F32) {
+          float* o = reinterpret_cast<float*>(dst);
+          if (full_vec) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 v;
-            v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
-            v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
-            v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
-            v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
-            reinterpret_cast<uint4*>(dst)[j] = v;
+            for (int j = 0; j < 8; ++j) {
+              float4 v = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+              if (ACCUM) {
+                const float4 o4 = reinterpret_cast<const float4*>(o)[j];
+                v.x += o4.x; v.y += o4.y; v.z += o4.z; v.w += o4.w;
+              }
+              reinterpret_cast<float4*>(o)[j] = v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) o[j] = ACCUM ? o[j] + f[j] : f[j];
           }
         } else {
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dst);
+          if (ACCUM) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < N) dst[j] = __float2bfloat16_rn(f[j]);
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) f[j] += __bfloat162float(o[j]);
+          }
+          if (full_vec) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 v;
+              v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
+              v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
+              v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
+              v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
+              reinterpret_cast<uint4*>(o)[j] = v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) o[j] = __float2bfloat16_rn(f[j]);
+          }
         }
       }
       // accumulator drained: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tmem_empty[acc]))
-                     : "memory");
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -296,12 +354,20 @@ static int get_encoder() {
   return ZI_OK;
 }
 
-// 2-D bf16 K-major tensor map: inner dim K (contiguous), outer dim rows.
-static int make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, int box_rows) {
-  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
+// Operand map. K-major: dims {K, rows}, box {64, box_rows}. MN-major (rows
+// contiguous): dims {rows, K}, box {64, 64}. ld = elements between the
+// starts of consecutive outer-dimension lines.
+static int make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, int box_rows,
+                    bool mn_major) {
+  cuuint64_t dims[2], strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (!mn_major) {
+    dims[0] = (cuuint64_t)K; dims[1] = (cuuint64_t)rows;
+    box[0] = BK; box[1] = (cuuint32_t)box_rows;
+  } else {
+    dims[0] = (cuuint64_t)rows; dims[1] = (cuuint64_t)K;
+    box[0] = 64; box[1] = BK;
+  }
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -313,25 +379,13 @@ static int make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, i
   return ZI_OK;
 }
 
-}  // namespace gemm
-}  // namespace zi
-
-extern "C" int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y, int M, int N,
-                             int K, int ldx, int ldw, int ldy, void* stream) {
-  using namespace zi::gemm;
-  ZI_CHECK_ARG(x && w && y, "zi_linear_fwd: NULL operand");
-  ZI_CHECK_ARG(M > 0 && N > 0 && K > 0, "zi_linear_fwd: empty shape");
-  ZI_CHECK_ARG(ldx % 8 == 0 && ldw % 8 == 0 && ldx >= K && ldw >= K && ldy >= N,
-               "zi_linear_fwd: leading dims must be >= the row length and multiples of 8");
-  ZI_CHECK_ARG(zi::aligned(x, 16) && zi::aligned(w, 16), "zi_linear_fwd: operands must be 16-byte aligned");
-  int st = get_encoder();
-  if (st != ZI_OK) return st;
-  CUtensorMap ma, mb;
-  if ((st = make_map(&ma, x, M, K, ldx, BM)) != ZI_OK) return st;
-  if ((st = make_map(&mb, w, N, K, ldw, BN)) != ZI_OK) return st;
+template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
+static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const void* bias, void* D, int M,
+                  int N, int K, int ldd, cudaStream_t s) {
+  auto kern = gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM>;
   static bool attr = false;
   if (!attr) {
-    ZI_CUDA(cudaFuncSetAttribute(linear_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    ZI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)SMEM_BYTES), "cudaFuncSetAttribute(smem)");
     attr = true;
   }
@@ -342,9 +396,47 @@ extern "C" int zi_linear_fwd(const void* x, const void* w, const void* bias, voi
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  dim3 grid(ntiles < sms ? ntiles : sms);
-  linear_fwd_kernel<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      ma, mb, static_cast<const __nv_bfloat16*>(bias), static_cast<__nv_bfloat16*>(y), M, N, K,
-      ldy);
-  return zi::launch_status("zi_linear_fwd");
+  kern<<<ntiles < sms ? ntiles : sms, THREADS, SMEM_BYTES, s>>>(
+      ma, mb, static_cast<const __nv_bfloat16*>(bias), D, M, N, K, ldd);
+  return launch_status("zi_gemm");
+}
+
+}  // namespace gemm
+}  // namespace zi
+
+extern "C" int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major,
+                       int ldb, const void* bias, void* D, int d_f32, int accumulate, int ldd,
+                       int M, int N, int K, void* stream) {
+  using namespace zi::gemm;
+  ZI_CHECK_ARG(A && B && D, "zi_gemm: NULL operand");
+  ZI_CHECK_ARG(M > 0 && N > 0 && K > 0, "zi_gemm: empty shape");
+  ZI_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "zi_gemm: lda/ldb must be multiples of 8");
+  ZI_CHECK_ARG(lda >= (a_mn_major ? M : K) && ldb >= (b_mn_major ? N : K) && ldd >= N,
+               "zi_gemm: leading dimension smaller than the row length");
+  ZI_CHECK_ARG(zi::aligned(A, 16) && zi::aligned(B, 16), "zi_gemm: operands must be 16-byte aligned");
+  int st = get_encoder();
+  if (st != ZI_OK) return st;
+  CUtensorMap ma, mb;
+  if ((st = make_map(&ma, A, M, K, lda, BM, a_mn_major != 0)) != ZI_OK) return st;
+  if ((st = make_map(&mb, B, N, K, ldb, BN, b_mn_major != 0)) != ZI_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int key = (a_mn_major ? 8 : 0) | (b_mn_major ? 4 : 0) | (d_f32 ? 2 : 0) | (accumulate ? 1 : 0);
+  switch (key) {
+    case 0: return launch<false, false, false, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 4: return launch<false, true, false, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 6: return launch<false, true, true, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 7: return launch<false, true, true, true>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 12: return launch<true, true, false, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 14: return launch<true, true, true, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 2: return launch<false, false, true, false>(ma, mb, bias, D, M, N, K, ldd, s);
+    case 3: return launch<false, false, true, true>(ma, mb, bias, D, M, N, K, ldd, s);
+    default:
+      zi::set_error("zi_gemm: unsupported operand/output combination %d", key);
+      return ZI_EINVAL;
+  }
+}
+
+extern "C" int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y, int M, int N,
+                             int K, int ldx, int ldw, int ldy, void* stream) {
+  return zi_gemm(x, 0, ldx, w, 0, ldw, bias, y, 0, 0, ldy, M, N, K, stream);
 }

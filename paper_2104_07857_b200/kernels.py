@@ -130,6 +130,43 @@ def cast_half_to_f32(src, dst, stream=None) -> None:
               half_kind(src.dtype), _stream(stream))
 
 
+def _operand(t: torch.Tensor, name: str):
+    """(pointer, mn_major, ld) of a 2-D bf16 view seen as (rows, k).
+
+    A row-major view (stride(1) == 1) is K-major with ld = stride(0); a
+    transposed view (stride(0) == 1) is MN-major with ld = stride(1).
+    """
+    if t.dtype != torch.bfloat16 or t.dim() != 2 or not t.is_cuda:
+        raise ValueError(f"{name}: 2-D bf16 CUDA tensor required")
+    if t.stride(1) == 1:
+        return t.data_ptr(), 0, t.stride(0)
+    if t.stride(0) == 1:
+        return t.data_ptr(), 1, t.stride(1)
+    raise ValueError(f"{name}: one dimension must be contiguous")
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, accumulate=False,
+         stream=None) -> torch.Tensor:
+    """zi_gemm: out[m, n] (+)= sum_k a[m, k] * b[n, k] (+ bias[n]) on tcgen05.
+
+    ``a`` is (M, K), ``b`` is (N, K); either may be a transposed view
+    (MN-major). ``out`` is a row-major bf16 or fp32 (M, N) view.
+    """
+    M, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K or out.shape != (M, N) or out.stride(1) != 1:
+        raise ValueError("gemm: shape mismatch or non-row-major output")
+    if out.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("gemm: out must be bf16 or fp32")
+    pa, amn, lda = _operand(a, "a")
+    pb, bmn, ldb = _operand(b, "b")
+    _lib.call("zi_gemm", pa, amn, lda, pb, bmn, ldb,
+              _dev(bias, "bias") if bias is not None else None, out.data_ptr(),
+              int(out.dtype == torch.float32), int(accumulate), out.stride(0), M, N, K,
+              _stream(stream))
+    return out
+
+
 def linear_fwd(x: torch.Tensor, w: torch.Tensor, bias, y: torch.Tensor, stream=None) -> None:
     """zi_linear_fwd (tcgen05 tile GEMM): y = x @ w.T + bias, bf16."""
     M, K = x.shape
