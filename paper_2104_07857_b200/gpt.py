@@ -156,7 +156,7 @@ class GPTZeroEngine:
                  placement: Placement | None = None,
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool = False,
-                 trace: bool = False):
+                 trace: bool = False, offload_chunk: int = 16 << 20):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -172,6 +172,7 @@ class GPTZeroEngine:
             if not self.comm.is_local and self.N > 1 and self.placement.params is not TierKind.DEVICE:
                 raise NotImplementedError("host-resident params need the cg staging ring (multi-process)")
         self.lr, self.betas, self.eps = lr, betas, eps
+        self.offload_chunk = offload_chunk
         self.prefetch = prefetch
         self.copy_engine_gather = copy_engine_gather
         self.dev = torch.device("cuda", torch.cuda.current_device())
@@ -228,9 +229,17 @@ class GPTZeroEngine:
         hp = self.placement.params is TierKind.HOST
         ho = self.placement.optim is TierKind.HOST
 
+        self._pinned = []
+
         def mk(dtype, host):
-            if host:
-                return torch.zeros(nloc, A, dtype=dtype, pin_memory=True)
+            if host:  # exact-size cudaHostAlloc (zi_host_alloc): copy-engine DMA source/target
+                from .store import _PinnedBuffer
+                nbytes = nloc * A * torch.empty(0, dtype=dtype).element_size()
+                buf = _PinnedBuffer(nbytes)
+                self._pinned.append(buf)
+                t = buf.tensor.view(dtype).view(nloc, A)
+                t.zero_()
+                return t
             return torch.zeros(nloc, A, dtype=dtype, device=self.dev)
         self.p16 = mk(self.half, hp)
         self.p32 = mk(torch.float32, ho)
@@ -296,6 +305,17 @@ class GPTZeroEngine:
             self.peer_gembed = self.comm.share(self.gembed[0])
             self.peer_p16 = self.comm.share(self.p16[0])
         self.events = {}
+        # offload engine: double-buffered HBM staging for optimizer-state chunks
+        self.offload = self.placement.optim is TierKind.HOST
+        self.opt_stream = torch.cuda.Stream(self.dev) if self.offload else None
+        self.gfree = {}          # grad slot -> event: optimizer finished reading it
+        if self.offload:
+            C = self.offload_chunk
+            self.stage = [[torch.empty(C, dtype=torch.float32, device=self.dev) for _ in range(3)]
+                          for _ in range(2)]
+            self.stage16 = [torch.empty(C, dtype=self.half, device=self.dev) for _ in range(2)]
+            self.ev_d2h = [None, None]
+            self.offload_bytes = 0
 
     # ------------------------------------------------------------- fetch/release
     def _shard_view(self, arena, li, b: Bucket):
@@ -467,12 +487,82 @@ class GPTZeroEngine:
             else:
                 contribs = list(self.peer_gslots[slot])
         scale = 1.0 / self.N
+        if self.offload:
+            self._reduce_update_offload(b, slot, consts, contribs, scale)
+            return
         for li, r in enumerate(self.ranks):
             kernels.rs_adam(contribs, r * b.shard, b.shard, b.numel, scale,
                             self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
                             self._shard_view(self.v, li, b), self._shard_view(self.p16, li, b),
                             consts, g_out=self._gout(li, b))
             self.launches += 1
+
+    def _reduce_update_offload(self, b: Bucket, slot: int, consts, contribs, scale: float):
+        """Optimizer states in pinned host DRAM (PAPER §5.1.1).
+
+        The shard streams through two HBM staging slots in chunks:
+        H2D(c+1) on the h2d stream || zi_rs_adam(c) on the optimizer stream ||
+        D2H(c-1) on the d2h stream — three engines busy at once, the compute
+        stream never waits on PCIe. The bf16 param shard is updated in place
+        in HBM (or staged back to host when params are offloaded too).
+        """
+        cur = torch.cuda.current_stream()
+        opt, h2d, d2h = self.opt_stream, self.h2d_stream, self.d2h_stream
+        opt.wait_stream(cur)                 # grads of bucket b are complete
+        h2d.wait_stream(d2h)                 # host state of this bucket is settled
+        host_params = self.placement.params is TierKind.HOST
+        C = self.offload_chunk
+        for li, r in enumerate(self.ranks):
+            L = b.shard
+            hp, hm, hv = (self._shard_view(a, li, b) for a in (self.p32, self.m, self.v))
+            p16 = self._shard_view(self.p16, li, b)
+            chunks = [(s, min(C, L - s)) for s in range(0, L, C)]
+            ev_h2d = [None, None]
+
+            def issue(ci):
+                k = ci % 2
+                s, n = chunks[ci]
+                with torch.cuda.stream(h2d):
+                    if self.ev_d2h[k] is not None:
+                        h2d.wait_event(self.ev_d2h[k])   # staging slot drained
+                    for dst, src in zip(self.stage[k], (hp, hm, hv)):
+                        dst[:n].copy_(src[s:s + n], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                ev_h2d[k] = ev
+
+            issue(0)
+            for ci, (s, n) in enumerate(chunks):
+                k = ci % 2
+                if ci + 1 < len(chunks):
+                    issue(ci + 1)
+                sp, sm, sv = (x[:n] for x in self.stage[k])
+                with torch.cuda.stream(opt):
+                    opt.wait_event(ev_h2d[k])
+                    ph = self.stage16[k][:n] if host_params else p16[s:s + n]
+                    kernels.rs_adam(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph, consts)
+                    self.launches += 1
+                    ev_c = torch.cuda.Event()
+                    ev_c.record(opt)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(ev_c)
+                    for dst, src in zip((hp, hm, hv), (sp, sm, sv)):
+                        dst[s:s + n].copy_(src, non_blocking=True)
+                    if host_params:
+                        p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
+                    ev_d = torch.cuda.Event()
+                    ev_d.record(d2h)
+                self.ev_d2h[k] = ev_d
+                self.offload_bytes += 2 * 12 * n + (2 if host_params else 0) * n
+        ev_free = torch.cuda.Event()
+        ev_free.record(opt)
+        self.gfree["embed" if b.key == "embed" else slot] = ev_free
+
+    def _wait_gslot(self, slot) -> None:
+        """Before overwriting a gradient slot: the optimizer stream must be done reading it."""
+        ev = self.gfree.pop(slot, None)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
 
     def _gout(self, li, b):
         if getattr(self, "capture_grads", False):
@@ -486,8 +576,6 @@ class GPTZeroEngine:
         """One partitioned training step; ``batches[li] = (tokens, targets)``
         (int64 [batch, seq] CUDA tensors) for each local rank. Returns the
         mean loss over all ranks as a 0-d fp32 CUDA tensor."""
-        if self.placement.optim is not TierKind.DEVICE:
-            raise NotImplementedError("optimizer offload: use OffloadGPTEngine")
         c = self.cfg
         self.t += 1
         consts = _lib.adam_consts(self.lr, self.betas[0], self.betas[1], self.eps, self.t)
@@ -527,6 +615,7 @@ class GPTZeroEngine:
         # ---- head (forward + backward fused; its bucket reduces first)
         losses = []
         GF = []
+        self._wait_gslot(fslot)
         for li in range(nloc):
             G, flat = self._grad_views(li, FB, fslot)
             loss, xs[li] = self._head_fwd_bwd(xs[li], PF, PE, G, batches[li][1], self.wte_acc[li])
@@ -546,6 +635,7 @@ class GPTZeroEngine:
                 gs.wait_stream(cur)
                 self._fetch(blocks[j - 1], (j - 1) % 2, gs)
             P = self._params(b, full)
+            self._wait_gslot(slot)
             for li in range(nloc):
                 G, flat = self._grad_views(li, b, slot)
                 xs[li] = self._block_bwd(xs[li], caches[li][j], P, G)
@@ -553,6 +643,7 @@ class GPTZeroEngine:
                 self._finish_grad(li, b, slot, flat)
             self._reduce_update(b, slot, consts)
         # ---- embedding backward: tied wte = head part + scatter of dx
+        self._wait_gslot("embed")
         for li in range(nloc):
             G, flat = self._grad_views(li, E, 0)
             tok = batches[li][0].reshape(-1)
@@ -564,6 +655,9 @@ class GPTZeroEngine:
             G["wpe"].copy_(dwpe)
             self._finish_grad(li, E, 0, flat)
         self._reduce_update(E, 0, consts)
+        if self.offload:  # the step ends when the last optimizer chunk is back in host DRAM
+            cur.wait_stream(self.opt_stream)
+            cur.wait_stream(self.d2h_stream)
         total = losses[0].float()
         for l in losses[1:]:
             total = total + l.float()

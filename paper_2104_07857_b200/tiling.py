@@ -171,7 +171,13 @@ def backward_tiled(tl: TiledLinear, x: torch.Tensor, gy: torch.Tensor, store: Ti
             f.issue(order[i + 1])
         s, e = tl.rows[t]
         g = gy[:, s:e]
-        dW[t] = g.t() @ x
+        if x.dtype == torch.bfloat16:
+            # tcgen05: dW_t = g^T x (both operands MN-major), dx += g W_t (fp32 accumulate)
+            dW[t] = kernels.gemm(g.t(), x.t(), torch.empty(e - s, tl.in_dim, dtype=x.dtype,
+                                                           device=x.device))
+            kernels.gemm(g, W_t.t(), dx, accumulate=True)
+        else:
+            dW[t] = g.t() @ x
+            dx += g @ W_t
         db[t] = g.sum(0)
-        dx += (g @ W_t).to(acc_dt)
     return dW, db, dx.to(x.dtype)

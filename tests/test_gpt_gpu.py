@@ -104,6 +104,30 @@ def test_loss_decreases_and_world_sizes_agree():
     assert np.isfinite(out[1]).all() and np.isfinite(out[2]).all()
 
 
+@pytest.mark.parametrize("params_host", [False, True])
+def test_offload_matches_hbm(params_host):
+    """Optimizer states (and optionally bf16 params) in pinned host DRAM, streamed in
+    small chunks through the staging pipeline: same result as all-in-HBM."""
+    from paper_2104_07857_b200.gpt import Placement
+    from paper_2104_07857_b200.store import TierKind
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
+    pl = Placement(params=TierKind.HOST if params_host else TierKind.DEVICE, optim=TierKind.HOST)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007)
+    assert not b.p32.is_cuda and b.p32.is_pinned()
+    for step in range(3):
+        bs = batches_for(SMALL, 2, step)
+        la, lb = a.step(bs).item(), b.step(bs).item()
+        assert abs(la - lb) <= 1e-5 * abs(la), (step, la, lb)
+    torch.cuda.synchronize()
+    for key in a.by_key:
+        for r in range(2):
+            sa, sb = a.shard(key, r), b.shard(key, r)
+            for n in ("p32", "m", "v"):
+                torch.testing.assert_close(sa[n].cpu(), sb[n].cpu(), rtol=0, atol=5e-5)
+            assert (sa["p16"].cpu().float() - sb["p16"].cpu().float()).abs().max() < 1e-2
+    assert b.offload_bytes > 0
+
+
 def test_copy_engine_gather_same_result():
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, copy_engine_gather=True, prefetch=False)

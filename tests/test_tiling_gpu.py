@@ -64,3 +64,10 @@ def test_bf16_tiled_linear_tcgen05(store, tiles):
     ref = x.float() @ W.float().t() + b.float()
     err = (y.float() - ref).abs()
     assert (err <= ref.abs() * 2 ** -7 + 2e-2).all()
+    gy = torch.randn(M, Nout, device="cuda").bfloat16()
+    dW, db, dx = T.backward_tiled(tl, x, gy, store)
+    rW = gy.float().t() @ x.float()
+    rx = gy.float() @ W.float()
+    gw = torch.cat([d for d in dW if d is not None]).float()
+    assert ((gw - rW).abs() <= rW.abs() * 2 ** -7 + M * 2 ** -20).all()
+    assert ((dx.float() - rx).abs() <= rx.abs() * 2 ** -7 + Nout * 2 ** -20).all()
