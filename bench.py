@@ -242,6 +242,13 @@ def run_ours(args):
         e2e_ms = comm.allreduce_max(e2e_ms)
     e2e_tflops = flops * world / (e2e_ms / args.steps / 1e3) / 1e12
 
+    # ---------------- offload leg: fp32 optimizer state in pinned host DRAM
+    offload = None
+    if world == 1 and not args.no_offload:
+        del eng
+        torch.cuda.empty_cache()
+        offload = offload_leg(cfg, args)
+
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -277,6 +284,7 @@ def run_ours(args):
                          "share_of_step": round(rs_share, 4),
                          "traffic": None},
             "clocks": clocks.summary(),
+            "offload": offload,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
@@ -285,8 +293,83 @@ def run_ours(args):
     return 0
 
 
+def host_link_peak(nbytes: int = 1 << 30) -> dict:
+    """Pinned cudaMemcpyAsync H2D, D2H and both at once (copy engines), GB/s."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d: bool, d2h: bool) -> float:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d.copy_(h, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        return 3 * nbytes * (int(h2d) + int(d2h)) / (time.perf_counter() - t0) / 1e9
+    run(True, True)
+    return {"h2d_gbs": round(run(True, False), 1), "d2h_gbs": round(run(False, True), 1),
+            "duplex_gbs": round(run(True, True), 1)}
+
+
+def offload_leg(cfg, args) -> dict:
+    """The 1.3B step with fp32 master/m/v in pinned host memory (ZeRO-Offload placement;
+    per-GPU traffic equals BASELINE config 3's 10B/8 shard), streamed per bucket through
+    the H2D || rs_adam || D2H pipeline during backward."""
+    import torch
+    from paper_2104_07857_b200 import gpt as eg
+    from paper_2104_07857_b200.comm import LocalComm
+    from paper_2104_07857_b200.store import TierKind
+    peak = host_link_peak()
+    eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4,
+                           placement=eg.Placement(TierKind.DEVICE, TierKind.HOST))
+    bs = [eg.synthetic_tokens(cfg, 7, 0, s) for s in range(2)]
+    for w in range(2):
+        eng.step([bs[w % 2]])
+    torch.cuda.synchronize()
+    b0 = eng.offload_bytes
+    steps = max(2, min(args.steps, 5))
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for s in range(steps):
+        eng.step([bs[s % 2]])
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    moved = (eng.offload_bytes - b0) / steps
+    eng.trace = True          # one extra traced step for the overlap Timeline
+    eng.step([bs[0]])
+    tl = eng.timeline()
+    eng.trace = False
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "offload_timeline.csv"), "w") as f:
+        f.write(tl.to_csv())
+    out = {"workload": "GPT-1.3B ZeRO-3 step, fp32 optimizer state (15.8 GB) in pinned host DRAM",
+           "ms_per_step": round(ms, 2),
+           "tflops": round(eg.model_flops_per_step(cfg) / (ms / 1e3) / 1e12, 1),
+           "host_bytes_per_step": int(moved),
+           "host_link_gbs": round(moved / (ms / 1e3) / 1e9, 1),
+           "host_link_peak": peak,
+           "frac_of_duplex_peak": round(moved / (ms / 1e3) / 1e9 / peak["duplex_gbs"], 3),
+           "timeline": {"pcie_busy_s": round(tl.lane_busy_s("pcie"), 4),
+                        "compute_busy_s": round(tl.lane_busy_s("compute"), 4),
+                        "traced_step_s": round(tl.total_s, 4),
+                        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)}}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--no-offload", action="store_true", help="skip the optimizer-offload leg")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)

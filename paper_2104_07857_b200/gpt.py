@@ -178,7 +178,7 @@ class GPTZeroEngine:
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.t = 0
         self.trace = trace
-        self.timeline = Timeline()
+        self._spans, self._t0 = [], None
         self._build_buckets()
         self._alloc_state()
         self._init_state()
@@ -321,12 +321,34 @@ class GPTZeroEngine:
     def _shard_view(self, arena, li, b: Bucket):
         return arena[li, b.arena_off:b.arena_off + b.shard]
 
+    # ------------------------------------------------------------------ tracing
+    def _tmark(self, stream):
+        """Timing event on `stream` (only while tracing)."""
+        if not self.trace:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def _tspan(self, op: int, stage: str, e0, e1) -> None:
+        if e0 is not None and e1 is not None:
+            self._spans.append((op, stage, e0, e1))
+
+    def timeline(self) -> Timeline:
+        """Timeline of the last traced step, seconds from step start."""
+        torch.cuda.synchronize()
+        tl = Timeline()
+        for op, stage, e0, e1 in self._spans:
+            tl.add(op, stage, self._t0.elapsed_time(e0) / 1e3, self._t0.elapsed_time(e1) / 1e3)
+        return tl
+
     def _fetch(self, b: Bucket, slot: int, stream):
         """Issue the gather of bucket b into ring slot `slot` on `stream`."""
         if self.zero_copy:
             return
         dst = self.embed_slot if b.key == "embed" else self.slots[slot]
         with torch.cuda.stream(stream):
+            t0 = self._tmark(stream)
             if self.comm.is_local:
                 shards = [self._shard_view(self.p16, li, b) for li in range(len(self.ranks))]
                 kernels.allgather(shards, b.shard, dst, b.numel,
@@ -342,6 +364,8 @@ class GPTZeroEngine:
                 wide = self.wide_embed if b.key == "embed" else self.wide_slots[slot]
                 kernels.cast_half_to_f32(dst[:b.numel], wide[:b.numel])
                 self.launches += 1
+            self._tspan(b.op, "cg" if self.placement.params is TierKind.HOST else "gg",
+                        t0, self._tmark(stream))
             ev = torch.cuda.Event()
             ev.record(stream)
         self.events[(b.key, slot)] = ev
@@ -509,7 +533,9 @@ class GPTZeroEngine:
         cur = torch.cuda.current_stream()
         opt, h2d, d2h = self.opt_stream, self.h2d_stream, self.d2h_stream
         opt.wait_stream(cur)                 # grads of bucket b are complete
-        h2d.wait_stream(d2h)                 # host state of this bucket is settled
+        # (the host state of this bucket was settled by the previous step's
+        # final D2H: step() orders h2d after it once per step, not per bucket,
+        # so consecutive buckets stream back to back)
         host_params = self.placement.params is TierKind.HOST
         C = self.offload_chunk
         for li, r in enumerate(self.ranks):
@@ -525,8 +551,10 @@ class GPTZeroEngine:
                 with torch.cuda.stream(h2d):
                     if self.ev_d2h[k] is not None:
                         h2d.wait_event(self.ev_d2h[k])   # staging slot drained
+                    t0 = self._tmark(h2d)
                     for dst, src in zip(self.stage[k], (hp, hm, hv)):
                         dst[:n].copy_(src[s:s + n], non_blocking=True)
+                    self._tspan(b.op, "cg", t0, self._tmark(h2d))
                     ev = torch.cuda.Event()
                     ev.record(h2d)
                 ev_h2d[k] = ev
@@ -546,10 +574,12 @@ class GPTZeroEngine:
                     ev_c.record(opt)
                 with torch.cuda.stream(d2h):
                     d2h.wait_event(ev_c)
+                    t0 = self._tmark(d2h)
                     for dst, src in zip((hp, hm, hv), (sp, sm, sv)):
                         dst[s:s + n].copy_(src, non_blocking=True)
                     if host_params:
                         p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
+                    self._tspan(b.op, "grad_offload", t0, self._tmark(d2h))
                     ev_d = torch.cuda.Event()
                     ev_d.record(d2h)
                 self.ev_d2h[k] = ev_d
@@ -586,6 +616,10 @@ class GPTZeroEngine:
         if not self.comm.is_local and self.N > 1:
             self.comm.device_barrier()  # peers' previous-step Adam writes are done
             self.launches += 1
+        if self.offload:
+            self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
+        self._spans = []
+        self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
         E, FB = self.buckets[0], self.buckets[-1]
@@ -606,8 +640,10 @@ class GPTZeroEngine:
                 gs.wait_stream(cur)
                 self._fetch(FB, (i + 1) % 2, gs)
             P = self._params(b, full)
+            c0 = self._tmark(cur)
             for li in range(nloc):
                 xs[li], caches[li][i] = self._block_fwd(xs[li], P)
+            self._tspan(b.op, "compute", c0, self._tmark(cur))
         fslot = len(blocks) % 2
         if not blocks:
             self._fetch(FB, 0, gs)
@@ -616,11 +652,13 @@ class GPTZeroEngine:
         losses = []
         GF = []
         self._wait_gslot(fslot)
+        c0 = self._tmark(cur)
         for li in range(nloc):
             G, flat = self._grad_views(li, FB, fslot)
             loss, xs[li] = self._head_fwd_bwd(xs[li], PF, PE, G, batches[li][1], self.wte_acc[li])
             self._finish_grad(li, FB, fslot, flat)
             losses.append(loss)
+        self._tspan(FB.op, "compute", c0, self._tmark(cur))
         self._reduce_update(FB, fslot, consts)
         # ---- backward through the blocks, re-gathering each one
         nb = len(blocks)
@@ -636,11 +674,13 @@ class GPTZeroEngine:
                 self._fetch(blocks[j - 1], (j - 1) % 2, gs)
             P = self._params(b, full)
             self._wait_gslot(slot)
+            c0 = self._tmark(cur)
             for li in range(nloc):
                 G, flat = self._grad_views(li, b, slot)
                 xs[li] = self._block_bwd(xs[li], caches[li][j], P, G)
                 caches[li][j] = None
                 self._finish_grad(li, b, slot, flat)
+            self._tspan(b.op, "compute", c0, self._tmark(cur))
             self._reduce_update(b, slot, consts)
         # ---- embedding backward: tied wte = head part + scatter of dx
         self._wait_gslot("embed")

@@ -128,6 +128,22 @@ def test_offload_matches_hbm(params_host):
     assert b.offload_bytes > 0
 
 
+def test_traced_timeline():
+    """Real CUDA-event Timeline: gathers overlap compute on their own lane."""
+    from paper_2104_07857_b200.gpt import Placement
+    from paper_2104_07857_b200.store import TierKind
+    eng = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, trace=True,
+                           placement=Placement(TierKind.DEVICE, TierKind.HOST), offload_chunk=5000)
+    eng.step(batches_for(SMALL, 2))
+    tl = eng.timeline()
+    stages = {e[1] for e in tl.events}
+    assert {"compute", "gg", "cg", "grad_offload"} <= stages
+    for op, st, lane, s, e in tl.events:
+        assert e >= s >= 0
+    assert 0.0 <= tl.hidden_fraction() <= 1.0
+    assert tl.to_csv().count("\n") == len(tl.events) + 1
+
+
 def test_copy_engine_gather_same_result():
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, copy_engine_gather=True, prefetch=False)
