@@ -311,10 +311,12 @@ class GPTZeroEngine:
         self.gfree = {}          # grad slot -> event: optimizer finished reading it
         if self.offload:
             C = self.offload_chunk
+            NS = 3  # staging slots: H2D(c+2) || rs_adam(c+1) || D2H(c)
             self.stage = [[torch.empty(C, dtype=torch.float32, device=self.dev) for _ in range(3)]
-                          for _ in range(2)]
-            self.stage16 = [torch.empty(C, dtype=self.half, device=self.dev) for _ in range(2)]
-            self.ev_d2h = [None, None]
+                          for _ in range(NS)]
+            self.stage16 = [torch.empty(C, dtype=self.half, device=self.dev) for _ in range(NS)]
+            self.ev_d2h = [None] * NS
+            self._stage_ctr = 0
             self.offload_bytes = 0
 
     # ------------------------------------------------------------- fetch/release
@@ -538,15 +540,22 @@ class GPTZeroEngine:
         # so consecutive buckets stream back to back)
         host_params = self.placement.params is TierKind.HOST
         C = self.offload_chunk
+        NS = len(self.stage)
         for li, r in enumerate(self.ranks):
             L = b.shard
             hp, hm, hv = (self._shard_view(a, li, b) for a in (self.p32, self.m, self.v))
             p16 = self._shard_view(self.p16, li, b)
-            chunks = [(s, min(C, L - s)) for s in range(0, L, C)]
-            ev_h2d = [None, None]
+            nch = -(-L // C)
+            cs = -(-L // nch)                 # balanced chunks, no runt tail
+            chunks = [(s, min(cs, L - s)) for s in range(0, L, cs)]
+            slots = []                        # staging slot of each chunk (rolling, global)
+            for _ in chunks:
+                slots.append(self._stage_ctr % NS)
+                self._stage_ctr += 1
+            ev_h2d = {}
 
             def issue(ci):
-                k = ci % 2
+                k = slots[ci]
                 s, n = chunks[ci]
                 with torch.cuda.stream(h2d):
                     if self.ev_d2h[k] is not None:
@@ -557,16 +566,17 @@ class GPTZeroEngine:
                     self._tspan(b.op, "cg", t0, self._tmark(h2d))
                     ev = torch.cuda.Event()
                     ev.record(h2d)
-                ev_h2d[k] = ev
+                ev_h2d[ci] = ev
 
-            issue(0)
+            for ci in range(min(NS - 1, len(chunks))):
+                issue(ci)
             for ci, (s, n) in enumerate(chunks):
-                k = ci % 2
-                if ci + 1 < len(chunks):
-                    issue(ci + 1)
+                k = slots[ci]
+                if ci + NS - 1 < len(chunks):
+                    issue(ci + NS - 1)
                 sp, sm, sv = (x[:n] for x in self.stage[k])
                 with torch.cuda.stream(opt):
-                    opt.wait_event(ev_h2d[k])
+                    opt.wait_event(ev_h2d.pop(ci))
                     ph = self.stage16[k][:n] if host_params else p16[s:s + n]
                     kernels.rs_adam(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph, consts)
                     self.launches += 1
