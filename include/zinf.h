@@ -125,7 +125,11 @@ int zi_event_query(void* ev);                         /* ZI_OK done, ZI_ENOTFOUN
 int zi_event_sync(void* ev);
 int zi_stream_wait_event(void* stream, void* ev);
 
-/* ---- CUDA IPC (peer buffers for the P2P collectives) --------------------- */
+/* ---- CUDA IPC (peer buffers for the P2P collectives) ---------------------
+ * Buffers that peers map are plain cudaMalloc allocations (zi_device_alloc)
+ * so the IPC handle names exactly that buffer (offset 0). */
+int zi_device_alloc(size_t bytes, void** out);
+int zi_device_free(void* p);
 int zi_ipc_get_handle(void* dptr, unsigned char handle[64]);
 int zi_ipc_open(const unsigned char handle[64], void** dptr);
 int zi_ipc_close(void* dptr);

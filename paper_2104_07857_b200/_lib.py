@@ -59,6 +59,8 @@ SIGNATURES = {
     "zi_event_query": [c_void_p],
     "zi_event_sync": [c_void_p],
     "zi_stream_wait_event": [c_void_p, c_void_p],
+    "zi_device_alloc": [c_size_t, ctypes.POINTER(c_void_p)],
+    "zi_device_free": [c_void_p],
     "zi_ipc_get_handle": [c_void_p, ctypes.c_char_p],
     "zi_ipc_open": [ctypes.c_char_p, ctypes.POINTER(c_void_p)],
     "zi_ipc_close": [c_void_p],

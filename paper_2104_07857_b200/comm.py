@@ -26,6 +26,38 @@ import torch.distributed as dist
 from . import _lib
 
 
+class _DeviceBuffer:
+    """cudaMalloc'd buffer exposed through __cuda_array_interface__ (freed on collection)."""
+
+    _TYPESTR = {torch.float32: "<f4", torch.float16: "<f2", torch.bfloat16: "<V2",
+                torch.int32: "<i4", torch.float64: "<f8", torch.uint8: "|u1"}
+
+    def __init__(self, nbytes: int):
+        p = ctypes.c_void_p()
+        _lib.call("zi_device_alloc", max(nbytes, 16), ctypes.byref(p))
+        self.ptr = p.value
+        self.nbytes = nbytes
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (self.ptr, False), "version": 3}
+
+    def __del__(self):
+        try:
+            _lib.call("zi_device_free", self.ptr)
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
+
+
+def _ipc_tensor(shape, dtype: torch.dtype) -> torch.Tensor:
+    n = 1
+    for s in shape:
+        n *= s
+    nbytes = n * torch.empty(0, dtype=dtype).element_size()
+    buf = _DeviceBuffer(nbytes)
+    t = torch.as_tensor(buf, device="cuda")[:nbytes].view(dtype).view(*shape)
+    t.zero_()
+    return t
+
+
 class LocalComm:
     """``world`` simulated ranks in one process."""
 
@@ -49,6 +81,9 @@ class LocalComm:
     def allreduce_max(self, x: float) -> float:
         return x
 
+    def alloc(self, shape, dtype: torch.dtype) -> torch.Tensor:
+        return torch.zeros(*shape, dtype=dtype, device="cuda")
+
 
 class DistComm:
     """One process per GPU (torch.distributed); IPC-mapped peer buffers."""
@@ -66,6 +101,7 @@ class DistComm:
         self._flag_ptrs = None
         self._epoch = 0
         self._opened: dict[bytes, int] = {}
+        self._owned: dict[int, int] = {}   # base pointer -> bytes of our shareable buffers
 
     def ranks(self):
         return [self.rank]
@@ -85,32 +121,41 @@ class DistComm:
         return float(t.item())
 
     # -- peer memory -------------------------------------------------------------
+    def alloc(self, shape, dtype: torch.dtype) -> torch.Tensor:
+        """A zeroed CUDA buffer peers can map: its own cudaMalloc (zi_device_alloc),
+        so the IPC handle names exactly this buffer."""
+        t = _ipc_tensor(shape, dtype)
+        self._owned[t.data_ptr()] = t.untyped_storage().nbytes()
+        return t
+
     def share(self, t: torch.Tensor) -> list[int]:
         """Device pointers of every rank's copy of a same-shaped buffer (IPC).
 
-        Collective: every rank calls it with its own buffer. The returned list
-        holds our local pointer at index ``rank`` and IPC mappings elsewhere.
-        The mapping covers the whole allocation; offsets are preserved.
+        Collective: every rank calls it with a view of a buffer from ``alloc``.
+        Returns our own pointer at index ``rank`` and IPC mappings of the
+        peers' buffers (same offset) elsewhere.
         """
         if not t.is_cuda:
             raise ValueError("share() needs a CUDA tensor")
-        st = t.untyped_storage()
-        # torch's caching allocator sub-allocates: the IPC handle names the
-        # underlying cudaMalloc block, so ship our offset inside it as well.
-        _dev, handle, _size, st_off = st._share_cuda_()[:4]
-        info = (bytes(handle), int(st_off) + (t.data_ptr() - st.data_ptr()), os.getpid())
-        infos = self.all_gather_object(info)
+        ptr = t.data_ptr()
+        base = next((b for b, n in self._owned.items() if b <= ptr < b + n), None)
+        if base is None:
+            raise ValueError("share() needs a view of a DistComm.alloc() buffer")
+        h = (ctypes.c_char * 64)()
+        _lib.call("zi_ipc_get_handle", base, h)
+        infos = self.all_gather_object((bytes(h), ptr - base))
         ptrs = []
-        for r, (hb, off, _pid) in enumerate(infos):
+        for r, (hb, off) in enumerate(infos):
             if r == self.rank:
-                ptrs.append(t.data_ptr())
+                ptrs.append(ptr)
                 continue
-            base = self._opened.get(hb)
-            if base is None:  # one mapping per cudaMalloc block and process
+            pbase = self._opened.get(hb)
+            if pbase is None:  # one mapping per peer allocation
+                buf = (ctypes.c_char * 64).from_buffer_copy(hb)
                 p = ctypes.c_void_p()
-                _lib.call("zi_ipc_open", ctypes.create_string_buffer(hb, 64), ctypes.byref(p))
-                base = self._opened[hb] = p.value
-            ptrs.append(base + off)
+                _lib.call("zi_ipc_open", buf, ctypes.byref(p))
+                pbase = self._opened[hb] = p.value
+            ptrs.append(pbase + off)
         return ptrs
 
     def device_barrier(self, stream=None) -> None:
@@ -118,7 +163,7 @@ class DistComm:
         if self.world == 1:
             return
         if self._flags is None:
-            self._flags = torch.zeros(self.world, dtype=torch.int32, device="cuda")
+            self._flags = self.alloc((self.world,), torch.int32)
             self._flag_ptrs = self.share(self._flags)
         self._epoch += 1
         s = stream if stream is not None else torch.cuda.current_stream()

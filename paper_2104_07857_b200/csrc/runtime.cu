@@ -106,6 +106,20 @@ int zi_stream_wait_event(void* stream, void* ev) {
   return ZI_OK;
 }
 
+int zi_device_alloc(size_t bytes, void** out) {
+  ZI_CHECK_ARG(out != nullptr, "zi_device_alloc: out is NULL");
+  *out = nullptr;
+  if (bytes == 0) return ZI_OK;
+  ZI_CUDA(cudaMalloc(out, bytes), "cudaMalloc");
+  return ZI_OK;
+}
+
+int zi_device_free(void* p) {
+  if (!p) return ZI_OK;
+  ZI_CUDA(cudaFree(p), "cudaFree");
+  return ZI_OK;
+}
+
 int zi_ipc_get_handle(void* dptr, unsigned char handle[64]) {
   ZI_CHECK_ARG(dptr && handle, "zi_ipc_get_handle: NULL");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");

@@ -241,7 +241,10 @@ class GPTZeroEngine:
                 t.zero_()
                 return t
             return torch.zeros(nloc, A, dtype=dtype, device=self.dev)
-        self.p16 = mk(self.half, hp)
+        if hp or self.comm.is_local:
+            self.p16 = mk(self.half, hp)
+        else:  # peers gather from it over NVLink: an IPC-shareable allocation
+            self.p16 = self.comm.alloc((nloc, A), self.half)
         self.p32 = mk(torch.float32, ho)
         self.m = mk(torch.float32, ho)
         self.v = mk(torch.float32, ho)
@@ -292,10 +295,10 @@ class GPTZeroEngine:
         self.slot_ready = [None, None]
         # gradient contribution buckets: per local rank, 2-slot ring + embed slot
         nloc = len(self.ranks)
-        self.gslots = [[torch.zeros(maxn, dtype=self.half, device=self.dev) for _ in range(2)]
+        sh = self.comm.alloc  # IPC-shareable when peers read the contributions
+        self.gslots = [[sh((maxn,), self.half) for _ in range(2)]
                        for _ in range(nloc)]
-        self.gembed = [torch.zeros(e.shard * self.N, dtype=self.half, device=self.dev)
-                       for _ in range(nloc)]
+        self.gembed = [sh((e.shard * self.N,), self.half) for _ in range(nloc)]
         if self.cdt != self.half:
             self.gwide = [torch.zeros(maxn, dtype=self.cdt, device=self.dev) for _ in range(nloc)]
         self.wte_acc = [torch.zeros(c.vocab, c.hd, dtype=torch.float32, device=self.dev)
