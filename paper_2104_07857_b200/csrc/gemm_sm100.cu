@@ -21,6 +21,7 @@
 //     accumulator back, so the epilogue of tile i overlaps the mainloop of i+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -82,6 +83,29 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Same load, written to the same smem offset in every CTA of `mask` and
+// completing bytes on each destination CTA's mbarrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
 // Shared-memory matrix descriptor (tcgen05), SWIZZLE_128B, version 1.
 //  K-major : rows of 128 B (64 k), 8-row atoms -> SBO = 1024 B, LBO unused (16 B).
 //  MN-major: 128 B lines of 64 mn per k-row, 8 k-rows per atom -> SBO = 1024 B
@@ -114,6 +138,14 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Commit arriving on the barrier at the same offset in every CTA of `mask`
+// (1-SM MMA + multicast TMA: a ring slot is free once every CTA consumed it).
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
@@ -159,7 +191,24 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
   }
 }
 
-template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
+// Rows [r0, r0 + ROWS) of an operand, multicast to the whole cluster pair.
+template <bool MN, int ROWS>
+__device__ __forceinline__ void load_operand_mc(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int k0, int r0, uint16_t mask) {
+  if (!MN) {
+    tma_load_2d_mc(dst, map, bar, k0, r0, mask);
+  } else {
+#pragma unroll
+    for (int j = 0; j < ROWS / 64; ++j)
+      tma_load_2d_mc(dst + j * MN_BOX_BYTES, map, bar, r0 + 64 * j, k0, mask);
+  }
+}
+
+// CL = CTAs per cluster along M (1 or 2). With CL = 2 the pair computes a
+// 256 x 256 output block: each CTA its own 128 rows of A, while the shared
+// 256-row B tile is loaded half by each CTA and multicast to both — 32 KiB
+// instead of 48 KiB of L2->SM traffic per CTA per k-block.
+template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __nv_bfloat16* __restrict__ bias, void* __restrict__ Dout, int M, int N, int K,
@@ -177,13 +226,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (K + BK - 1) / BK;
-  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
-  const int ntiles = tiles_m * tiles_n;
+  const int tiles_m = (M + BM * CL - 1) / (BM * CL), tiles_n = (N + BN - 1) / BN;
+  const int ntiles = tiles_m * tiles_n;          // cluster tiles
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+  const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+  constexpr uint16_t MASK = (1u << CL) - 1;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // every CTA of the cluster must release the slot
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -200,22 +252,30 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CL > 1) cluster_sync();   // peers' barriers exist before any multicast lands
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t it = 0;  // global k-block counter across tiles (ring position)
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = cid; t < ntiles; t += ncl) {
         int mt, nt;
         tile_coords(t, tiles_m, tiles_n, mt, nt);
+        const int m0 = (mt * CL + (int)crank) * BM;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], STAGE_BYTES);
-          load_operand<A_MN, BM>(sA + s * A_BYTES, &tmA, &full[s], kb * BK, mt * BM);
-          load_operand<B_MN, BN>(sB + s * B_BYTES, &tmB, &full[s], kb * BK, nt * BN);
+          load_operand<A_MN, BM>(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+          if (CL == 1) {
+            load_operand<B_MN, BN>(sB + s * B_BYTES, &tmB, &full[s], kb * BK, nt * BN);
+          } else {
+            constexpr int HB = BN / CL;
+            load_operand_mc<B_MN, HB>(sB + s * B_BYTES + crank * (B_BYTES / CL), &tmB, &full[s],
+                                      kb * BK, nt * BN + (int)crank * HB, MASK);
+          }
         }
       }
     }
@@ -227,7 +287,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       constexpr uint32_t kstep = 32;
       constexpr uint32_t kstep_mn = 2 * 1024;
       uint32_t it = 0, tcount = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+      for (int t = cid; t < ntiles; t += ncl, ++tcount) {
         const uint32_t acc = tcount & 1;
         mbar_wait(&tmem_empty[acc], ((tcount >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -246,7 +306,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                      : sdesc_sw128(b0 + k * kstep, 16);
             umma_bf16(d, da, db, idesc, (kb | k) != 0);
           }
-          umma_commit(&empty[s]);
+          if (CL == 1) umma_commit(&empty[s]);
+          else umma_commit_mc(&empty[s], MASK);
         }
         umma_commit(&tmem_full[acc]);
       }
@@ -258,13 +319,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     constexpr int OB = OUT_F32 ? 4 : 2;
     const bool vec_ok = (ldd % 8) == 0 && ((reinterpret_cast<uintptr_t>(Dout) & 15) == 0);
     uint32_t tcount = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tcount) {
+    for (int t = cid; t < ntiles; t += ncl, ++tcount) {
       int mt, nt;
       tile_coords(t, tiles_m, tiles_n, mt, nt);
       const uint32_t acc = tcount & 1;
       mbar_wait(&tmem_full[acc], (tcount >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int row = mt * BM + q * 32 + lane;
+      const int row = (mt * CL + (int)crank) * BM + q * 32 + lane;
       const int n0 = nt * BN;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -330,6 +391,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (CL > 1) cluster_sync();   // no CTA leaves while its peer may still multicast into it
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -379,25 +441,54 @@ static int make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, i
   return ZI_OK;
 }
 
+// Pair CTAs along M (cluster of 2, multicast B). Measured on B200: correct but
+// 1-5 % slower than unpaired (the two CTAs lock-step on every ring slot and
+// smem per stage stays 48 KiB), so it is opt-in: ZI_GEMM_PAIR=1.
+static inline bool pair_m(int M) {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("ZI_GEMM_PAIR");
+    env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return env == 1 && M > BM;
+}
+
 template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const void* bias, void* D, int M,
                   int N, int K, int ldd, cudaStream_t s) {
-  auto kern = gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM>;
-  static bool attr = false;
-  if (!attr) {
-    ZI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)SMEM_BYTES), "cudaFuncSetAttribute(smem)");
-    attr = true;
-  }
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int ntiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  kern<<<ntiles < sms ? ntiles : sms, THREADS, SMEM_BYTES, s>>>(
-      ma, mb, static_cast<const __nv_bfloat16*>(bias), D, M, N, K, ldd);
+  // pair CTAs along M whenever there are at least two m-tiles
+  const bool pair = pair_m(M);
+  const int CL = pair ? 2 : 1;
+  auto kern = pair ? gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 2>
+                   : gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 1>;
+  static bool attr[2] = {false, false};
+  if (!attr[CL - 1]) {
+    ZI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)SMEM_BYTES), "cudaFuncSetAttribute(smem)");
+    attr[CL - 1] = true;
+  }
+  const int ntiles = ((M + BM * CL - 1) / (BM * CL)) * ((N + BN - 1) / BN);
+  int grid = ntiles * CL < sms ? ntiles * CL : (sms / CL) * CL;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, static_cast<const __nv_bfloat16*>(bias), D, M, N,
+                             K, ldd), "cudaLaunchKernelEx(zi_gemm)");
   return launch_status("zi_gemm");
 }
 
@@ -418,7 +509,9 @@ extern "C" int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, in
   if (st != ZI_OK) return st;
   CUtensorMap ma, mb;
   if ((st = make_map(&ma, A, M, K, lda, BM, a_mn_major != 0)) != ZI_OK) return st;
-  if ((st = make_map(&mb, B, N, K, ldb, BN, b_mn_major != 0)) != ZI_OK) return st;
+  // paired CTAs each load (and multicast) half of the 256-row B tile
+  const int b_box = pair_m(M) ? BN / 2 : BN;
+  if ((st = make_map(&mb, B, N, K, ldb, b_box, b_mn_major != 0)) != ZI_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
   const int key = (a_mn_major ? 8 : 0) | (b_mn_major ? 4 : 0) | (d_f32 ? 2 : 0) | (accumulate ? 1 : 0);
   switch (key) {
