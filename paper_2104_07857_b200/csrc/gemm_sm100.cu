@@ -191,6 +191,64 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
   }
 }
 
+// Epilogue for 32 accumulator columns of one row: + bias, (+ existing D), store.
+template <bool OUT_F32, bool ACCUM>
+__device__ __forceinline__ void store_chunk(const uint32_t* r, int row, int col0, int M, int N,
+                                            const __nv_bfloat16* __restrict__ bias,
+                                            void* __restrict__ Dout, int ldd, bool vec_ok) {
+  if (row >= M || col0 >= N) return;
+  constexpr int OB = OUT_F32 ? 4 : 2;
+  float f[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int col = col0 + j;
+    const float b = (bias != nullptr && col < N) ? __bfloat162float(bias[col]) : 0.f;
+    f[j] = __uint_as_float(r[j]) + b;
+  }
+  uint8_t* dst = static_cast<uint8_t*>(Dout) + ((size_t)row * ldd + col0) * OB;
+  const bool full_vec = vec_ok && col0 + 32 <= N;
+  if (OUT_F32) {
+    float* o = reinterpret_cast<float*>(dst);
+    if (full_vec) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 v = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+        if (ACCUM) {
+          const float4 o4 = reinterpret_cast<const float4*>(o)[j];
+          v.x += o4.x; v.y += o4.y; v.z += o4.z; v.w += o4.w;
+        }
+        reinterpret_cast<float4*>(o)[j] = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) o[j] = ACCUM ? o[j] + f[j] : f[j];
+    }
+  } else {
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dst);
+    if (ACCUM) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) f[j] += __bfloat162float(o[j]);
+    }
+    if (full_vec) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 v;
+        v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
+        v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
+        v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
+        v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
+        reinterpret_cast<uint4*>(o)[j] = v;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < N) o[j] = __float2bfloat16_rn(f[j]);
+    }
+  }
+}
+
 // Rows [r0, r0 + ROWS) of an operand, multicast to the whole cluster pair.
 template <bool MN, int ROWS>
 __device__ __forceinline__ void load_operand_mc(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
@@ -316,7 +374,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   } else {
     // epilogue: warp w owns TMEM lanes 32*(w%4) .. +31 (= tile rows)
     const int q = warp & 3;
-    constexpr int OB = OUT_F32 ? 4 : 2;
     const bool vec_ok = (ldd % 8) == 0 && ((reinterpret_cast<uintptr_t>(Dout) & 15) == 0);
     uint32_t tcount = 0;
     for (int t = cid; t < ntiles; t += ncl, ++tcount) {
@@ -331,57 +388,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c, r);
-        const int col0 = n0 + c;
-        if (row >= M || col0 >= N) continue;
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = col0 + j;
-          const float b = (bias != nullptr && col < N) ? __bfloat162float(bias[col]) : 0.f;
-          f[j] = __uint_as_float(r[j]) + b;
-        }
-        uint8_t* dst = static_cast<uint8_t*>(Dout) + ((size_t)row * ldd + col0) * OB;
-        const bool full_vec = vec_ok && col0 + 32 <= N;
-        if (OUT_F32) {
-          float* o = reinterpret_cast<float*>(dst);
-          if (full_vec) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float4 v = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
-              if (ACCUM) {
-                const float4 o4 = reinterpret_cast<const float4*>(o)[j];
-                v.x += o4.x; v.y += o4.y; v.z += o4.z; v.w += o4.w;
-              }
-              reinterpret_cast<float4*>(o)[j] = v;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) o[j] = ACCUM ? o[j] + f[j] : f[j];
-          }
-        } else {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(dst);
-          if (ACCUM) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) f[j] += __bfloat162float(o[j]);
-          }
-          if (full_vec) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 v;
-              v.x = pack_bf16(f[8 * j + 0], f[8 * j + 1]);
-              v.y = pack_bf16(f[8 * j + 2], f[8 * j + 3]);
-              v.z = pack_bf16(f[8 * j + 4], f[8 * j + 5]);
-              v.w = pack_bf16(f[8 * j + 6], f[8 * j + 7]);
-              reinterpret_cast<uint4*>(o)[j] = v;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) o[j] = __float2bfloat16_rn(f[j]);
-          }
-        }
+        store_chunk<OUT_F32, ACCUM>(r, row, n0 + c, M, N, bias, Dout, ldd, vec_ok);
       }
       // accumulator drained: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -395,6 +402,201 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS) : "memory");
+  }
+}
+
+// ------------------------------------------------------------ 2-SM variant
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 output block with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
+// and its own half (128 rows) of B — 32 KiB per k-block per CTA instead of
+// 48 KiB, so six ring stages fit — and the leader CTA's single thread issues
+// the MMA over both CTAs' shared memory. Each CTA's TMEM holds the fp32
+// accumulators of its 128 rows; each CTA runs its own epilogue.
+//   full[s]   leader only: both CTAs' TMA bytes land here (peer bit cleared)
+//   empty[s]  both CTAs: the leader's commit multicasts the release
+//   tmem_full both CTAs (multicast commit); tmem_empty leader only: 8 arrivals
+//             (4 epilogue warps x 2 CTAs, the peer's remote)
+namespace g2 {
+constexpr int STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BK * 2;        // this CTA's 128 rows of A
+constexpr int B2_BYTES = 128 * BK * 2;        // this CTA's half of the 256-row B tile
+constexpr int STAGE2_BYTES = A2_BYTES + B2_BYTES;
+constexpr size_t SMEM2_BYTES = (size_t)STAGES2 * STAGE2_BYTES + 1024 + 256;
+}  // namespace g2
+
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map,
+                                                uint32_t leader_bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+template <bool MN>
+__device__ __forceinline__ void load_operand_2sm(uint8_t* dst, const CUtensorMap* map,
+                                                 uint32_t leader_bar, int k0, int r0) {
+  if (!MN) {
+    tma_load_2d_2sm(dst, map, leader_bar, k0, r0);       // box {64 k, 128 rows}
+  } else {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)                           // boxes {64 mn, 64 k}
+      tma_load_2d_2sm(dst + j * MN_BOX_BYTES, map, leader_bar, r0 + 64 * j, k0);
+  }
+}
+
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)), "h"((uint16_t)0x3) : "memory");
+}
+
+template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __nv_bfloat16* __restrict__ bias, void* __restrict__ Dout, int M, int N,
+               int K, int ldd) {
+  using namespace g2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES2 * A2_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B2_BYTES);
+  uint64_t* empty = full + STAGES2;
+  uint64_t* tmem_full = empty + STAGES2;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int nk = (K + BK - 1) / BK;
+  const int tiles_m = (M + 255) / 256, tiles_n = (N + BN - 1) / BN;
+  const int ntiles = tiles_m * tiles_n;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tmem_full[a], 1);
+      mbar_init(&tmem_empty[a], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {  // same warp id in both CTAs: a paired 2-SM allocation
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int t = cid; t < ntiles; t += ncl) {
+        int mt, nt;
+        tile_coords(t, tiles_m, tiles_n, mt, nt);
+        const int m0 = mt * 256 + (int)crank * 128;
+        const int nb = nt * BN + (int)crank * 128;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t lbar = map_to_rank(smem_u32(&full[s]), 0);
+          if (leader) mbar_expect_tx(&full[s], 2 * STAGE2_BYTES);
+          load_operand_2sm<A_MN>(sA + s * A2_BYTES, &tmA, lbar, kb * BK, m0);
+          load_operand_2sm<B_MN>(sB + s * B2_BYTES, &tmB, lbar, kb * BK, nb);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN, A_MN, B_MN);
+      constexpr uint32_t kstep = 32, kstep_mn = 2 * 1024;
+      uint32_t it = 0, tcount = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++tcount) {
+        const uint32_t acc = tcount & 1;
+        mbar_wait(&tmem_empty[acc], ((tcount >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES2;
+          const uint32_t ph = (it / STAGES2) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t a0 = smem_u32(sA + s * A2_BYTES), b0 = smem_u32(sB + s * B2_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = A_MN ? sdesc_sw128(a0 + k * kstep_mn, MN_BOX_BYTES)
+                                     : sdesc_sw128(a0 + k * kstep, 16);
+            const uint64_t db = B_MN ? sdesc_sw128(b0 + k * kstep_mn, MN_BOX_BYTES)
+                                     : sdesc_sw128(b0 + k * kstep, 16);
+            umma_bf16_2sm(d, da, db, idesc, (kb | k) != 0);
+          }
+          umma_commit_2sm(&empty[s]);
+        }
+        umma_commit_2sm(&tmem_full[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    const bool vec_ok = (ldd % 8) == 0 && ((reinterpret_cast<uintptr_t>(Dout) & 15) == 0);
+    uint32_t tcount = 0;
+    for (int t = cid; t < ntiles; t += ncl, ++tcount) {
+      int mt, nt;
+      tile_coords(t, tiles_m, tiles_n, mt, nt);
+      const uint32_t acc = tcount & 1;
+      mbar_wait(&tmem_full[acc], (tcount >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row = mt * 256 + (int)crank * 128 + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + acc * BN + ((uint32_t)(q * 32) << 16) + c, r);
+        store_chunk<OUT_F32, ACCUM>(r, row, nt * BN + c, M, N, bias, Dout, ldd, vec_ok);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t rb = map_to_rank(smem_u32(&tmem_empty[acc]), 0);
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb)
+                     : "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(TMEM_COLS) : "memory");
   }
 }
@@ -444,14 +646,20 @@ static int make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, i
 // Pair CTAs along M (cluster of 2, multicast B). Measured on B200: correct but
 // 1-5 % slower than unpaired (the two CTAs lock-step on every ring slot and
 // smem per stage stays 48 KiB), so it is opt-in: ZI_GEMM_PAIR=1.
-static inline bool pair_m(int M) {
-  static int env = -1;
-  if (env < 0) {
-    const char* e = getenv("ZI_GEMM_PAIR");
-    env = (e && e[0] == '1') ? 1 : 0;
+// Kernel choice: MODE_1SM (one CTA per 128x256 tile), MODE_PAIR (1-SM MMAs in
+// a cluster of 2 sharing B by multicast), MODE_2SM (cta_group::2, 256x256 per
+// CTA pair, 6 stages). ZI_GEMM_MODE=1sm|pair|2sm overrides the default.
+enum { MODE_1SM = 0, MODE_PAIR = 1, MODE_2SM = 2 };
+static inline int gemm_mode(int M) {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("ZI_GEMM_MODE");
+    env = !e ? -1 : (e[0] == 'p' ? MODE_PAIR : (e[0] == '2' ? MODE_2SM : MODE_1SM));
   }
-  return env == 1 && M > BM;
+  const int m = env >= 0 ? env : MODE_2SM;
+  return (m != MODE_1SM && M <= BM) ? MODE_1SM : m;
 }
+static inline bool pair_m(int M) { return gemm_mode(M) != MODE_1SM; }
 
 template <bool A_MN, bool B_MN, bool OUT_F32, bool ACCUM>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const void* bias, void* D, int M,
@@ -462,23 +670,24 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const void* bias
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  // pair CTAs along M whenever there are at least two m-tiles
-  const bool pair = pair_m(M);
-  const int CL = pair ? 2 : 1;
-  auto kern = pair ? gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 2>
-                   : gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 1>;
-  static bool attr[2] = {false, false};
-  if (!attr[CL - 1]) {
-    ZI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)SMEM_BYTES), "cudaFuncSetAttribute(smem)");
-    attr[CL - 1] = true;
+  const int mode = gemm_mode(M);
+  const int CL = mode == MODE_1SM ? 1 : 2;
+  auto kern = mode == MODE_2SM ? gemm2sm_kernel<A_MN, B_MN, OUT_F32, ACCUM>
+            : mode == MODE_PAIR ? gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 2>
+                                : gemm_kernel<A_MN, B_MN, OUT_F32, ACCUM, 1>;
+  const size_t smem = mode == MODE_2SM ? g2::SMEM2_BYTES : SMEM_BYTES;
+  static bool attr[3] = {false, false, false};
+  if (!attr[mode]) {
+    ZI_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "cudaFuncSetAttribute(smem)");
+    attr[mode] = true;
   }
   const int ntiles = ((M + BM * CL - 1) / (BM * CL)) * ((N + BN - 1) / BN);
   int grid = ntiles * CL < sms ? ntiles * CL : (sms / CL) * CL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -509,7 +718,7 @@ extern "C" int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, in
   if (st != ZI_OK) return st;
   CUtensorMap ma, mb;
   if ((st = make_map(&ma, A, M, K, lda, BM, a_mn_major != 0)) != ZI_OK) return st;
-  // paired CTAs each load (and multicast) half of the 256-row B tile
+  // paired CTAs each load half of the 256-row B tile (multicast or 2-SM)
   const int b_box = pair_m(M) ? BN / 2 : BN;
   if ((st = make_map(&mb, B, N, K, ldb, b_box, b_mn_major != 0)) != ZI_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
