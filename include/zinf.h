@@ -113,6 +113,29 @@ int zi_cast_f32_to_half(const float* src, void* dst, size_t n, int half_kind,
 int zi_cast_half_to_f32(const void* src, float* dst, size_t n, int half_kind,
                         void* stream);
 
+/* ---- fused block kernels of the GPT step (bf16 activations, fp32 math) ----
+ * Row-wise ops take T rows of H (H in {128, 256, 512, 1024, 2048}); column
+ * reductions are deterministic (fixed-order fold of per-CTA partials in the
+ * caller's fp32 `work` buffer). Gradient outputs are bf16 (RNE of the fp32
+ * sum) or fp32 when *_f32 != 0.
+ *   zi_ln_fwd     y = (x [+ resid] - mean) * rstd * w + b; with resid, also
+ *                 xsum = bf16(x + resid) (residual add fused); mean/rstd per row.
+ *   zi_ln_bwd     dx = rstd * (dy*w - mean(dy*w) - xh * mean(dy*w*xh)) [+ dres];
+ *                 dgamma = sum_rows dy * xh, dbeta = sum_rows dy.
+ *   zi_bias_grad  db = sum_rows dy; with u given, first du = gelu_tanh'(u) * dy
+ *                 (stored to du) and db = sum_rows du.
+ *   zi_softmax_ce in place over T rows of V bf16 logits: loss_rows = lse - l[t],
+ *                 logits <- (softmax - onehot(t)) * scale; *loss = mean(loss_rows). */
+int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const void* b, void* y,
+              float* mean, float* rstd, int T, int H, float eps, void* stream);
+int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
+              const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
+              size_t work_elems, int T, int H, void* stream);
+int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, float* work,
+                 size_t work_elems, int T, int N, void* stream);
+int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T,
+                  int V, float scale, void* stream);
+
 /* ---- offload engine (tier-store host tier, store.py:81-153) -------------- */
 int zi_host_alloc(size_t bytes, void** out);          /* pinned, portable */
 int zi_host_free(void* p);

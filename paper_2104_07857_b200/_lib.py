@@ -50,6 +50,13 @@ SIGNATURES = {
     "zi_fill": [c_void_p, c_void_p, c_size_t, c_float, c_int, c_void_p],
     "zi_cast_f32_to_half": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],
     "zi_cast_half_to_f32": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],
+    "zi_ln_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                  c_int, c_int, c_float, c_void_p],
+    "zi_ln_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                  c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p],
+    "zi_bias_grad": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_int,
+                     c_int, c_void_p],
+    "zi_softmax_ce": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, c_void_p],
     "zi_host_alloc": [c_size_t, ctypes.POINTER(c_void_p)],
     "zi_host_free": [c_void_p],
     "zi_memcpy_async": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],

@@ -1,0 +1,446 @@
+// Fused HBM-bound kernels of the GPT block around the GEMMs (bf16 activations,
+// fp32 math). Each reads its inputs once and writes its outputs once; column
+// reductions (LayerNorm gamma/beta grads, bias grads) are deterministic:
+// per-CTA fp32 partials reduced in a fixed order by zi_colsum_finish.
+//
+//   zi_ln_fwd        y = LN(x) * w + b            (+ x2 = x + r fused residual)
+//   zi_ln_bwd        dx = LN'(dy) (+ dres), partial dgamma / dbeta
+//   zi_bias_grad     partial column sums of dy (bias gradient)
+//   zi_gelu_bwd      du = gelu'(u) * da, partial column sums of du
+//   zi_colsum_finish partials [P x N] -> out[N] (bf16 RNE or fp32), fixed order
+//   zi_softmax_ce    per-row logsumexp, loss, dlogits = (softmax - onehot) * scale
+#include "common.cuh"
+
+namespace zi {
+namespace fused {
+
+__device__ __forceinline__ float bf(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
+__device__ __forceinline__ uint16_t tobf(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+
+template <int N>
+__device__ __forceinline__ void ld_row(const uint16_t* p, float* f) {
+  // N elements (multiple of 4) -> fp32, 8- or 4-element vector loads
+  if constexpr (N % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[i];
+      const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        f[8 * i + 2 * j] = bf(u[j] & 0xFFFF);
+        f[8 * i + 2 * j + 1] = bf(u[j] >> 16);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      const uint2 v = reinterpret_cast<const uint2*>(p)[i];
+      f[4 * i] = bf(v.x & 0xFFFF); f[4 * i + 1] = bf(v.x >> 16);
+      f[4 * i + 2] = bf(v.y & 0xFFFF); f[4 * i + 3] = bf(v.y >> 16);
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void st_row(uint16_t* p, const float* f) {
+  if constexpr (N % 8 == 0) {
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i) {
+      uint4 v;
+      v.x = tobf(f[8 * i]) | ((uint32_t)tobf(f[8 * i + 1]) << 16);
+      v.y = tobf(f[8 * i + 2]) | ((uint32_t)tobf(f[8 * i + 3]) << 16);
+      v.z = tobf(f[8 * i + 4]) | ((uint32_t)tobf(f[8 * i + 5]) << 16);
+      v.w = tobf(f[8 * i + 6]) | ((uint32_t)tobf(f[8 * i + 7]) << 16);
+      reinterpret_cast<uint4*>(p)[i] = v;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) {
+      uint2 v;
+      v.x = tobf(f[4 * i]) | ((uint32_t)tobf(f[4 * i + 1]) << 16);
+      v.y = tobf(f[4 * i + 2]) | ((uint32_t)tobf(f[4 * i + 3]) << 16);
+      reinterpret_cast<uint2*>(p)[i] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Lane l of a warp owns the EPL contiguous columns [l*EPL, (l+1)*EPL) of a row
+// (H = 32 * EPL). One warp per row, rows grid-strided over warps. The row
+// stays in registers; w / b are read per 8-column chunk (L1-resident).
+template <int EPL>
+__global__ void __launch_bounds__(256)
+ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
+              uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
+              const uint16_t* __restrict__ b, uint16_t* __restrict__ y, float* __restrict__ mean,
+              float* __restrict__ rstd, int T, float eps) {
+  constexpr int H = 32 * EPL;
+  constexpr int C = EPL < 8 ? EPL : 8;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < T; row += warps) {
+    float v[EPL];
+    ld_row<EPL>(x + (size_t)row * H + lane * EPL, v);
+    if (r != nullptr) {
+#pragma unroll
+      for (int c = 0; c < EPL; c += C) {
+        float rv[C];
+        ld_row<C>(r + (size_t)row * H + lane * EPL + c, rv);
+#pragma unroll
+        for (int i = 0; i < C; ++i) v[c + i] = __bfloat162float(__float2bfloat16_rn(v[c + i] + rv[i]));
+      }
+      st_row<EPL>(xsum + (size_t)row * H + lane * EPL, v);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) s += v[i];
+    const float mu = warp_sum(s) * (1.0f / H);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) {
+      const float d = v[i] - mu;
+      q += d * d;
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.0f / H) + eps);
+#pragma unroll
+    for (int c = 0; c < EPL; c += C) {
+      float wf[C], bv[C];
+      ld_row<C>(w + lane * EPL + c, wf);
+      ld_row<C>(b + lane * EPL + c, bv);
+#pragma unroll
+      for (int i = 0; i < C; ++i) v[c + i] = (v[c + i] - mu) * rs * wf[i] + bv[i];
+    }
+    st_row<EPL>(y + (size_t)row * H + lane * EPL, v);
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+  }
+}
+
+// dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w,
+// plus dres (residual gradient) if given. Two passes over the row (the second
+// re-reads dy / x from L1): pass 1 forms the row sums and accumulates the
+// per-lane dgamma = sum dy * xh, dbeta = sum dy partials in registers; the
+// CTA's 8 warps are then folded through shared memory into one partial row.
+template <int EPL>
+__global__ void __launch_bounds__(256)
+ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+              const uint16_t* __restrict__ w, const float* __restrict__ mean,
+              const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
+              uint16_t* __restrict__ dx, float* __restrict__ part_g, float* __restrict__ part_b,
+              int T) {
+  constexpr int H = 32 * EPL;
+  constexpr int C = EPL < 8 ? EPL : 8;
+  extern __shared__ float red[];  // [8 warps][2][H]: per-warp gamma / beta partials
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  float* ag = red + (size_t)wid * 2 * H + lane * EPL;   // this lane's columns only
+  float* ab = ag + H;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) ag[i] = ab[i] = 0.f;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + wid; row < T; row += warps) {
+    const uint16_t* gp = dy + (size_t)row * H + lane * EPL;
+    const uint16_t* xp = x + (size_t)row * H + lane * EPL;
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll 2
+    for (int c = 0; c < EPL; c += C) {
+      float g[C], xv[C], wf[C];
+      ld_row<C>(gp + c, g);
+      ld_row<C>(xp + c, xv);
+      ld_row<C>(w + lane * EPL + c, wf);
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const float xh = (xv[i] - mu) * rs;
+        const float d = g[i] * wf[i];
+        ag[c + i] += g[i] * xh;
+        ab[c + i] += g[i];
+        s1 += d;
+        s2 += d * xh;
+      }
+    }
+    const float m1 = warp_sum(s1) * (1.0f / H), m2 = warp_sum(s2) * (1.0f / H);
+#pragma unroll 2
+    for (int c = 0; c < EPL; c += C) {
+      float g[C], xv[C], wf[C], o[C];
+      ld_row<C>(gp + c, g);
+      ld_row<C>(xp + c, xv);
+      ld_row<C>(w + lane * EPL + c, wf);
+#pragma unroll
+      for (int i = 0; i < C; ++i) o[i] = rs * (g[i] * wf[i] - m1 - (xv[i] - mu) * rs * m2);
+      if (dres != nullptr) {
+        float rv[C];
+        ld_row<C>(dres + (size_t)row * H + lane * EPL + c, rv);
+#pragma unroll
+        for (int i = 0; i < C; ++i) o[i] += rv[i];
+      }
+      st_row<C>(dx + (size_t)row * H + lane * EPL + c, o);
+    }
+  }
+  // fold the 8 warps' partials (fixed order) into one gamma / beta row per CTA
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    float tg = 0.f, tb = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      tg += red[(size_t)k * 2 * H + c];
+      tb += red[(size_t)k * 2 * H + H + c];
+    }
+    part_g[(size_t)blockIdx.x * H + c] = tg;
+    part_b[(size_t)blockIdx.x * H + c] = tb;
+  }
+}
+
+// Column partial sums over a chunk of rows: thread owns 8 columns. If GELU,
+// du = gelu_tanh'(u) * da is computed, stored to out, and summed.
+template <bool GELU>
+__global__ void __launch_bounds__(256)
+colsum_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
+              uint16_t* __restrict__ out, float* __restrict__ part, int T, int N, int rows_per) {
+  const int c8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c8 >= N) return;
+  const int r0 = blockIdx.y * rows_per;
+  const int r1 = min(T, r0 + rows_per);
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int row = r0; row < r1; ++row) {
+    float v[8];
+    ld_row<8>(a + (size_t)row * N + c8, v);
+    if (GELU) {
+      float uv[8];
+      ld_row<8>(u + (size_t)row * N + c8, uv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float z = uv[j];
+        const float c = 0.7978845608028654f;
+        const float th = tanhf(c * (z + 0.044715f * z * z * z));
+        const float dg = 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * c * (1.f + 3.f * 0.044715f * z * z);
+        v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * dg));
+      }
+      st_row<8>(out + (size_t)row * N + c8, v);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] += v[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) part[(size_t)blockIdx.y * N + c8 + j] = acc[j];
+}
+
+__global__ void __launch_bounds__(256)
+colsum_finish_kernel(const float* __restrict__ part, int P, int N, void* __restrict__ out,
+                     int out_f32) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float s = 0.f;
+  for (int p = 0; p < P; ++p) s += part[(size_t)p * N + c];
+  if (out_f32) static_cast<float*>(out)[c] = s;
+  else static_cast<uint16_t*>(out)[c] = tobf(s);
+}
+
+// One CTA per row of V logits (bf16, in place): lse, loss_row = lse - l[t],
+// dlogits = (exp(l - lse) - [j == t]) * scale written back as bf16.
+__global__ void __launch_bounds__(512)
+softmax_ce_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ tgt,
+                  float* __restrict__ loss_rows, int V, float scale) {
+  const size_t row = blockIdx.x;
+  uint16_t* L = logits + row * (size_t)V;
+  __shared__ float red_m[16], red_s[16];
+  float m = -INFINITY, s = 0.f;
+  const int V8 = (V % 8 == 0) ? V / 8 : 0;
+  for (int i = threadIdx.x; i < V8; i += blockDim.x) {
+    float f[8];
+    ld_row<8>(L + 8 * i, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (f[j] > m) {
+        s *= __expf(m - f[j]);
+        m = f[j];
+      }
+      s += __expf(f[j] - m);
+    }
+  }
+  for (int i = V8 * 8 + threadIdx.x; i < V; i += blockDim.x) {
+    const float f = bf(L[i]);
+    if (f > m) { s *= __expf(m - f); m = f; }
+    s += __expf(f - m);
+  }
+  // block reduce (m, s)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mm = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+  }
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { red_m[wid] = m; red_s[wid] = s; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    m = lane < nw ? red_m[lane] : -INFINITY;
+    s = lane < nw ? red_s[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      const float mm = fmaxf(m, m2);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mm)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mm));
+      m = mm;
+    }
+    if (lane == 0) { red_m[0] = m; red_s[0] = s; }
+  }
+  __syncthreads();
+  const float lse = red_m[0] + __logf(red_s[0]);
+  const int t = (int)tgt[row];
+  if (threadIdx.x == 0) loss_rows[row] = lse - bf(L[t]);
+  __syncthreads();  // everyone read L[t] before it is overwritten
+  for (int i = threadIdx.x; i < V8; i += blockDim.x) {
+    float f[8];
+    ld_row<8>(L + 8 * i, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int col = 8 * i + j;
+      f[j] = (__expf(f[j] - lse) - (col == t ? 1.f : 0.f)) * scale;
+    }
+    st_row<8>(L + 8 * i, f);
+  }
+  for (int i = V8 * 8 + threadIdx.x; i < V; i += blockDim.x)
+    L[i] = tobf((__expf(bf(L[i]) - lse) - (i == t ? 1.f : 0.f)) * scale);
+}
+
+__global__ void sum_kernel(const float* __restrict__ v, int n, float scale, float* __restrict__ out) {
+  // single block, fixed-order tree: deterministic
+  __shared__ float sm[1024];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sm[0] * scale;
+}
+
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int d = 0;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+  }
+  return sms;
+}
+
+}  // namespace fused
+}  // namespace zi
+
+using namespace zi::fused;
+
+#define EPL_DISPATCH(H, KERNEL, GRID, BLOCK, STREAM, ...)                                 \
+  switch ((H) / 32) {                                                                      \
+    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                     \
+    case 8: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                     \
+    case 16: KERNEL<16><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 32: KERNEL<32><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 64: KERNEL<64><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    default: zi::set_error("LayerNorm: hidden size %d not in {128..2048, power of 2}", H); \
+      return ZI_EINVAL;                                                                    \
+  }
+
+extern "C" {
+
+int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const void* b, void* y,
+              float* mean, float* rstd, int T, int H, float eps, void* stream) {
+  ZI_CHECK_ARG(x && w && b && y && mean && rstd && T > 0, "zi_ln_fwd: bad arguments");
+  ZI_CHECK_ARG(!resid || xsum, "zi_ln_fwd: resid needs xsum");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = (T + 7) / 8 < sm_count() * 4 ? (T + 7) / 8 : sm_count() * 4;
+  EPL_DISPATCH(H, ln_fwd_kernel, grid, 256, s, (const uint16_t*)x, (const uint16_t*)resid,
+               (uint16_t*)xsum, (const uint16_t*)w, (const uint16_t*)b, (uint16_t*)y, mean, rstd,
+               T, eps);
+  return zi::launch_status("zi_ln_fwd");
+}
+
+int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
+              const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
+              size_t work_elems, int T, int H, void* stream) {
+  ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = (T + 7) / 8 < sm_count() ? (T + 7) / 8 : sm_count();
+  ZI_CHECK_ARG(work_elems >= 2 * (size_t)grid * H, "zi_ln_bwd: work needs %zu floats",
+               2 * (size_t)grid * H);
+  float* pg = work;
+  float* pb = work + (size_t)grid * H;
+  const size_t smem = (size_t)8 * 2 * H * sizeof(float);
+  switch (H / 32) {
+#define ZI_LNB(E)                                                                              \
+    case E: {                                                                                  \
+      static bool a = false;                                                                   \
+      if (!a) {                                                                                \
+        ZI_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<E>,                                         \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),  \
+                "cudaFuncSetAttribute(ln_bwd)");                                              \
+        a = true;                                                                              \
+      }                                                                                        \
+      ln_bwd_kernel<E><<<grid, 256, smem, s>>>((const uint16_t*)dy, (const uint16_t*)x,        \
+                                               (const uint16_t*)w, mean, rstd,                 \
+                                               (const uint16_t*)dres, (uint16_t*)dx, pg, pb, T); \
+      break;                                                                                   \
+    }
+    ZI_LNB(4) ZI_LNB(8) ZI_LNB(16) ZI_LNB(32) ZI_LNB(64)
+#undef ZI_LNB
+    default:
+      zi::set_error("zi_ln_bwd: hidden size %d not in {128..2048, power of 2}", H);
+      return ZI_EINVAL;
+  }
+  int st = zi::launch_status("zi_ln_bwd");
+  if (st) return st;
+  colsum_finish_kernel<<<(H + 255) / 256, 256, 0, s>>>(pg, grid, H, dgamma, grads_f32);
+  colsum_finish_kernel<<<(H + 255) / 256, 256, 0, s>>>(pb, grid, H, dbeta, grads_f32);
+  return zi::launch_status("zi_ln_bwd(finish)");
+}
+
+int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, float* work,
+                 size_t work_elems, int T, int N, void* stream) {
+  ZI_CHECK_ARG(dy && db && work && T > 0 && N > 0 && N % 8 == 0, "zi_bias_grad: bad arguments");
+  ZI_CHECK_ARG(!u || du, "zi_bias_grad: gelu backward needs du");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int cblocks = (N / 8 + 255) / 256;
+  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
+  if (chunks > T) chunks = T;
+  const int rows_per = (T + chunks - 1) / chunks;
+  chunks = (T + rows_per - 1) / rows_per;
+  ZI_CHECK_ARG(work_elems >= (size_t)chunks * N, "zi_bias_grad: work needs %zu floats",
+               (size_t)chunks * N);
+  dim3 grid(cblocks, chunks);
+  if (u)
+    colsum_kernel<true><<<grid, 256, 0, s>>>((const uint16_t*)dy, (const uint16_t*)u,
+                                             (uint16_t*)du, work, T, N, rows_per);
+  else
+    colsum_kernel<false><<<grid, 256, 0, s>>>((const uint16_t*)dy, nullptr, nullptr, work, T, N,
+                                              rows_per);
+  int st = zi::launch_status("zi_bias_grad");
+  if (st) return st;
+  colsum_finish_kernel<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, db, db_f32);
+  return zi::launch_status("zi_bias_grad(finish)");
+}
+
+int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T, int V,
+                  float scale, void* stream) {
+  ZI_CHECK_ARG(logits && targets && loss_rows && loss && T > 0 && V > 0, "zi_softmax_ce: bad args");
+  cudaStream_t s = (cudaStream_t)stream;
+  softmax_ce_kernel<<<T, 512, 0, s>>>((uint16_t*)logits, targets, loss_rows, V, scale);
+  int st = zi::launch_status("zi_softmax_ce");
+  if (st) return st;
+  sum_kernel<<<1, 1024, 0, s>>>(loss_rows, T, 1.0f / T, loss);
+  return zi::launch_status("zi_softmax_ce(sum)");
+}
+
+}  // extern "C"

@@ -167,6 +167,66 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, accumul
     return out
 
 
+class Workspace:
+    """fp32 scratch for the deterministic column reductions (per-CTA partials)."""
+
+    def __init__(self, elems: int = 4 << 20, device="cuda"):
+        self.t = torch.empty(elems, dtype=torch.float32, device=device)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def __len__(self):
+        return self.t.numel()
+
+
+def _bf16_2d(t: torch.Tensor, name: str):
+    if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{name}: contiguous bf16 CUDA tensor required")
+    return t.data_ptr()
+
+
+def ln_fwd(x, w, b, y, mean, rstd, eps=1e-5, resid=None, xsum=None, stream=None) -> None:
+    """zi_ln_fwd: y = LN(x [+ resid]) * w + b; xsum = x + resid when fused."""
+    H = x.shape[-1]
+    T = x.numel() // H
+    _lib.call("zi_ln_fwd", _bf16_2d(x, "x"), _bf16_2d(resid, "resid") if resid is not None else None,
+              _bf16_2d(xsum, "xsum") if xsum is not None else None, _bf16_2d(w, "w"),
+              _bf16_2d(b, "b"), _bf16_2d(y, "y"), _dev(mean, "mean"), _dev(rstd, "rstd"), T, H,
+              eps, _stream(stream))
+
+
+def ln_bwd(dy, x, w, mean, rstd, dx, dgamma, dbeta, ws: Workspace, dres=None, stream=None) -> None:
+    """zi_ln_bwd: dx (+ dres), dgamma, dbeta (bf16 or fp32 outputs)."""
+    H = x.shape[-1]
+    T = x.numel() // H
+    f32 = int(dgamma.dtype == torch.float32)
+    _lib.call("zi_ln_bwd", _bf16_2d(dy, "dy"), _bf16_2d(x, "x"), _bf16_2d(w, "w"),
+              _dev(mean, "mean"), _dev(rstd, "rstd"),
+              _bf16_2d(dres, "dres") if dres is not None else None, _bf16_2d(dx, "dx"),
+              dgamma.data_ptr(), dbeta.data_ptr(), f32, ws.ptr, len(ws), T, H, _stream(stream))
+
+
+def bias_grad(dy, db, ws: Workspace, u=None, du=None, stream=None) -> None:
+    """zi_bias_grad: db = column sums of dy; with u: du = gelu'(u) * dy and db = sums of du."""
+    N = dy.shape[-1]
+    T = dy.numel() // N
+    _lib.call("zi_bias_grad", _bf16_2d(dy, "dy"), _bf16_2d(u, "u") if u is not None else None,
+              _bf16_2d(du, "du") if du is not None else None, db.data_ptr(),
+              int(db.dtype == torch.float32), ws.ptr, len(ws), T, N, _stream(stream))
+
+
+def softmax_ce(logits, targets, loss_rows, loss, scale: float, stream=None) -> None:
+    """zi_softmax_ce: in place (softmax - onehot) * scale; loss_rows and the mean loss."""
+    V = logits.shape[-1]
+    T = logits.numel() // V
+    if targets.dtype != torch.int64 or targets.numel() != T:
+        raise ValueError("targets must be int64 with one entry per row")
+    _lib.call("zi_softmax_ce", _bf16_2d(logits, "logits"), _dev(targets, "targets"),
+              _dev(loss_rows, "loss_rows"), _dev(loss, "loss"), T, V, scale, _stream(stream))
+
+
 def linear_fwd(x: torch.Tensor, w: torch.Tensor, bias, y: torch.Tensor, stream=None) -> None:
     """zi_linear_fwd (tcgen05 tile GEMM): y = x @ w.T + bias, bf16."""
     M, K = x.shape

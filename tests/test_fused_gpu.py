@@ -1,0 +1,107 @@
+"""Fused block kernels (csrc/fused.cu) against plain fp32 PyTorch references.
+
+Tolerances: outputs are bf16, so 2^-7 relative (one bf16 ulp) plus an
+absolute term scaled by the reduction length; column reductions are
+additionally checked for determinism (bit-identical on re-run).
+"""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2104_07857_b200 import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+
+def close(a, b, rtol=2 ** -7, atol=1e-2):
+    a, b = a.float(), b.float()
+    bad = ((a - b).abs() > rtol * b.abs() + atol).sum().item()
+    assert bad == 0, f"{bad} mismatches, max err {(a - b).abs().max().item()}"
+
+
+@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048), (513, 1024)])
+@pytest.mark.parametrize("resid", [False, True])
+def test_ln_fwd(T, H, resid):
+    g = torch.Generator(device="cuda").manual_seed(T + H)
+    x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    r = torch.randn(T, H, device="cuda", generator=g).bfloat16() if resid else None
+    w = (1 + 0.1 * torch.randn(H, device="cuda", generator=g)).bfloat16()
+    b = (0.1 * torch.randn(H, device="cuda", generator=g)).bfloat16()
+    y = torch.empty_like(x)
+    xs = torch.empty_like(x) if resid else None
+    mean = torch.empty(T, device="cuda")
+    rstd = torch.empty(T, device="cuda")
+    K.ln_fwd(x, w, b, y, mean, rstd, resid=r, xsum=xs)
+    xin = (x.float() + r.float()).bfloat16() if resid else x
+    if resid:
+        assert torch.equal(xs, xin)
+    ref = F.layer_norm(xin.float(), (H,), w.float(), b.float(), 1e-5)
+    close(y, ref)
+    torch.testing.assert_close(mean, xin.float().mean(-1), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048)])
+@pytest.mark.parametrize("dres", [False, True])
+def test_ln_bwd(T, H, dres):
+    g = torch.Generator(device="cuda").manual_seed(T * H)
+    x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    w = (1 + 0.1 * torch.randn(H, device="cuda", generator=g)).bfloat16()
+    b = torch.zeros(H, device="cuda").bfloat16()
+    dy = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    dr = torch.randn(T, H, device="cuda", generator=g).bfloat16() if dres else None
+    y = torch.empty_like(x)
+    mean = torch.empty(T, device="cuda")
+    rstd = torch.empty(T, device="cuda")
+    K.ln_fwd(x, w, b, y, mean, rstd)
+    dx = torch.empty_like(x)
+    dg = torch.empty(H, device="cuda", dtype=torch.float32)
+    db = torch.empty(H, device="cuda", dtype=torch.float32)
+    ws = K.Workspace()
+    K.ln_bwd(dy, x, w, mean, rstd, dx, dg, db, ws, dres=dr)
+    xr = x.float().requires_grad_(True)
+    wr = w.float().requires_grad_(True)
+    br = b.float().requires_grad_(True)
+    F.layer_norm(xr, (H,), wr, br, 1e-5).backward(dy.float())
+    ref_dx = xr.grad + (dr.float() if dres else 0)
+    close(dx, ref_dx, atol=2e-2)
+    torch.testing.assert_close(dg, wr.grad, rtol=1e-3, atol=1e-3 * T ** 0.5)
+    torch.testing.assert_close(db, br.grad, rtol=1e-3, atol=1e-3 * T ** 0.5)
+    dg2 = torch.empty_like(dg)
+    db2 = torch.empty_like(db)
+    K.ln_bwd(dy, x, w, mean, rstd, dx, dg2, db2, ws, dres=dr)
+    assert torch.equal(dg, dg2) and torch.equal(db, db2)   # deterministic
+
+
+@pytest.mark.parametrize("T,N", [(8192, 8192), (1000, 2048), (7, 24)])
+@pytest.mark.parametrize("gelu", [False, True])
+def test_bias_grad(T, N, gelu):
+    g = torch.Generator(device="cuda").manual_seed(N)
+    dy = torch.randn(T, N, device="cuda", generator=g).bfloat16()
+    u = torch.randn(T, N, device="cuda", generator=g).bfloat16() if gelu else None
+    du = torch.empty_like(dy) if gelu else None
+    db = torch.empty(N, device="cuda").bfloat16()
+    K.bias_grad(dy, db, K.Workspace(), u=u, du=du)
+    if gelu:
+        ref_du = torch.ops.aten.gelu_backward(dy.float(), u.float(), approximate="tanh")
+        close(du, ref_du, atol=1e-2)
+        ref = du.float().sum(0)
+    else:
+        ref = dy.float().sum(0)
+    close(db, ref, atol=1e-3 * T ** 0.5)
+
+
+@pytest.mark.parametrize("T,V", [(8, 512), (1024, 50304), (33, 1000)])
+def test_softmax_ce(T, V):
+    g = torch.Generator(device="cuda").manual_seed(V)
+    logits = (3 * torch.randn(T, V, device="cuda", generator=g)).bfloat16()
+    tgt = torch.randint(0, V, (T,), device="cuda", generator=g)
+    lf = logits.float().requires_grad_(True)
+    ref_loss = F.cross_entropy(lf, tgt)
+    ref_loss.backward()
+    work = logits.clone()
+    rows = torch.empty(T, device="cuda")
+    loss = torch.empty((), device="cuda")
+    K.softmax_ce(work, tgt, rows, loss, 1.0 / T)
+    assert abs(loss.item() - ref_loss.item()) < 1e-4 * max(1.0, abs(ref_loss.item()))
+    close(work, lf.grad, atol=1e-4 / T)
