@@ -156,7 +156,7 @@ class GPTZeroEngine:
                  placement: Placement | None = None,
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool = False,
-                 trace: bool = False, offload_chunk: int = 16 << 20):
+                 trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -189,6 +189,11 @@ class GPTZeroEngine:
         self.d2h_stream = torch.cuda.Stream(self.dev)
         self._alloc_work()
         self.launches = 0  # libzinf kernel launches issued by step()
+        # bf16 path: LayerNorm / bias-grad / GELU-bwd / softmax-CE on libzinf kernels
+        self.fused = (self.cdt == torch.bfloat16 and cfg.hd in (128, 256, 512, 1024, 2048)
+                      and fused)
+        self.ws = kernels.Workspace(max(4 << 20, 2 * 148 * cfg.hd, 600 * 4 * cfg.hd),
+                                    device=self.dev) if self.fused else None
 
     # ------------------------------------------------------------------ layout
     def _build_buckets(self):
@@ -415,7 +420,21 @@ class GPTZeroEngine:
         (dqkv,) = torch.autograd.grad(o4, leaf, g4)
         return dqkv.reshape(-1, 3 * c.hd)
 
+    def _ln(self, x, w, b, resid=None):
+        """libzinf LayerNorm (bf16); with resid the residual add is fused: returns
+        (x + resid, y, mean, rstd)."""
+        T = x.shape[0]
+        y = torch.empty_like(x)
+        mean = torch.empty(T, dtype=torch.float32, device=x.device)
+        rstd = torch.empty(T, dtype=torch.float32, device=x.device)
+        xs = torch.empty_like(x) if resid is not None else None
+        kernels.ln_fwd(x, w, b, y, mean, rstd, LN_EPS, resid=resid, xsum=xs)
+        self.launches += 1
+        return xs, y, mean, rstd
+
     def _block_fwd(self, x, P):
+        if self.fused:
+            return self._block_fwd_fused(x, P)
         hd = self.cfg.hd
         h1, m1, r1 = torch.native_layer_norm(x, (hd,), P["ln1_w"], P["ln1_b"], LN_EPS)
         qkv = torch.addmm(P["qkv_b"], h1, P["qkv_w"].t())
@@ -429,7 +448,54 @@ class GPTZeroEngine:
         y += x2
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
+    def _block_fwd_fused(self, x, P):
+        """bf16 block with libzinf LayerNorms; the attention residual add is fused
+        into LN2 (x2 = x + proj(o), h2 = LN(x2) in one pass)."""
+        _, h1, m1, r1 = self._ln(x, P["ln1_w"], P["ln1_b"])
+        qkv = torch.addmm(P["qkv_b"], h1, P["qkv_w"].t())
+        o, att = self._attn_fwd(qkv)
+        p = torch.addmm(P["proj_b"], o, P["proj_w"].t())
+        x2, h2, m2, r2 = self._ln(p, P["ln2_w"], P["ln2_b"], resid=x)
+        del p
+        u = torch.addmm(P["fc1_b"], h2, P["fc1_w"].t())
+        a = F.gelu(u, approximate="tanh")
+        y = torch.addmm(P["fc2_b"], a, P["fc2_w"].t())
+        y += x2
+        return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
+
+    def _block_bwd_fused(self, dy, cache, P, G):
+        """bf16 block backward: bias grads via deterministic column sums, GELU
+        backward fused with the fc1 bias grad, LayerNorm backward with the
+        residual gradient folded in — all libzinf; GEMMs and attention via
+        cuBLAS / cuDNN."""
+        x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
+        ws = self.ws
+        torch.mm(dy.t(), a, out=G["fc2_w"])
+        kernels.bias_grad(dy, G["fc2_b"], ws)
+        da = torch.mm(dy, P["fc2_w"])
+        du = torch.empty_like(da)
+        kernels.bias_grad(da, G["fc1_b"], ws, u=u, du=du)
+        del da
+        torch.mm(du.t(), h2, out=G["fc1_w"])
+        dh2 = torch.mm(du, P["fc1_w"])
+        del du
+        dx2 = torch.empty_like(dh2)
+        kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy)
+        torch.mm(dx2.t(), o, out=G["proj_w"])
+        kernels.bias_grad(dx2, G["proj_b"], ws)
+        do = torch.mm(dx2, P["proj_w"])
+        dqkv = self._attn_bwd(do, att)
+        torch.mm(dqkv.t(), h1, out=G["qkv_w"])
+        kernels.bias_grad(dqkv, G["qkv_b"], ws)
+        dh1 = torch.mm(dqkv, P["qkv_w"])
+        dx = torch.empty_like(dh1)
+        kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2)
+        self.launches += 6
+        return dx
+
     def _block_bwd(self, dy, cache, P, G):
+        if self.fused:
+            return self._block_bwd_fused(dy, cache, P, G)
         hd = self.cfg.hd
         x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
         torch.mm(dy.t(), a, out=G["fc2_w"])
@@ -461,6 +527,8 @@ class GPTZeroEngine:
     def _head_fwd_bwd(self, x, PF, PE, G, targets, wte_acc):
         """Final LN + tied LM head + mean token CE; returns (loss, dx). Fills
         G (final bucket grads) and wte_acc (fp32 head contribution to wte)."""
+        if self.fused:
+            return self._head_fused(x, PF, PE, G, targets, wte_acc)
         hd = self.cfg.hd
         hf, mf, rf = torch.native_layer_norm(x, (hd,), PF["lnf_w"], PF["lnf_b"], LN_EPS)
         logits = torch.mm(hf, PE["wte"].t()).float()
@@ -481,6 +549,25 @@ class GPTZeroEngine:
             dhf, x, (hd,), mf, rf, PF["lnf_w"], PF["lnf_b"], [True, True, True])
         G["lnf_w"].copy_(dw)
         G["lnf_b"].copy_(db)
+        return loss, dx
+
+    def _head_fused(self, x, PF, PE, G, targets, wte_acc):
+        """libzinf LN + one-pass softmax cross-entropy over bf16 logits (in place:
+        the logits buffer becomes dlogits); cuBLAS for the tied-head GEMMs."""
+        _, hf, mf, rf = self._ln(x, PF["lnf_w"], PF["lnf_b"])
+        logits = torch.mm(hf, PE["wte"].t())
+        tgt = targets.reshape(-1)
+        T = tgt.numel()
+        rows = torch.empty(T, dtype=torch.float32, device=x.device)
+        loss = torch.empty((), dtype=torch.float32, device=x.device)
+        kernels.softmax_ce(logits, tgt, rows, loss, 1.0 / T)
+        dlog = logits
+        wte_acc.copy_(torch.ops.aten.mm.dtype(dlog.t(), hf, torch.float32))
+        dhf = torch.mm(dlog, PE["wte"])
+        del logits, dlog
+        dx = torch.empty_like(dhf)
+        kernels.ln_bwd(dhf, x, PF["lnf_w"], mf, rf, dx, G["lnf_w"], G["lnf_b"], self.ws)
+        self.launches += 2
         return loss, dx
 
     # ------------------------------------------------------------------- reduce

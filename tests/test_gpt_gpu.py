@@ -91,6 +91,20 @@ def test_step_bf16_matches_oracle():
             assert rel(eng.grad_shards[key][r].cpu().numpy(), gsh[key][r]) < 6e-2, key
 
 
+def test_fused_kernels_match_torch_path():
+    """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path."""
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=False)
+    assert a.fused and not b.fused
+    a.capture_grads = b.capture_grads = True
+    bs = batches_for(SMALL, 2)
+    la, lb = a.step(bs).item(), b.step(bs).item()
+    assert abs(la - lb) <= 2e-3 * abs(lb)
+    for key in a.grad_shards:
+        for r in range(2):
+            assert rel(a.grad_shards[key][r].cpu().numpy(), b.grad_shards[key][r].cpu().numpy()) < 3e-2, key
+
+
 def test_loss_decreases_and_world_sizes_agree():
     c = SMALL
     out = {}
