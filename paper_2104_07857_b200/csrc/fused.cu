@@ -9,6 +9,8 @@
 //   zi_gelu_bwd      du = gelu'(u) * da, partial column sums of du
 //   zi_colsum_finish partials [P x N] -> out[N] (bf16 RNE or fp32), fixed order
 //   zi_softmax_ce    per-row logsumexp, loss, dlogits = (softmax - onehot) * scale
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace zi {
@@ -124,76 +126,93 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
 }
 
 // dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w,
-// plus dres (residual gradient) if given. Two passes over the row (the second
-// re-reads dy / x from L1): pass 1 forms the row sums and accumulates the
-// per-lane dgamma = sum dy * xh, dbeta = sum dy partials in registers; the
-// CTA's 8 warps are then folded through shared memory into one partial row.
+// plus dres (residual gradient) if given. One warp per row; the row's dy and
+// x stay packed (bf16) in registers across the two passes.
 template <int EPL>
 __global__ void __launch_bounds__(256)
-ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
-              const uint16_t* __restrict__ w, const float* __restrict__ mean,
-              const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
-              uint16_t* __restrict__ dx, float* __restrict__ part_g, float* __restrict__ part_b,
-              int T) {
+ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                 const uint16_t* __restrict__ w, const float* __restrict__ mean,
+                 const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
+                 uint16_t* __restrict__ dx, int T) {
   constexpr int H = 32 * EPL;
   constexpr int C = EPL < 8 ? EPL : 8;
-  extern __shared__ float red[];  // [8 warps][2][H]: per-warp gamma / beta partials
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NV = EPL / C;          // vectors per lane
+  using V = typename std::conditional<C == 8, uint4, uint2>::type;
+  const int lane = threadIdx.x & 31;
   const int warps = gridDim.x * (blockDim.x >> 5);
-  float* ag = red + (size_t)wid * 2 * H + lane * EPL;   // this lane's columns only
-  float* ab = ag + H;
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < T; row += warps) {
+    const size_t off = (size_t)row * H + lane * EPL;
+    V gv[NV], xv[NV];
 #pragma unroll
-  for (int i = 0; i < EPL; ++i) ag[i] = ab[i] = 0.f;
-  for (int row = blockIdx.x * (blockDim.x >> 5) + wid; row < T; row += warps) {
-    const uint16_t* gp = dy + (size_t)row * H + lane * EPL;
-    const uint16_t* xp = x + (size_t)row * H + lane * EPL;
+    for (int k = 0; k < NV; ++k) {
+      gv[k] = reinterpret_cast<const V*>(dy + off)[k];
+      xv[k] = reinterpret_cast<const V*>(x + off)[k];
+    }
     const float mu = mean[row], rs = rstd[row];
     float s1 = 0.f, s2 = 0.f;
-#pragma unroll 2
-    for (int c = 0; c < EPL; c += C) {
-      float g[C], xv[C], wf[C];
-      ld_row<C>(gp + c, g);
-      ld_row<C>(xp + c, xv);
-      ld_row<C>(w + lane * EPL + c, wf);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float g[C], xf[C], wf[C];
+      ld_row<C>(reinterpret_cast<const uint16_t*>(&gv[k]), g);
+      ld_row<C>(reinterpret_cast<const uint16_t*>(&xv[k]), xf);
+      ld_row<C>(w + lane * EPL + k * C, wf);
 #pragma unroll
       for (int i = 0; i < C; ++i) {
-        const float xh = (xv[i] - mu) * rs;
         const float d = g[i] * wf[i];
-        ag[c + i] += g[i] * xh;
-        ab[c + i] += g[i];
         s1 += d;
-        s2 += d * xh;
+        s2 += d * (xf[i] - mu) * rs;
       }
     }
     const float m1 = warp_sum(s1) * (1.0f / H), m2 = warp_sum(s2) * (1.0f / H);
-#pragma unroll 2
-    for (int c = 0; c < EPL; c += C) {
-      float g[C], xv[C], wf[C], o[C];
-      ld_row<C>(gp + c, g);
-      ld_row<C>(xp + c, xv);
-      ld_row<C>(w + lane * EPL + c, wf);
 #pragma unroll
-      for (int i = 0; i < C; ++i) o[i] = rs * (g[i] * wf[i] - m1 - (xv[i] - mu) * rs * m2);
+    for (int k = 0; k < NV; ++k) {
+      float g[C], xf[C], wf[C], o[C];
+      ld_row<C>(reinterpret_cast<const uint16_t*>(&gv[k]), g);
+      ld_row<C>(reinterpret_cast<const uint16_t*>(&xv[k]), xf);
+      ld_row<C>(w + lane * EPL + k * C, wf);
+#pragma unroll
+      for (int i = 0; i < C; ++i) o[i] = rs * (g[i] * wf[i] - m1 - (xf[i] - mu) * rs * m2);
       if (dres != nullptr) {
         float rv[C];
-        ld_row<C>(dres + (size_t)row * H + lane * EPL + c, rv);
+        ld_row<C>(dres + off + k * C, rv);
 #pragma unroll
         for (int i = 0; i < C; ++i) o[i] += rv[i];
       }
-      st_row<C>(dx + (size_t)row * H + lane * EPL + c, o);
+      st_row<C>(dx + off + k * C, o);
     }
   }
-  // fold the 8 warps' partials (fixed order) into one gamma / beta row per CTA
-  __syncthreads();
-  for (int c = threadIdx.x; c < H; c += blockDim.x) {
-    float tg = 0.f, tb = 0.f;
+}
+
+// dgamma / dbeta partials over a chunk of rows: thread owns 8 columns,
+// acc_g += dy * (x - mean) * rstd, acc_b += dy.
+__global__ void __launch_bounds__(256)
+ln_bwd_gb_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                 const float* __restrict__ mean, const float* __restrict__ rstd,
+                 float* __restrict__ part_g, float* __restrict__ part_b, int T, int H,
+                 int rows_per) {
+  const int c8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c8 >= H) return;
+  const int r0 = blockIdx.y * rows_per;
+  const int r1 = min(T, r0 + rows_per);
+  float ag[8], ab[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      tg += red[(size_t)k * 2 * H + c];
-      tb += red[(size_t)k * 2 * H + H + c];
+  for (int j = 0; j < 8; ++j) ag[j] = ab[j] = 0.f;
+#pragma unroll 2
+  for (int row = r0; row < r1; ++row) {
+    float g[8], xv[8];
+    ld_row<8>(dy + (size_t)row * H + c8, g);
+    ld_row<8>(x + (size_t)row * H + c8, xv);
+    const float mu = mean[row], rs = rstd[row];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ag[j] += g[j] * (xv[j] - mu) * rs;
+      ab[j] += g[j];
     }
-    part_g[(size_t)blockIdx.x * H + c] = tg;
-    part_b[(size_t)blockIdx.x * H + c] = tb;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    part_g[(size_t)blockIdx.y * H + c8 + j] = ag[j];
+    part_b[(size_t)blockIdx.y * H + c8 + j] = ab[j];
   }
 }
 
@@ -210,6 +229,7 @@ colsum_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
   float acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll 2
   for (int row = r0; row < r1; ++row) {
     float v[8];
     ld_row<8>(a + (size_t)row * N + c8, v);
@@ -233,15 +253,28 @@ colsum_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
   for (int j = 0; j < 8; ++j) part[(size_t)blockIdx.y * N + c8 + j] = acc[j];
 }
 
+// partials [P x N] -> out[N]: CTA = 32 columns x 8 row groups; group k sums
+// rows p = k, k+8, ... in order, then the 8 group sums fold in order (deterministic).
 __global__ void __launch_bounds__(256)
 colsum_finish_kernel(const float* __restrict__ part, int P, int N, void* __restrict__ out,
                      int out_f32) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
+  __shared__ float sm[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
   float s = 0.f;
-  for (int p = 0; p < P; ++p) s += part[(size_t)p * N + c];
-  if (out_f32) static_cast<float*>(out)[c] = s;
-  else static_cast<uint16_t*>(out)[c] = tobf(s);
+  if (c < N) {
+#pragma unroll 4
+    for (int p = ty; p < P; p += 8) s += part[(size_t)p * N + c];
+  }
+  sm[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += sm[k][tx];
+    if (out_f32) static_cast<float*>(out)[c] = t;
+    else static_cast<uint16_t*>(out)[c] = tobf(t);
+  }
 }
 
 // One CTA per row of V logits (bf16, in place): lse, loss_row = lse - l[t],
@@ -372,38 +405,28 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
               const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
               size_t work_elems, int T, int H, void* stream) {
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
+  ZI_CHECK_ARG(H % 8 == 0, "zi_ln_bwd: H must be a multiple of 8");
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = (T + 7) / 8 < sm_count() ? (T + 7) / 8 : sm_count();
-  ZI_CHECK_ARG(work_elems >= 2 * (size_t)grid * H, "zi_ln_bwd: work needs %zu floats",
-               2 * (size_t)grid * H);
-  float* pg = work;
-  float* pb = work + (size_t)grid * H;
-  const size_t smem = (size_t)8 * 2 * H * sizeof(float);
-  switch (H / 32) {
-#define ZI_LNB(E)                                                                              \
-    case E: {                                                                                  \
-      static bool a = false;                                                                   \
-      if (!a) {                                                                                \
-        ZI_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<E>,                                         \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),  \
-                "cudaFuncSetAttribute(ln_bwd)");                                              \
-        a = true;                                                                              \
-      }                                                                                        \
-      ln_bwd_kernel<E><<<grid, 256, smem, s>>>((const uint16_t*)dy, (const uint16_t*)x,        \
-                                               (const uint16_t*)w, mean, rstd,                 \
-                                               (const uint16_t*)dres, (uint16_t*)dx, pg, pb, T); \
-      break;                                                                                   \
-    }
-    ZI_LNB(4) ZI_LNB(8) ZI_LNB(16) ZI_LNB(32) ZI_LNB(64)
-#undef ZI_LNB
-    default:
-      zi::set_error("zi_ln_bwd: hidden size %d not in {128..2048, power of 2}", H);
-      return ZI_EINVAL;
-  }
-  int st = zi::launch_status("zi_ln_bwd");
+  const int grid = (T + 7) / 8 < sm_count() * 4 ? (T + 7) / 8 : sm_count() * 4;
+  EPL_DISPATCH(H, ln_bwd_dx_kernel, grid, 256, s, (const uint16_t*)dy, (const uint16_t*)x,
+               (const uint16_t*)w, mean, rstd, (const uint16_t*)dres, (uint16_t*)dx, T);
+  int st = zi::launch_status("zi_ln_bwd(dx)");
   if (st) return st;
-  colsum_finish_kernel<<<(H + 255) / 256, 256, 0, s>>>(pg, grid, H, dgamma, grads_f32);
-  colsum_finish_kernel<<<(H + 255) / 256, 256, 0, s>>>(pb, grid, H, dbeta, grads_f32);
+  const int cblocks = (H / 8 + 255) / 256;
+  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
+  if (chunks > T) chunks = T;
+  const int rows_per = (T + chunks - 1) / chunks;
+  chunks = (T + rows_per - 1) / rows_per;
+  ZI_CHECK_ARG(work_elems >= 2 * (size_t)chunks * H, "zi_ln_bwd: work needs %zu floats",
+               2 * (size_t)chunks * H);
+  float* pg = work;
+  float* pb = work + (size_t)chunks * H;
+  ln_bwd_gb_kernel<<<dim3(cblocks, chunks), 256, 0, s>>>((const uint16_t*)dy, (const uint16_t*)x,
+                                                         mean, rstd, pg, pb, T, H, rows_per);
+  st = zi::launch_status("zi_ln_bwd(gamma/beta)");
+  if (st) return st;
+  colsum_finish_kernel<<<(H + 31) / 32, 256, 0, s>>>(pg, chunks, H, dgamma, grads_f32);
+  colsum_finish_kernel<<<(H + 31) / 32, 256, 0, s>>>(pb, chunks, H, dbeta, grads_f32);
   return zi::launch_status("zi_ln_bwd(finish)");
 }
 
@@ -428,7 +451,7 @@ int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, 
                                               rows_per);
   int st = zi::launch_status("zi_bias_grad");
   if (st) return st;
-  colsum_finish_kernel<<<(N + 255) / 256, 256, 0, s>>>(work, chunks, N, db, db_f32);
+  colsum_finish_kernel<<<(N + 31) / 32, 256, 0, s>>>(work, chunks, N, db, db_f32);
   return zi::launch_status("zi_bias_grad(finish)");
 }
 
