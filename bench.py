@@ -168,13 +168,12 @@ def run_ours(args):
 
     # device-resident synthetic batches (distinct per step)
     dev_batches = [eg.synthetic_tokens(cfg, 7, rank, s) for s in range(max(args.steps, 1))]
-    for w in range(args.warmup):
-        eng.step([dev_batches[w % len(dev_batches)]])
-    barrier()
 
-    # ---------------- kernel-level roofline instrumentation (rs_adam on its stream)
+    # ---------------- kernel-level roofline instrumentation: CUDA events around every
+    # zi_rs_adam launch on its stream. Under CUDA graphs the events are captured
+    # into the graph, so each replay re-times the launches of that step.
     from paper_2104_07857_b200 import kernels as K
-    orig = K.rs_adam
+    orig = K.rs_adam_dc
     rec = []
 
     def timed_rs_adam(*a, **kw):
@@ -185,12 +184,17 @@ def run_ours(args):
         e1.record(s)
         n = a[2]
         ncontrib = len(a[0])
-        rec.append((e0, e1, n * (2 * ncontrib + 12 + 14)))
+        rec.append((e0, e1, n * (2 * ncontrib + 12 + 14), torch.cuda.is_current_stream_capturing()))
+
+    K.rs_adam_dc = timed_rs_adam
+    step = eng.step if args.no_graph else eng.step_graphed
+    for w in range(args.warmup):
+        step([dev_batches[w % len(dev_batches)]])
+    barrier()
+    if args.no_graph:
+        rec.clear()
 
     # ---------------- timed region (device-resident inputs)
-    K.rs_adam = timed_rs_adam
-    import paper_2104_07857_b200.gpt as gmod
-    gmod.kernels.rs_adam = timed_rs_adam
     launches0 = eng.launches
     clocks = ClockSampler(local)
     with clocks:
@@ -198,11 +202,11 @@ def run_ours(args):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
         for s in range(args.steps):
-            loss = eng.step([dev_batches[s % len(dev_batches)]])
+            loss = step([dev_batches[s % len(dev_batches)]])
         t1.record()
         barrier()
-    K.rs_adam = orig
-    gmod.kernels.rs_adam = orig
+    K.rs_adam_dc = orig
+    rec = [r for r in rec if r[3]] if not args.no_graph else rec
     ms = t0.elapsed_time(t1)
     if world > 1:
         ms = comm.allreduce_max(ms)
@@ -211,15 +215,16 @@ def run_ours(args):
     flops = eg.model_flops_per_step(cfg)          # per rank
     tflops_job = flops * world / (ms_step / 1e3) / 1e12
     samples_s = cfg.batch * world / (ms_step / 1e3)
-    k_ms = [a.elapsed_time(b) for a, b, _ in rec]
-    k_bytes = [nb for _, _, nb in rec]
+    k_ms = [a.elapsed_time(b) for a, b, _, _ in rec]
+    k_bytes = [nb for _, _, nb, _ in rec]
     hbm, tc, peak_kind = _peaks()
     # the largest bucket's launches (the 24 block buckets) dominate
     big = max(k_bytes) if k_bytes else 0
     sel = [(t, b) for t, b in zip(k_ms, k_bytes) if b == big]
     avg_ms = sum(t for t, _ in sel) / max(1, len(sel))
     achieved = big / (avg_ms / 1e3) / 1e9 if avg_ms > 0 else 0.0
-    rs_share = sum(k_ms) / args.steps / ms_step if ms_step > 0 else 0.0
+    per_step = sum(k_ms) if not args.no_graph else sum(k_ms) / args.steps
+    rs_share = per_step / ms_step if ms_step > 0 else 0.0
 
     # ---------------- e2e through the public API with host buffers
     import numpy as np
@@ -233,7 +238,7 @@ def run_ours(args):
     e0.record()
     for s in range(args.steps):
         d = host[s].to("cuda", non_blocking=True)
-        loss = eng.step([(d[:, :-1], d[:, 1:])])
+        loss = step([(d[:, :-1], d[:, 1:])])
         _ = loss.item()
     e1.record()
     barrier()
@@ -370,6 +375,7 @@ def offload_leg(cfg, args) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--no-offload", action="store_true", help="skip the optimizer-offload leg")
+    ap.add_argument("--no-graph", action="store_true", help="eager steps instead of the CUDA graph")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)

@@ -85,6 +85,18 @@ int zi_rs_adam(const void* const* contribs, int n_contrib, size_t shard_offset,
                float* p, float* m, float* v, void* p_half, float* g_out,
                const zi_adam_consts* c, void* stream);
 
+/* zi_rs_adam with the Adam constants read from device memory (c_dev), so a
+ * captured CUDA graph replays with per-step bias corrections. */
+int zi_rs_adam_dc(const void* const* contribs, int n_contrib, size_t shard_offset,
+                  size_t shard_elems, size_t contrib_len, float scale, int half_kind,
+                  float* p, float* m, float* v, void* p_half, float* g_out,
+                  const zi_adam_consts* c_dev, void* stream);
+
+/* Device-side step advance: *step_dev += 1, then *consts_dev = the constants
+ * of that step folded exactly as on the host (double math, one rounding). */
+int zi_adam_advance(double lr, double beta1, double beta2, double eps, int* step_dev,
+                    zi_adam_consts* consts_dev, void* stream);
+
 /* allgather: full[r*shard_elems + i] = shards[r][i],
  * truncated to full_elems. shards[r] may be IPC-mapped peer memory.
  * elem_bytes in {2,4,8}. use_copy_engine != 0 issues one cudaMemcpyAsync per

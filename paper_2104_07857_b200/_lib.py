@@ -43,6 +43,10 @@ SIGNATURES = {
     "zi_rs_adam": [ctypes.POINTER(c_void_p), c_int, c_size_t, c_size_t, c_size_t, c_float, c_int,
                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                    ctypes.POINTER(AdamConstsC), c_void_p],
+    "zi_rs_adam_dc": [ctypes.POINTER(c_void_p), c_int, c_size_t, c_size_t, c_size_t, c_float,
+                      c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    "zi_adam_advance": [ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                        c_void_p, c_void_p, c_void_p],
     "zi_allgather": [ctypes.POINTER(c_void_p), c_int, c_size_t, c_size_t, c_void_p, c_size_t,
                      c_int, c_void_p],
     "zi_barrier": [ctypes.POINTER(c_void_p), c_int, c_int, c_uint32, c_void_p],

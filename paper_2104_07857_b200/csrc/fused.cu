@@ -72,114 +72,118 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Lane l of a warp owns the EPL contiguous columns [l*EPL, (l+1)*EPL) of a row
-// (H = 32 * EPL). One warp per row, rows grid-strided over warps. The row
-// stays in registers; w / b are read per 8-column chunk (L1-resident).
-template <int EPL>
+// Row-group LayerNorm: TPR threads per row, 8 contiguous columns each
+// (H = 8 * TPR); a 256-thread CTA holds 256 / TPR rows. Row statistics are
+// reduced with shuffles (TPR <= 32) or shuffles + shared memory.
+template <int TPR>
+__device__ __forceinline__ float row_reduce(float v, float* sm) {
+#pragma unroll
+  for (int o = (TPR < 32 ? TPR : 32) / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if constexpr (TPR > 32) {
+    constexpr int W = TPR / 32;              // warps per row
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sm[wid] = v;
+    __syncthreads();
+    const int base = (wid / W) * W;
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < W; ++k) t += sm[base + k];
+    __syncthreads();
+    v = t;
+  }
+  return v;
+}
+
+template <int TPR>
 __global__ void __launch_bounds__(256)
 ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
               uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
               const uint16_t* __restrict__ b, uint16_t* __restrict__ y, float* __restrict__ mean,
               float* __restrict__ rstd, int T, float eps) {
-  constexpr int H = 32 * EPL;
-  constexpr int C = EPL < 8 ? EPL : 8;
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < T; row += warps) {
-    float v[EPL];
-    ld_row<EPL>(x + (size_t)row * H + lane * EPL, v);
+  constexpr int H = 8 * TPR, RPC = 256 / TPR;
+  __shared__ float sm[8];
+  const int t = threadIdx.x % TPR;
+  float wf[8], bv[8];
+  ld_row<8>(w + t * 8, wf);
+  ld_row<8>(b + t * 8, bv);
+  for (int row0 = blockIdx.x * RPC; row0 < T; row0 += gridDim.x * RPC) {
+    const int row = row0 + threadIdx.x / TPR;
+    const bool live = row < T;
+    const size_t off = (size_t)(live ? row : 0) * H + t * 8;
+    float v[8];
+    ld_row<8>(x + off, v);
     if (r != nullptr) {
+      float rv[8];
+      ld_row<8>(r + off, rv);
 #pragma unroll
-      for (int c = 0; c < EPL; c += C) {
-        float rv[C];
-        ld_row<C>(r + (size_t)row * H + lane * EPL + c, rv);
-#pragma unroll
-        for (int i = 0; i < C; ++i) v[c + i] = __bfloat162float(__float2bfloat16_rn(v[c + i] + rv[i]));
-      }
-      st_row<EPL>(xsum + (size_t)row * H + lane * EPL, v);
+      for (int i = 0; i < 8; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i] + rv[i]));
+      if (live) st_row<8>(xsum + off, v);
     }
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) s += v[i];
-    const float mu = warp_sum(s) * (1.0f / H);
+    for (int i = 0; i < 8; ++i) s += v[i];
+    const float mu = row_reduce<TPR>(s, sm) * (1.0f / H);
     float q = 0.f;
 #pragma unroll
-    for (int i = 0; i < EPL; ++i) {
+    for (int i = 0; i < 8; ++i) {
       const float d = v[i] - mu;
       q += d * d;
     }
-    const float rs = rsqrtf(warp_sum(q) * (1.0f / H) + eps);
+    const float rs = rsqrtf(row_reduce<TPR>(q, sm) * (1.0f / H) + eps);
 #pragma unroll
-    for (int c = 0; c < EPL; c += C) {
-      float wf[C], bv[C];
-      ld_row<C>(w + lane * EPL + c, wf);
-      ld_row<C>(b + lane * EPL + c, bv);
-#pragma unroll
-      for (int i = 0; i < C; ++i) v[c + i] = (v[c + i] - mu) * rs * wf[i] + bv[i];
-    }
-    st_row<EPL>(y + (size_t)row * H + lane * EPL, v);
-    if (lane == 0) {
-      mean[row] = mu;
-      rstd[row] = rs;
+    for (int i = 0; i < 8; ++i) v[i] = (v[i] - mu) * rs * wf[i] + bv[i];
+    if (live) {
+      st_row<8>(y + off, v);
+      if (t == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+      }
     }
   }
 }
 
 // dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w,
-// plus dres (residual gradient) if given. One warp per row; the row's dy and
-// x stay packed (bf16) in registers across the two passes.
-template <int EPL>
+// plus dres (residual gradient) if given.
+template <int TPR>
 __global__ void __launch_bounds__(256)
 ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
                  const uint16_t* __restrict__ w, const float* __restrict__ mean,
                  const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
                  uint16_t* __restrict__ dx, int T) {
-  constexpr int H = 32 * EPL;
-  constexpr int C = EPL < 8 ? EPL : 8;
-  constexpr int NV = EPL / C;          // vectors per lane
-  using V = typename std::conditional<C == 8, uint4, uint2>::type;
-  const int lane = threadIdx.x & 31;
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < T; row += warps) {
-    const size_t off = (size_t)row * H + lane * EPL;
-    V gv[NV], xv[NV];
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      gv[k] = reinterpret_cast<const V*>(dy + off)[k];
-      xv[k] = reinterpret_cast<const V*>(x + off)[k];
-    }
-    const float mu = mean[row], rs = rstd[row];
+  constexpr int H = 8 * TPR, RPC = 256 / TPR;
+  __shared__ float sm[8];
+  const int t = threadIdx.x % TPR;
+  float wf[8];
+  ld_row<8>(w + t * 8, wf);
+  for (int row0 = blockIdx.x * RPC; row0 < T; row0 += gridDim.x * RPC) {
+    const int row = row0 + threadIdx.x / TPR;
+    const bool live = row < T;
+    const int rr = live ? row : 0;
+    const size_t off = (size_t)rr * H + t * 8;
+    float g[8], xv[8];
+    ld_row<8>(dy + off, g);
+    ld_row<8>(x + off, xv);
+    const float mu = mean[rr], rs = rstd[rr];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      float g[C], xf[C], wf[C];
-      ld_row<C>(reinterpret_cast<const uint16_t*>(&gv[k]), g);
-      ld_row<C>(reinterpret_cast<const uint16_t*>(&xv[k]), xf);
-      ld_row<C>(w + lane * EPL + k * C, wf);
-#pragma unroll
-      for (int i = 0; i < C; ++i) {
-        const float d = g[i] * wf[i];
-        s1 += d;
-        s2 += d * (xf[i] - mu) * rs;
-      }
+    for (int i = 0; i < 8; ++i) {
+      g[i] *= wf[i];                 // dxh
+      xv[i] = (xv[i] - mu) * rs;     // xh
+      s1 += g[i];
+      s2 += g[i] * xv[i];
     }
-    const float m1 = warp_sum(s1) * (1.0f / H), m2 = warp_sum(s2) * (1.0f / H);
+    const float m1 = row_reduce<TPR>(s1, sm) * (1.0f / H);
+    const float m2 = row_reduce<TPR>(s2, sm) * (1.0f / H);
+    float o[8];
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      float g[C], xf[C], wf[C], o[C];
-      ld_row<C>(reinterpret_cast<const uint16_t*>(&gv[k]), g);
-      ld_row<C>(reinterpret_cast<const uint16_t*>(&xv[k]), xf);
-      ld_row<C>(w + lane * EPL + k * C, wf);
+    for (int i = 0; i < 8; ++i) o[i] = rs * (g[i] - m1 - xv[i] * m2);
+    if (dres != nullptr) {
+      float rv[8];
+      ld_row<8>(dres + off, rv);
 #pragma unroll
-      for (int i = 0; i < C; ++i) o[i] = rs * (g[i] * wf[i] - m1 - (xf[i] - mu) * rs * m2);
-      if (dres != nullptr) {
-        float rv[C];
-        ld_row<C>(dres + off + k * C, rv);
-#pragma unroll
-        for (int i = 0; i < C; ++i) o[i] += rv[i];
-      }
-      st_row<C>(dx + off + k * C, o);
+      for (int i = 0; i < 8; ++i) o[i] += rv[i];
     }
+    if (live) st_row<8>(dx + off, o);
   }
 }
 
@@ -197,7 +201,7 @@ ln_bwd_gb_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x
   float ag[8], ab[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) ag[j] = ab[j] = 0.f;
-#pragma unroll 2
+#pragma unroll 4
   for (int row = r0; row < r1; ++row) {
     float g[8], xv[8];
     ld_row<8>(dy + (size_t)row * H + c8, g);
@@ -229,7 +233,7 @@ colsum_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
   float acc[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-#pragma unroll 2
+#pragma unroll 4
   for (int row = r0; row < r1; ++row) {
     float v[8];
     ld_row<8>(a + (size_t)row * N + c8, v);
@@ -376,16 +380,23 @@ static int sm_count() {
 
 using namespace zi::fused;
 
-#define EPL_DISPATCH(H, KERNEL, GRID, BLOCK, STREAM, ...)                                 \
-  switch ((H) / 32) {                                                                      \
-    case 4: KERNEL<4><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                     \
-    case 8: KERNEL<8><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                     \
-    case 16: KERNEL<16><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    case 32: KERNEL<32><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    case 64: KERNEL<64><<<GRID, BLOCK, 0, STREAM>>>(__VA_ARGS__); break;                   \
+#define TPR_DISPATCH(H, KERNEL, GRID, STREAM, ...)                                        \
+  switch ((H) / 8) {                                                                       \
+    case 16: KERNEL<16><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
+    case 32: KERNEL<32><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
+    case 64: KERNEL<64><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
+    case 128: KERNEL<128><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 256: KERNEL<256><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
     default: zi::set_error("LayerNorm: hidden size %d not in {128..2048, power of 2}", H); \
       return ZI_EINVAL;                                                                    \
   }
+
+static int ln_grid(int T, int H) {
+  const int rpc = 256 / (H / 8);
+  const int need = (T + rpc - 1) / rpc;
+  const int cap = sm_count() * 8;
+  return need < cap ? need : cap;
+}
 
 extern "C" {
 
@@ -394,8 +405,9 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
   ZI_CHECK_ARG(x && w && b && y && mean && rstd && T > 0, "zi_ln_fwd: bad arguments");
   ZI_CHECK_ARG(!resid || xsum, "zi_ln_fwd: resid needs xsum");
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = (T + 7) / 8 < sm_count() * 4 ? (T + 7) / 8 : sm_count() * 4;
-  EPL_DISPATCH(H, ln_fwd_kernel, grid, 256, s, (const uint16_t*)x, (const uint16_t*)resid,
+  ZI_CHECK_ARG(H >= 128 && H <= 2048 && (H & (H - 1)) == 0, "zi_ln_fwd: H must be 128..2048, power of 2");
+  const int grid = ln_grid(T, H);
+  TPR_DISPATCH(H, ln_fwd_kernel, grid, s, (const uint16_t*)x, (const uint16_t*)resid,
                (uint16_t*)xsum, (const uint16_t*)w, (const uint16_t*)b, (uint16_t*)y, mean, rstd,
                T, eps);
   return zi::launch_status("zi_ln_fwd");
@@ -407,8 +419,9 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
   ZI_CHECK_ARG(H % 8 == 0, "zi_ln_bwd: H must be a multiple of 8");
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = (T + 7) / 8 < sm_count() * 4 ? (T + 7) / 8 : sm_count() * 4;
-  EPL_DISPATCH(H, ln_bwd_dx_kernel, grid, 256, s, (const uint16_t*)dy, (const uint16_t*)x,
+  ZI_CHECK_ARG(H >= 128 && H <= 2048 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..2048, power of 2");
+  const int grid = ln_grid(T, H);
+  TPR_DISPATCH(H, ln_bwd_dx_kernel, grid, s, (const uint16_t*)dy, (const uint16_t*)x,
                (const uint16_t*)w, mean, rstd, (const uint16_t*)dres, (uint16_t*)dx, T);
   int st = zi::launch_status("zi_ln_bwd(dx)");
   if (st) return st;

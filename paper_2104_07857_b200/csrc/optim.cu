@@ -90,7 +90,9 @@ template <int KIND, bool ADAM>
 __global__ void __launch_bounds__(256)
 rs_kernel(Contribs cb, int K, size_t off, size_t n, size_t nvec8, size_t clen, float scale,
           float* __restrict__ out_or_g, float* __restrict__ p, float* __restrict__ m,
-          float* __restrict__ v, uint16_t* __restrict__ ph, zi_adam_consts c) {
+          float* __restrict__ v, uint16_t* __restrict__ ph, zi_adam_consts c,
+          const zi_adam_consts* __restrict__ cdev) {
+  if (ADAM && cdev != nullptr) c = *cdev;  // constants advanced on the device (CUDA graphs)
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = tid; i < nvec8; i += stride) {
@@ -144,11 +146,12 @@ rs_kernel(Contribs cb, int K, size_t off, size_t n, size_t nvec8, size_t clen, f
 template <bool ADAM>
 int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t clen,
               float scale, int half_kind, float* out_or_g, float* p, float* m, float* v,
-              void* p_half, const zi_adam_consts* c, void* stream, const char* name) {
+              void* p_half, const zi_adam_consts* c, void* stream, const char* name,
+              const zi_adam_consts* cdev = nullptr) {
   ZI_CHECK_ARG(contribs != nullptr && K >= 1 && K <= kMaxContrib,
                "%s: need 1 <= n_contrib <= %d", name, kMaxContrib);
   ZI_CHECK_ARG(half_kind == ZI_HALF_FP16 || half_kind == ZI_HALF_BF16, "%s: bad half_kind", name);
-  if (ADAM) ZI_CHECK_ARG(p && m && v && c, "%s: NULL p/m/v/consts", name);
+  if (ADAM) ZI_CHECK_ARG(p && m && v && (c || cdev), "%s: NULL p/m/v/consts", name);
   else ZI_CHECK_ARG(out_or_g != nullptr, "%s: NULL out", name);
   if (n == 0) return ZI_OK;
   Contribs cb{};
@@ -170,11 +173,29 @@ int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t c
   uint16_t* ph = static_cast<uint16_t*>(p_half);
   if (half_kind == ZI_HALF_BF16)
     rs_kernel<ZI_HALF_BF16, ADAM><<<grid, block, 0, s>>>(cb, K, off, n, nvec8, clen, scale,
-                                                          out_or_g, p, m, v, ph, cc);
+                                                          out_or_g, p, m, v, ph, cc, cdev);
   else
     rs_kernel<ZI_HALF_FP16, ADAM><<<grid, block, 0, s>>>(cb, K, off, n, nvec8, clen, scale,
-                                                          out_or_g, p, m, v, ph, cc);
+                                                          out_or_g, p, m, v, ph, cc, cdev);
   return launch_status(name);
+}
+
+// t <- t + 1 on the device and the step's folded constants, exactly the
+// host-side folding (oracle/adam.py AdamConsts.make): doubles rounded once.
+__global__ void adam_advance_kernel(double lr, double b1, double b2, double eps, int* step,
+                                    zi_adam_consts* out) {
+  const int t = *step + 1;
+  *step = t;
+  zi_adam_consts c;
+  c.lr = (float)lr;
+  c.b1 = (float)b1;
+  c.omb1 = (float)(1.0 - b1);
+  c.b2 = (float)b2;
+  c.omb2 = (float)(1.0 - b2);
+  c.bc1 = (float)(1.0 - pow(b1, (double)t));
+  c.bc2 = (float)(1.0 - pow(b2, (double)t));
+  c.eps = (float)eps;
+  *out = c;
 }
 
 // Generic SPEC reduce_scatter for full-precision contributions: fp32 inputs
@@ -259,6 +280,24 @@ int zi_rs_adam(const void* const* contribs, int n_contrib, size_t shard_offset, 
                void* p_half, float* g_out, const zi_adam_consts* c, void* stream) {
   return zi::launch_rs<true>(contribs, n_contrib, shard_offset, shard_elems, contrib_len, scale,
                              half_kind, g_out, p, m, v, p_half, c, stream, "zi_rs_adam");
+}
+
+int zi_rs_adam_dc(const void* const* contribs, int n_contrib, size_t shard_offset,
+                  size_t shard_elems, size_t contrib_len, float scale, int half_kind, float* p,
+                  float* m, float* v, void* p_half, float* g_out, const zi_adam_consts* c_dev,
+                  void* stream) {
+  ZI_CHECK_ARG(c_dev != nullptr, "zi_rs_adam_dc: NULL device constants");
+  return zi::launch_rs<true>(contribs, n_contrib, shard_offset, shard_elems, contrib_len, scale,
+                             half_kind, g_out, p, m, v, p_half, nullptr, stream, "zi_rs_adam_dc",
+                             c_dev);
+}
+
+int zi_adam_advance(double lr, double beta1, double beta2, double eps, int* step_dev,
+                    zi_adam_consts* consts_dev, void* stream) {
+  ZI_CHECK_ARG(step_dev && consts_dev, "zi_adam_advance: NULL device pointer");
+  zi::adam_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(lr, beta1, beta2, eps, step_dev,
+                                                            consts_dev);
+  return zi::launch_status("zi_adam_advance");
 }
 
 }  // extern "C"

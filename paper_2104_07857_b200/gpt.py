@@ -189,6 +189,8 @@ class GPTZeroEngine:
         self.d2h_stream = torch.cuda.Stream(self.dev)
         self._alloc_work()
         self.launches = 0  # libzinf kernel launches issued by step()
+        self.adam = kernels.DeviceAdamState(lr, betas, eps, device=self.dev)
+        self._graph = None
         # bf16 path: LayerNorm / bias-grad / GELU-bwd / softmax-CE on libzinf kernels
         self.fused = (self.cdt == torch.bfloat16 and cfg.hd in (128, 256, 512, 1024, 2048)
                       and fused)
@@ -607,10 +609,10 @@ class GPTZeroEngine:
             self._reduce_update_offload(b, slot, consts, contribs, scale)
             return
         for li, r in enumerate(self.ranks):
-            kernels.rs_adam(contribs, r * b.shard, b.shard, b.numel, scale,
-                            self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
-                            self._shard_view(self.v, li, b), self._shard_view(self.p16, li, b),
-                            consts, g_out=self._gout(li, b))
+            kernels.rs_adam_dc(contribs, r * b.shard, b.shard, b.numel, scale,
+                               self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
+                               self._shard_view(self.v, li, b), self._shard_view(self.p16, li, b),
+                               self.adam, g_out=self._gout(li, b))
             self.launches += 1
 
     def _reduce_update_offload(self, b: Bucket, slot: int, consts, contribs, scale: float):
@@ -668,7 +670,8 @@ class GPTZeroEngine:
                 with torch.cuda.stream(opt):
                     opt.wait_event(ev_h2d.pop(ci))
                     ph = self.stage16[k][:n] if host_params else p16[s:s + n]
-                    kernels.rs_adam(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph, consts)
+                    kernels.rs_adam_dc(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph,
+                                       self.adam)
                     self.launches += 1
                     ev_c = torch.cuda.Event()
                     ev_c.record(opt)
@@ -708,9 +711,11 @@ class GPTZeroEngine:
         mean loss over all ranks as a 0-d fp32 CUDA tensor."""
         c = self.cfg
         self.t += 1
-        consts = _lib.adam_consts(self.lr, self.betas[0], self.betas[1], self.eps, self.t)
+        consts = None                 # Adam constants live on the device (self.adam)
         self.grad_shards = {}
         cur = torch.cuda.current_stream()
+        self.adam.advance()           # t += 1 and this step's bias corrections, on the GPU
+        self.launches += 1
         gs = self.gather_stream if self.prefetch else cur
         nloc = len(self.ranks)
         if not self.comm.is_local and self.N > 1:
@@ -798,10 +803,46 @@ class GPTZeroEngine:
         if self.offload:  # the step ends when the last optimizer chunk is back in host DRAM
             cur.wait_stream(self.opt_stream)
             cur.wait_stream(self.d2h_stream)
+            cur.wait_stream(self.h2d_stream)
+        if gs is not cur:
+            cur.wait_stream(gs)       # join the gather stream (required for graph capture)
         total = losses[0].float()
         for l in losses[1:]:
             total = total + l.float()
         return total / nloc if self.comm.is_local else total
+
+    def step_graphed(self, batches) -> torch.Tensor:
+        """``step`` captured once into a CUDA graph and replayed.
+
+        The step's ~1000 launches (GEMMs, attention, libzinf kernels, the
+        gathers and offload copies on their side streams) become one graph
+        launch; Adam's per-step constants come from the device counter
+        (zi_adam_advance inside the graph), tokens from static buffers the
+        caller's batch is copied into. The first call warms up with two eager
+        steps (real training steps) and captures; every call then replays.
+        """
+        cur = torch.cuda.current_stream()
+        if self._graph is None:
+            if self.trace:
+                raise ValueError("tracing is not supported under graph capture")
+            self._static = [(t.clone(), y.clone()) for t, y in batches]
+            for _ in range(2):       # warm cuBLAS / cuDNN plans and the allocator
+                self.step(self._static)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            l0, t0 = self.launches, self.t
+            with torch.cuda.graph(g):
+                self._static_loss = self.step(self._static)
+            self._graph = g
+            self._launches_per_replay = self.launches - l0
+            self.launches, self.t = l0, t0      # capture executes nothing
+        for (st, sy), (t, y) in zip(self._static, batches):
+            st.copy_(t, non_blocking=True)
+            sy.copy_(y, non_blocking=True)
+        self._graph.replay()
+        self.t += 1
+        self.launches += self._launches_per_replay
+        return self._static_loss
 
     # ------------------------------------------------------------------ access
     def gathered(self, key: str) -> torch.Tensor:

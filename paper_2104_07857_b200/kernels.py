@@ -92,6 +92,29 @@ def rs_adam(contribs, shard_offset: int, shard_elems: int, contrib_len: int, sca
               consts, _stream(stream))
 
 
+class DeviceAdamState:
+    """Device-resident step counter + folded Adam constants (zi_adam_advance)."""
+
+    def __init__(self, lr: float, betas, eps: float, device="cuda"):
+        self.hp = (float(lr), float(betas[0]), float(betas[1]), float(eps))
+        self.step = torch.zeros(1, dtype=torch.int32, device=device)
+        self.consts = torch.zeros(8, dtype=torch.float32, device=device)
+
+    def advance(self, stream=None) -> None:
+        _lib.call("zi_adam_advance", *self.hp, self.step.data_ptr(), self.consts.data_ptr(),
+                  _stream(stream))
+
+
+def rs_adam_dc(contribs, shard_offset: int, shard_elems: int, contrib_len: int, scale: float,
+               p, m, v, p_half, state: DeviceAdamState, g_out=None, stream=None) -> None:
+    """zi_rs_adam_dc: zi_rs_adam with constants from the device (graph-replayable)."""
+    arr, k = _contrib_ptrs(contribs)
+    _lib.call("zi_rs_adam_dc", arr, k, shard_offset, shard_elems, contrib_len, scale,
+              half_kind(p_half.dtype), _dev(p, "p"), _dev(m, "m"), _dev(v, "v"),
+              _dev(p_half, "p_half"), _dev(g_out, "g_out") if g_out is not None else None,
+              state.consts.data_ptr(), _stream(stream))
+
+
 def allgather(shards, shard_elems: int, full: torch.Tensor, full_elems: int,
               use_copy_engine: bool = False, stream=None) -> None:
     """zi_allgather: full[r*L:(r+1)*L] = shards[r], truncated to full_elems."""

@@ -43,7 +43,8 @@ def launches(path: str, top: int = 25) -> str:
            "", "| share | time (us) | launches | kernel |", "|---:|---:|---:|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1])[:top]:
         out.append(f"| {v / T * 100:.2f}% | {v:.0f} | {cnt[k]} | `{k}` |")
-    mine = sum(v for k, v in tot.items() if "zi::" in k or k.startswith(("rs_kernel", "adam_kernel", "gather_", "linear_fwd")))
+    mine = sum(v for k, v in tot.items() if "zi::" in k or "fused::" in k or "gemm" in k or
+               k.startswith(("rs_kernel", "adam_kernel", "gather_", "linear_fwd")))
     out.append("")
     out.append(f"libzinf kernels: {mine / T * 100:.2f}% of device time")
     return "\n".join(out)

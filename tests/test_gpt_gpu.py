@@ -91,6 +91,32 @@ def test_step_bf16_matches_oracle():
             assert rel(eng.grad_shards[key][r].cpu().numpy(), gsh[key][r]) < 6e-2, key
 
 
+@pytest.mark.parametrize("world", [1, 2])
+def test_cuda_graph_step_matches_eager(world):
+    """The captured step replays the same math: device Adam counter + static inputs."""
+    a = eg.GPTZeroEngine(SMALL, LocalComm(world), lr=1e-3)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(world), lr=1e-3)
+    la, lb = [], []
+    for step in range(5):
+        bs = batches_for(SMALL, world, step)
+        la.append(a.step(bs).item())
+        lb.append(b.step_graphed(bs).item())
+    np.testing.assert_allclose(la, lb, rtol=2e-5)
+    assert int(a.adam.step.item()) == int(b.adam.step.item()) == 5
+    for key in a.by_key:
+        torch.testing.assert_close(a.shard(key, 0)["p32"], b.shard(key, 0)["p32"], rtol=0, atol=5e-5)
+
+
+def test_device_adam_constants_match_host_folding():
+    from paper_2104_07857_b200 import _lib, kernels
+    st = kernels.DeviceAdamState(3e-4, (0.9, 0.95), 1e-8)
+    for t in range(1, 200):
+        st.advance()
+        h = _lib.adam_consts(3e-4, 0.9, 0.95, 1e-8, t)
+        want = np.array([h.lr, h.b1, h.omb1, h.b2, h.omb2, h.bc1, h.bc2, h.eps], np.float32)
+        assert np.array_equal(st.consts.cpu().numpy(), want), t
+
+
 def test_fused_kernels_match_torch_path():
     """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path."""
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True)
