@@ -155,6 +155,12 @@ int zi_host_free(void* p);
 int zi_memcpy_async(void* dst, const void* src, size_t bytes, int kind, void* stream);
 int zi_event_create(void** ev);                       /* timing disabled */
 int zi_event_destroy(void* ev);
+/* Timing events that survive CUDA-graph capture: an external record node is
+ * re-recorded on every replay, so kernel durations inside a graphed step are
+ * measured with CUDA events on the launching stream. */
+int zi_event_create_timed(void** ev);
+int zi_event_record_external(void* ev, void* stream);
+int zi_event_elapsed_ms(void* ev0, void* ev1, float* ms);
 int zi_event_record(void* ev, void* stream);
 int zi_event_query(void* ev);                         /* ZI_OK done, ZI_ENOTFOUND pending */
 int zi_event_sync(void* ev);

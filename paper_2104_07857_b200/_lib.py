@@ -66,6 +66,9 @@ SIGNATURES = {
     "zi_memcpy_async": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],
     "zi_event_create": [ctypes.POINTER(c_void_p)],
     "zi_event_destroy": [c_void_p],
+    "zi_event_create_timed": [ctypes.POINTER(c_void_p)],
+    "zi_event_record_external": [c_void_p, c_void_p],
+    "zi_event_elapsed_ms": [c_void_p, c_void_p, ctypes.POINTER(c_float)],
     "zi_event_record": [c_void_p, c_void_p],
     "zi_event_query": [c_void_p],
     "zi_event_sync": [c_void_p],

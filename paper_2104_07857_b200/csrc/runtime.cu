@@ -71,6 +71,32 @@ int zi_event_create(void** ev) {
   return ZI_OK;
 }
 
+int zi_event_create_timed(void** ev) {
+  ZI_CHECK_ARG(ev != nullptr, "zi_event_create_timed: NULL");
+  cudaEvent_t e;
+  ZI_CUDA(cudaEventCreate(&e), "cudaEventCreate");
+  *ev = (void*)e;
+  return ZI_OK;
+}
+
+int zi_event_record_external(void* ev, void* stream) {
+  ZI_CHECK_ARG(ev != nullptr, "zi_event_record_external: NULL event");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  ZI_CUDA(cudaStreamIsCapturing((cudaStream_t)stream, &cs), "cudaStreamIsCapturing");
+  if (cs == cudaStreamCaptureStatusActive)   // an external record node in the graph
+    ZI_CUDA(cudaEventRecordWithFlags((cudaEvent_t)ev, (cudaStream_t)stream, cudaEventRecordExternal),
+            "cudaEventRecordWithFlags(external)");
+  else
+    ZI_CUDA(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream), "cudaEventRecord");
+  return ZI_OK;
+}
+
+int zi_event_elapsed_ms(void* ev0, void* ev1, float* ms) {
+  ZI_CHECK_ARG(ev0 && ev1 && ms, "zi_event_elapsed_ms: NULL");
+  ZI_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)ev0, (cudaEvent_t)ev1), "cudaEventElapsedTime");
+  return ZI_OK;
+}
+
 int zi_event_destroy(void* ev) {
   if (!ev) return ZI_OK;
   ZI_CUDA(cudaEventDestroy((cudaEvent_t)ev), "cudaEventDestroy");

@@ -564,7 +564,7 @@ class GPTZeroEngine:
         loss = torch.empty((), dtype=torch.float32, device=x.device)
         kernels.softmax_ce(logits, tgt, rows, loss, 1.0 / T)
         dlog = logits
-        wte_acc.copy_(torch.ops.aten.mm.dtype(dlog.t(), hf, torch.float32))
+        torch.ops.aten.mm.dtype_out(dlog.t(), hf, torch.float32, out=wte_acc)  # fp32 out, no copy
         dhf = torch.mm(dlog, PE["wte"])
         del logits, dlog
         dx = torch.empty_like(dhf)
@@ -794,10 +794,14 @@ class GPTZeroEngine:
             tok = batches[li][0].reshape(-1)
             acc = self.wte_acc[li]
             acc.index_add_(0, tok, xs[li].float())
-            dwpe = torch.zeros(c.seq, c.hd, dtype=torch.float32, device=self.dev)
-            dwpe[: c.seq] = xs[li].float().view(c.batch, c.seq, c.hd).sum(0)
-            G["wte"].copy_(acc)
-            G["wpe"].copy_(dwpe)
+            dwpe = xs[li].view(c.batch, c.seq, c.hd).sum(0, dtype=torch.float32)
+            if G["wte"].dtype == torch.float32:
+                G["wte"].copy_(acc)
+                G["wpe"].copy_(dwpe)
+            else:  # fp32 accumulators -> RNE half contributions
+                kernels.cast_f32_to_half(acc.view(-1), G["wte"].view(-1))
+                kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
+                self.launches += 2
             self._finish_grad(li, E, 0, flat)
         self._reduce_update(E, 0, consts)
         if self.offload:  # the step ends when the last optimizer chunk is back in host DRAM
@@ -826,8 +830,18 @@ class GPTZeroEngine:
             if self.trace:
                 raise ValueError("tracing is not supported under graph capture")
             self._static = [(t.clone(), y.clone()) for t, y in batches]
-            for _ in range(2):       # warm cuBLAS / cuDNN plans and the allocator
+            # warm cuBLAS / cuDNN plans and the allocator with two eager steps on a
+            # snapshot of the model state, then restore it: every call of
+            # step_graphed is exactly one training step
+            state = [self.p16, self.p32, self.m, self.v, self.adam.step, self.adam.consts]
+            snap = [s.clone() for s in state]
+            for _ in range(2):
                 self.step(self._static)
+            torch.cuda.synchronize()
+            for s, c in zip(state, snap):
+                s.copy_(c)
+            del snap
+            self.t -= 2
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             l0, t0 = self.launches, self.t

@@ -92,6 +92,29 @@ def rs_adam(contribs, shard_offset: int, shard_elems: int, contrib_len: int, sca
               consts, _stream(stream))
 
 
+class GraphTimer:
+    """A pair of timing events recorded as external nodes (valid inside CUDA graphs)."""
+
+    def __init__(self):
+        import ctypes
+        self._c = ctypes
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("zi_event_create_timed", ctypes.byref(a))
+        _lib.call("zi_event_create_timed", ctypes.byref(b))
+        self.ev = (a.value, b.value)
+
+    def start(self, stream=None):
+        _lib.call("zi_event_record_external", self.ev[0], _stream(stream))
+
+    def stop(self, stream=None):
+        _lib.call("zi_event_record_external", self.ev[1], _stream(stream))
+
+    def ms(self) -> float:
+        v = self._c.c_float()
+        _lib.call("zi_event_elapsed_ms", self.ev[0], self.ev[1], self._c.byref(v))
+        return v.value
+
+
 class DeviceAdamState:
     """Device-resident step counter + folded Adam constants (zi_adam_advance)."""
 
