@@ -97,9 +97,7 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.backend = dist.get_backend(group)
-        self._flags = None
-        self._flag_ptrs = None
-        self._epoch = 0
+        self._chan: dict = {}   # barrier channel -> [flags tensor, peer flag pointers, epoch]
         self._opened: dict[bytes, int] = {}
         self._owned: dict[int, int] = {}   # base pointer -> bytes of our shareable buffers
 
@@ -158,17 +156,24 @@ class DistComm:
             ptrs.append(pbase + off)
         return ptrs
 
-    def device_barrier(self, stream=None) -> None:
-        """zi_barrier over IPC flag words (orders P2P reads with peer writers)."""
+    def device_barrier(self, stream=None, channel: int = 0) -> None:
+        """zi_barrier over IPC flag words (orders P2P reads with peer writers).
+
+        Each channel has its own flag array and epoch counter: barriers issued
+        on different CUDA streams (compute vs gather) must not share one, or
+        an epoch reached on one stream would release waiters on the other.
+        Every rank must issue the barriers of a channel in the same order.
+        """
         if self.world == 1:
             return
-        if self._flags is None:
-            self._flags = self.alloc((self.world,), torch.int32)
-            self._flag_ptrs = self.share(self._flags)
-        self._epoch += 1
+        if channel not in self._chan:   # collective on first use of the channel
+            flags = self.alloc((self.world,), torch.int32)
+            self._chan[channel] = [flags, self.share(flags), 0]
+        ch = self._chan[channel]
+        ch[2] += 1
         s = stream if stream is not None else torch.cuda.current_stream()
-        _lib.call("zi_barrier", _lib.ptr_array(self._flag_ptrs), self.world, self.rank,
-                  self._epoch, s.cuda_stream)
+        _lib.call("zi_barrier", _lib.ptr_array(ch[1]), self.world, self.rank, ch[2],
+                  s.cuda_stream)
 
     def barrier(self, stream=None) -> None:
         if self.backend == "nccl":

@@ -168,9 +168,9 @@ class GPTZeroEngine:
         self.half = half_dtype
         self.cdt = compute_dtype or half_dtype
         self.placement = placement or Placement()
-        if self.placement.optim is not TierKind.DEVICE or self.placement.params is not TierKind.DEVICE:
-            if not self.comm.is_local and self.N > 1 and self.placement.params is not TierKind.DEVICE:
-                raise NotImplementedError("host-resident params need the cg staging ring (multi-process)")
+        for t in (self.placement.params, self.placement.optim):
+            if t not in (TierKind.DEVICE, TierKind.HOST):
+                raise NotImplementedError("GPT engine tiers: DEVICE or HOST (NVMe: harness / store)")
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
         self.prefetch = prefetch
@@ -313,7 +313,13 @@ class GPTZeroEngine:
         if not self.comm.is_local and self.N > 1:
             self.peer_gslots = [self.comm.share(self.gslots[0][k]) for k in range(2)]
             self.peer_gembed = self.comm.share(self.gembed[0])
-            self.peer_p16 = self.comm.share(self.p16[0])
+            if self.placement.params is TierKind.HOST:
+                # cg staging slots (embed + 2-slot ring) that peers gather from
+                shmax = max(b.shard for b in self.buckets)
+                self.pstage = [self.comm.alloc((shmax,), self.half) for _ in range(3)]
+                self.peer_pstage = [self.comm.share(s) for s in self.pstage]
+            else:
+                self.peer_p16 = self.comm.share(self.p16[0])
         self.events = {}
         # offload engine: double-buffered HBM staging for optimizer-state chunks
         self.offload = self.placement.optim is TierKind.HOST
@@ -366,6 +372,18 @@ class GPTZeroEngine:
                 kernels.allgather(shards, b.shard, dst, b.numel,
                                   use_copy_engine=self.copy_engine_gather or
                                   self.placement.params is TierKind.HOST)
+            elif self.placement.params is TierKind.HOST:
+                # ZeRO-Infinity fetch (PAPER §6.2): cg = H2D of our pinned shard into an
+                # IPC-shared HBM staging slot, then gg = P2P gather of every rank's slot.
+                # The gather-channel barrier before the gg makes all ranks' cg visible; the
+                # next fetch's barrier keeps a slot from being refilled while peers read it.
+                k = 0 if b.key == "embed" else 1 + slot
+                stage = self.pstage[k]
+                stage[:b.shard].copy_(self._shard_view(self.p16, 0, b), non_blocking=True)
+                self.comm.device_barrier(stream, channel=1)
+                kernels.allgather(self.peer_pstage[k], b.shard, dst, b.numel,
+                                  use_copy_engine=self.copy_engine_gather)
+                self.launches += 1
             else:
                 base = b.arena_off * self.p16.element_size()
                 ptrs = [p + base for p in self.peer_p16]
@@ -608,11 +626,16 @@ class GPTZeroEngine:
         if self.offload:
             self._reduce_update_offload(b, slot, consts, contribs, scale)
             return
+        host_params = self.placement.params is TierKind.HOST
         for li, r in enumerate(self.ranks):
+            p16 = self._shard_view(self.p16, li, b)
+            ph = torch.empty(b.shard, dtype=self.half, device=self.dev) if host_params else p16
             kernels.rs_adam_dc(contribs, r * b.shard, b.shard, b.numel, scale,
                                self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
-                               self._shard_view(self.v, li, b), self._shard_view(self.p16, li, b),
+                               self._shard_view(self.v, li, b), ph,
                                self.adam, g_out=self._gout(li, b))
+            if host_params:  # updated bf16 shard back to its pinned home (D2H)
+                p16.copy_(ph, non_blocking=True)
             self.launches += 1
 
     def _reduce_update_offload(self, b: Bucket, slot: int, consts, contribs, scale: float):

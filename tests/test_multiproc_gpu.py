@@ -27,7 +27,14 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, q):
+def _placement(name):
+    from paper_2104_07857_b200.gpt import Placement
+    from paper_2104_07857_b200.store import TierKind
+    D, H = TierKind.DEVICE, TierKind.HOST
+    return {"hbm": Placement(D, D), "params_host": Placement(H, D), "all_host": Placement(H, H)}[name]
+
+
+def _rank_main(rank, world, port, q, placement="hbm"):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -37,7 +44,8 @@ def _rank_main(rank, world, port, q):
         from paper_2104_07857_b200.comm import DistComm
         c = eg.GPTConfig(nl=2, hd=128, heads=2, seq=64, vocab=256, batch=2)
         comm = DistComm()
-        eng = eg.GPTZeroEngine(c, comm, lr=1e-3)
+        eng = eg.GPTZeroEngine(c, comm, lr=1e-3, placement=_placement(placement),
+                               offload_chunk=20_000)
         losses = []
         for step in range(2):
             losses.append(eng.step([eg.synthetic_tokens(c, 7, rank, step)]).item())
@@ -52,14 +60,16 @@ def _rank_main(rank, world, port, q):
         q.put((rank, "error", traceback.format_exc()))
 
 
-def test_two_processes_match_local_comm():
+@pytest.mark.parametrize("placement", ["hbm", "params_host", "all_host"])
+def test_two_processes_match_local_comm(placement):
     from paper_2104_07857_b200 import gpt as eg
     from paper_2104_07857_b200.comm import LocalComm
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, placement))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
