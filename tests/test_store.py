@@ -76,6 +76,25 @@ def test_script_matches_reference(tmp_path, device_tier):
     st.close()
 
 
+@pytest.mark.parametrize("tier", ["host", "nvme"])
+def test_read_into_write_from(tmp_path, tier):
+    """Engine extensions: range I/O into / from caller tensors, same bytes as read_range."""
+    T = S.TierKind(tier)
+    st = S.TierStore(0, 1 << 20, nvme_root=str(tmp_path), sync_io=True)
+    a = np.arange(1000, dtype=np.float32)
+    st.flush([st.write("k", a, T)])
+    out = torch.empty(100, dtype=torch.float32)
+    st.flush([st.read_into("k", T, out, start=250)])
+    assert np.array_equal(out.numpy(), a[250:350])
+    st.flush([st.write_from("k", T, 10, torch.full((5,), -1.0))])
+    assert np.array_equal(st.read_range("k", T, 8, 9).wait().numpy(),
+                          np.array([8, 9, -1, -1, -1, -1, -1, 15, 16], np.float32))
+    with pytest.raises(ValueError):
+        st.read_into("k", T, torch.empty(10, dtype=torch.float64))
+    with pytest.raises(S.KeyNotFound):
+        st.read_into("nope", T, out)
+
+
 def test_buffer_pool_contract():
     p = S.BufferPool(buffer_bytes=16, buffer_count=2, blocking=False, pinned=False)
     a, b = p.acquire(), p.acquire()
