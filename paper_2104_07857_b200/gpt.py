@@ -156,7 +156,8 @@ class GPTZeroEngine:
                  placement: Placement | None = None,
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool = False,
-                 trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True):
+                 trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
+                 overlap_opt: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -323,7 +324,9 @@ class GPTZeroEngine:
         self.events = {}
         # offload engine: double-buffered HBM staging for optimizer-state chunks
         self.offload = self.placement.optim is TierKind.HOST
-        self.opt_stream = torch.cuda.Stream(self.dev) if self.offload else None
+        self.opt_stream = torch.cuda.Stream(self.dev)
+        self.overlap_opt = overlap_opt
+        self._pending_free = None
         self.gfree = {}          # grad slot -> event: optimizer finished reading it
         if self.offload:
             C = self.offload_chunk
@@ -612,31 +615,52 @@ class GPTZeroEngine:
             dst[b.numel:b.shard * self.N].zero_()
 
     def _reduce_update(self, b: Bucket, slot: int, consts):
-        """zi_rs_adam for every local rank's shard of bucket b."""
+        """zi_rs_adam for every local rank's shard of bucket b.
+
+        Runs on the optimizer stream, overlapped with the next bucket's backward
+        GEMMs (PAPER §6.2: reduce-scatter of op i+1 || compute of op i): the
+        fused RS + Adam is HBM-bound, the GEMMs tensor-bound. The gradient slot
+        is handed back through ``gfree``; with peers (DistComm) it is free only
+        once every rank finished reading it, i.e. after the next bucket's
+        opt-stream barrier (channel 2), which follows each rank's RS of b.
+        """
+        cur = torch.cuda.current_stream()
+        os_ = self.opt_stream if self.overlap_opt else cur
+        if os_ is not cur:
+            os_.wait_stream(cur)              # bucket b's gradients are complete
+        key = "embed" if b.key == "embed" else slot
         if self.comm.is_local:
             contribs = [self._contrib(li, b, slot) for li in range(len(self.ranks))]
         else:
-            self.comm.device_barrier()
+            self.comm.device_barrier(os_, channel=2)
             self.launches += 1
-            if b.key == "embed":
-                contribs = list(self.peer_gembed)
-            else:
-                contribs = list(self.peer_gslots[slot])
+            if self._pending_free is not None:   # peers are done with the previous slot
+                ev = torch.cuda.Event()
+                ev.record(os_)
+                self.gfree[self._pending_free] = ev
+            self._pending_free = key
+            contribs = list(self.peer_gembed) if b.key == "embed" else list(self.peer_gslots[slot])
         scale = 1.0 / self.N
         if self.offload:
             self._reduce_update_offload(b, slot, consts, contribs, scale)
             return
         host_params = self.placement.params is TierKind.HOST
-        for li, r in enumerate(self.ranks):
-            p16 = self._shard_view(self.p16, li, b)
-            ph = torch.empty(b.shard, dtype=self.half, device=self.dev) if host_params else p16
-            kernels.rs_adam_dc(contribs, r * b.shard, b.shard, b.numel, scale,
-                               self._shard_view(self.p32, li, b), self._shard_view(self.m, li, b),
-                               self._shard_view(self.v, li, b), ph,
-                               self.adam, g_out=self._gout(li, b))
-            if host_params:  # updated bf16 shard back to its pinned home (D2H)
-                p16.copy_(ph, non_blocking=True)
-            self.launches += 1
+        with torch.cuda.stream(os_):
+            for li, r in enumerate(self.ranks):
+                p16 = self._shard_view(self.p16, li, b)
+                ph = torch.empty(b.shard, dtype=self.half, device=self.dev) if host_params else p16
+                kernels.rs_adam_dc(contribs, r * b.shard, b.shard, b.numel, scale,
+                                   self._shard_view(self.p32, li, b),
+                                   self._shard_view(self.m, li, b),
+                                   self._shard_view(self.v, li, b), ph,
+                                   self.adam, g_out=self._gout(li, b))
+                if host_params:  # updated bf16 shard back to its pinned home (D2H)
+                    p16.copy_(ph, non_blocking=True)
+                self.launches += 1
+            if self.comm.is_local and os_ is not cur:
+                ev = torch.cuda.Event()
+                ev.record(os_)
+                self.gfree[key] = ev
 
     def _reduce_update_offload(self, b: Bucket, slot: int, consts, contribs, scale: float):
         """Optimizer states in pinned host DRAM (PAPER §5.1.1).
@@ -747,6 +771,7 @@ class GPTZeroEngine:
         if self.offload:
             self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
         self._spans = []
+        self._pending_free = None
         self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
@@ -827,8 +852,8 @@ class GPTZeroEngine:
                 self.launches += 2
             self._finish_grad(li, E, 0, flat)
         self._reduce_update(E, 0, consts)
-        if self.offload:  # the step ends when the last optimizer chunk is back in host DRAM
-            cur.wait_stream(self.opt_stream)
+        cur.wait_stream(self.opt_stream)  # the step ends when the last bucket is updated
+        if self.offload:  # ... and its optimizer chunks are back in host DRAM
             cur.wait_stream(self.d2h_stream)
             cur.wait_stream(self.h2d_stream)
         if gs is not cur:
