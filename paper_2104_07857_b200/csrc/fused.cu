@@ -187,98 +187,102 @@ ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x
   }
 }
 
-// dgamma / dbeta partials over a chunk of rows: thread owns 8 columns,
-// acc_g += dy * (x - mean) * rstd, acc_b += dy.
-__global__ void __launch_bounds__(256)
-ln_bwd_gb_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
-                 const float* __restrict__ mean, const float* __restrict__ rstd,
-                 float* __restrict__ part_g, float* __restrict__ part_b, int T, int H,
-                 int rows_per) {
-  const int c8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c8 >= H) return;
-  const int r0 = blockIdx.y * rows_per;
-  const int r1 = min(T, r0 + rows_per);
-  float ag[8], ab[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) ag[j] = ab[j] = 0.f;
-#pragma unroll 4
-  for (int row = r0; row < r1; ++row) {
-    float g[8], xv[8];
-    ld_row<8>(dy + (size_t)row * H + c8, g);
-    ld_row<8>(x + (size_t)row * H + c8, xv);
-    const float mu = mean[row], rs = rstd[row];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      ag[j] += g[j] * (xv[j] - mu) * rs;
-      ab[j] += g[j];
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    part_g[(size_t)blockIdx.y * H + c8 + j] = ag[j];
-    part_b[(size_t)blockIdx.y * H + c8 + j] = ab[j];
-  }
-}
+// Column reductions (bias grads, GELU-bwd + bias grad, LayerNorm dgamma/dbeta).
+// CTA = 64 columns (8 threads x 8) x 32 row groups; blockIdx.y = chunk of rows.
+// Each thread folds rows rg, rg+32, ... of its chunk; the CTA folds its 32 row
+// groups in order into one partial row; the last CTA of a column block (atomic
+// counter, self-resetting so CUDA graphs replay it) folds the chunk partials in
+// chunk order and writes the result. Deterministic, one launch, no finish kernel.
+//   MODE 0: out0 = sum a                          (bias grad)
+//   MODE 1: du = gelu_tanh'(u) * a -> d; out0 = sum du   (GELU bwd + fc1 bias grad)
+//   MODE 2: out0 = sum a * (u - mean) * rstd, out1 = sum a   (LN dgamma, dbeta)
+constexpr int CR_COLS = 64, CR_RG = 32;
 
-// Column partial sums over a chunk of rows: thread owns 8 columns. If GELU,
-// du = gelu_tanh'(u) * da is computed, stored to out, and summed.
-template <bool GELU>
+template <int MODE>
 __global__ void __launch_bounds__(256)
-colsum_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
-              uint16_t* __restrict__ out, float* __restrict__ part, int T, int N, int rows_per) {
-  const int c8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c8 >= N) return;
-  const int r0 = blockIdx.y * rows_per;
-  const int r1 = min(T, r0 + rows_per);
-  float acc[8];
+colred_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
+              uint16_t* __restrict__ d, const float* __restrict__ mean,
+              const float* __restrict__ rstd, float* __restrict__ part, int* __restrict__ counters,
+              void* __restrict__ out0, void* __restrict__ out1, int out_f32, int T, int N,
+              int rows_per) {
+  constexpr int NO = MODE == 2 ? 2 : 1;
+  __shared__ float red[NO][CR_RG][CR_COLS + 1];
+  __shared__ int last;
+  const int cx = threadIdx.x & 7, rg = threadIdx.x >> 3;
+  const int c8 = blockIdx.x * CR_COLS + cx * 8;
+  const bool colok = c8 < N;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
+  float acc[NO][8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[o][j] = 0.f;
+  if (colok) {
 #pragma unroll 4
-  for (int row = r0; row < r1; ++row) {
-    float v[8];
-    ld_row<8>(a + (size_t)row * N + c8, v);
-    if (GELU) {
-      float uv[8];
-      ld_row<8>(u + (size_t)row * N + c8, uv);
+    for (int row = r0 + rg; row < r1; row += CR_RG) {
+      const size_t off = (size_t)row * N + c8;
+      float v[8];
+      ld_row<8>(a + off, v);
+      if (MODE == 1) {
+        float uv[8];
+        ld_row<8>(u + off, uv);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float z = uv[j];
-        const float c = 0.7978845608028654f;
-        const float th = tanhf(c * (z + 0.044715f * z * z * z));
-        const float dg = 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * c * (1.f + 3.f * 0.044715f * z * z);
-        v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * dg));
+        for (int j = 0; j < 8; ++j) {
+          const float z = uv[j];
+          const float c = 0.7978845608028654f;
+          const float th = tanhf(c * (z + 0.044715f * z * z * z));
+          const float dg = 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * c * (1.f + 3.f * 0.044715f * z * z);
+          v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * dg));
+        }
+        st_row<8>(d + off, v);
       }
-      st_row<8>(out + (size_t)row * N + c8, v);
+      if (MODE == 2) {
+        float xv[8];
+        ld_row<8>(u + off, xv);
+        const float mu = mean[row], rs = rstd[row];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc[0][j] += v[j] * (xv[j] - mu) * rs;
+          acc[NO - 1][j] += v[j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[0][j] += v[j];
+      }
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += v[j];
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) part[(size_t)blockIdx.y * N + c8 + j] = acc[j];
-}
-
-// partials [P x N] -> out[N]: CTA = 32 columns x 8 row groups; group k sums
-// rows p = k, k+8, ... in order, then the 8 group sums fold in order (deterministic).
-__global__ void __launch_bounds__(256)
-colsum_finish_kernel(const float* __restrict__ part, int P, int N, void* __restrict__ out,
-                     int out_f32) {
-  __shared__ float sm[8][33];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + tx;
-  float s = 0.f;
-  if (c < N) {
-#pragma unroll 4
-    for (int p = ty; p < P; p += 8) s += part[(size_t)p * N + c];
-  }
-  sm[ty][tx] = s;
+  for (int o = 0; o < NO; ++o)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[o][rg][cx * 8 + j] = acc[o][j];
   __syncthreads();
-  if (ty == 0 && c < N) {
+  // fold the 32 row groups (fixed order) -> this chunk's partial row
+  if (threadIdx.x < CR_COLS * NO) {
+    const int o = threadIdx.x / CR_COLS, col = threadIdx.x % CR_COLS;
+    const int gc = blockIdx.x * CR_COLS + col;
     float t = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t += sm[k][tx];
-    if (out_f32) static_cast<float*>(out)[c] = t;
-    else static_cast<uint16_t*>(out)[c] = tobf(t);
+#pragma unroll 8
+    for (int k = 0; k < CR_RG; ++k) t += red[o][k][col];
+    if (gc < N) part[((size_t)o * gridDim.y + blockIdx.y) * N + gc] = t;
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1) == (int)gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < CR_COLS * NO) {
+    const int o = threadIdx.x / CR_COLS, col = threadIdx.x % CR_COLS;
+    const int gc = blockIdx.x * CR_COLS + col;
+    if (gc < N) {
+      float t = 0.f;
+      for (int p = 0; p < (int)gridDim.y; ++p) t += __ldcg(&part[((size_t)o * gridDim.y + p) * N + gc]);
+      void* dst = o == 0 ? out0 : out1;
+      if (out_f32) static_cast<float*>(dst)[gc] = t;
+      else static_cast<uint16_t*>(dst)[gc] = tobf(t);
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0;   // ready for the next launch / replay
 }
 
 // One CTA per row of V logits (bf16, in place): lse, loss_row = lse - l[t],
@@ -413,59 +417,57 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
   return zi::launch_status("zi_ln_fwd");
 }
 
+// work layout: [0, 1024) int counters (zeroed once, self-resetting), then partials
+static int launch_colred(int mode, const void* a, const void* u, void* d, const float* mean,
+                         const float* rstd, void* out0, void* out1, int out_f32, float* work,
+                         size_t work_elems, int T, int N, cudaStream_t s, const char* name) {
+  ZI_CHECK_ARG(N % 8 == 0, "%s: N must be a multiple of 8", name);
+  const int cblocks = (N + CR_COLS - 1) / CR_COLS;
+  ZI_CHECK_ARG(cblocks <= 1024, "%s: N too large for the counter block", name);
+  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
+  const int max_chunks = (T + CR_RG - 1) / CR_RG;
+  if (chunks > max_chunks) chunks = max_chunks;
+  if (chunks < 1) chunks = 1;
+  const int rows_per = (T + chunks - 1) / chunks;
+  chunks = (T + rows_per - 1) / rows_per;
+  const size_t need = 1024 + (size_t)(mode == 2 ? 2 : 1) * chunks * N;
+  ZI_CHECK_ARG(work_elems >= need, "%s: work needs %zu floats", name, need);
+  int* counters = reinterpret_cast<int*>(work);
+  float* part = work + 1024;
+  dim3 grid(cblocks, chunks);
+  const uint16_t* A = static_cast<const uint16_t*>(a);
+  const uint16_t* U = static_cast<const uint16_t*>(u);
+  uint16_t* D = static_cast<uint16_t*>(d);
+  if (mode == 0)
+    colred_kernel<0><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
+  else if (mode == 1)
+    colred_kernel<1><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
+  else
+    colred_kernel<2><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
+  return zi::launch_status(name);
+}
+
 int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
               const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
               size_t work_elems, int T, int H, void* stream) {
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
-  ZI_CHECK_ARG(H % 8 == 0, "zi_ln_bwd: H must be a multiple of 8");
-  cudaStream_t s = (cudaStream_t)stream;
   ZI_CHECK_ARG(H >= 128 && H <= 2048 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..2048, power of 2");
+  cudaStream_t s = (cudaStream_t)stream;
   const int grid = ln_grid(T, H);
   TPR_DISPATCH(H, ln_bwd_dx_kernel, grid, s, (const uint16_t*)dy, (const uint16_t*)x,
                (const uint16_t*)w, mean, rstd, (const uint16_t*)dres, (uint16_t*)dx, T);
   int st = zi::launch_status("zi_ln_bwd(dx)");
   if (st) return st;
-  const int cblocks = (H / 8 + 255) / 256;
-  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
-  if (chunks > T) chunks = T;
-  const int rows_per = (T + chunks - 1) / chunks;
-  chunks = (T + rows_per - 1) / rows_per;
-  ZI_CHECK_ARG(work_elems >= 2 * (size_t)chunks * H, "zi_ln_bwd: work needs %zu floats",
-               2 * (size_t)chunks * H);
-  float* pg = work;
-  float* pb = work + (size_t)chunks * H;
-  ln_bwd_gb_kernel<<<dim3(cblocks, chunks), 256, 0, s>>>((const uint16_t*)dy, (const uint16_t*)x,
-                                                         mean, rstd, pg, pb, T, H, rows_per);
-  st = zi::launch_status("zi_ln_bwd(gamma/beta)");
-  if (st) return st;
-  colsum_finish_kernel<<<(H + 31) / 32, 256, 0, s>>>(pg, chunks, H, dgamma, grads_f32);
-  colsum_finish_kernel<<<(H + 31) / 32, 256, 0, s>>>(pb, chunks, H, dbeta, grads_f32);
-  return zi::launch_status("zi_ln_bwd(finish)");
+  return launch_colred(2, dy, x, nullptr, mean, rstd, dgamma, dbeta, grads_f32, work, work_elems,
+                       T, H, s, "zi_ln_bwd(gamma/beta)");
 }
 
 int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, float* work,
                  size_t work_elems, int T, int N, void* stream) {
-  ZI_CHECK_ARG(dy && db && work && T > 0 && N > 0 && N % 8 == 0, "zi_bias_grad: bad arguments");
+  ZI_CHECK_ARG(dy && db && work && T > 0 && N > 0, "zi_bias_grad: bad arguments");
   ZI_CHECK_ARG(!u || du, "zi_bias_grad: gelu backward needs du");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int cblocks = (N / 8 + 255) / 256;
-  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
-  if (chunks > T) chunks = T;
-  const int rows_per = (T + chunks - 1) / chunks;
-  chunks = (T + rows_per - 1) / rows_per;
-  ZI_CHECK_ARG(work_elems >= (size_t)chunks * N, "zi_bias_grad: work needs %zu floats",
-               (size_t)chunks * N);
-  dim3 grid(cblocks, chunks);
-  if (u)
-    colsum_kernel<true><<<grid, 256, 0, s>>>((const uint16_t*)dy, (const uint16_t*)u,
-                                             (uint16_t*)du, work, T, N, rows_per);
-  else
-    colsum_kernel<false><<<grid, 256, 0, s>>>((const uint16_t*)dy, nullptr, nullptr, work, T, N,
-                                              rows_per);
-  int st = zi::launch_status("zi_bias_grad");
-  if (st) return st;
-  colsum_finish_kernel<<<(N + 31) / 32, 256, 0, s>>>(work, chunks, N, db, db_f32);
-  return zi::launch_status("zi_bias_grad(finish)");
+  return launch_colred(u ? 1 : 0, dy, u, du, nullptr, nullptr, db, nullptr, db_f32, work,
+                       work_elems, T, N, (cudaStream_t)stream, "zi_bias_grad");
 }
 
 int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T, int V,

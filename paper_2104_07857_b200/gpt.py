@@ -174,6 +174,7 @@ class GPTZeroEngine:
                 raise NotImplementedError("GPT engine tiers: DEVICE or HOST (NVMe: harness / store)")
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
+        self.overlap_opt = overlap_opt
         self.prefetch = prefetch
         self.copy_engine_gather = copy_engine_gather
         self.dev = torch.device("cuda", torch.cuda.current_device())
@@ -325,7 +326,6 @@ class GPTZeroEngine:
         # offload engine: double-buffered HBM staging for optimizer-state chunks
         self.offload = self.placement.optim is TierKind.HOST
         self.opt_stream = torch.cuda.Stream(self.dev)
-        self.overlap_opt = overlap_opt
         self._pending_free = None
         self.gfree = {}          # grad slot -> event: optimizer finished reading it
         if self.offload:
@@ -772,6 +772,10 @@ class GPTZeroEngine:
             self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
         self._spans = []
         self._pending_free = None
+        # events of the previous step are complete (cur joined every side stream at its
+        # end) and must not leak into a graph capture
+        self.gfree.clear()
+        self.events.clear()
         self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]

@@ -214,10 +214,12 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, accumul
 
 
 class Workspace:
-    """fp32 scratch for the deterministic column reductions (per-CTA partials)."""
+    """fp32 scratch for the deterministic column reductions: 1024 self-resetting int
+    counters (zeroed here once) followed by per-chunk partial rows. Use one workspace
+    per stream: reductions sharing it must be stream-ordered."""
 
     def __init__(self, elems: int = 4 << 20, device="cuda"):
-        self.t = torch.empty(elems, dtype=torch.float32, device=device)
+        self.t = torch.zeros(elems, dtype=torch.float32, device=device)
 
     @property
     def ptr(self) -> int:
