@@ -249,6 +249,14 @@ def run_ours(args):
         e2e_ms = comm.allreduce_max(e2e_ms)
     e2e_tflops = flops * world / (e2e_ms / args.steps / 1e3) / 1e12
 
+    # ---------------- collectives over NVLink (N > 1): bus GB/s of the step's AG / RS
+    collectives = None
+    if world > 1:
+        try:
+            collectives = collective_leg(eng, comm)
+        except Exception as e:  # noqa: BLE001 — report, never lose the main line
+            collectives = {"error": repr(e)[:300]}
+
     # ---------------- offload leg: fp32 optimizer state in pinned host DRAM
     offload = None
     if world == 1 and not args.no_offload:
@@ -293,12 +301,61 @@ def run_ours(args):
                          "traffic": None},
             "clocks": clocks.summary(),
             "offload": offload,
+            "collectives": collectives,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def collective_leg(eng, comm, iters: int = 10) -> dict:
+    """Bus GB/s of the step's collectives on one block bucket (bf16, ~100 MB at 1.3B):
+    the P2P all-gather (zi_allgather pulling every peer's shard over NVLink), the
+    fused P2P reduce-scatter (zi_reduce_scatter_cast folding the peers' gradient
+    buckets in rank order) and NCCL's all_gather_into_tensor for reference.
+    bus bytes = S * (N-1) / N per rank (S = full bucket bytes); max time over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2104_07857_b200 import kernels as K
+    N = comm.world
+    b = eng.by_key["h0"]
+    S = b.numel * 2
+    full = torch.empty(b.shard * N, dtype=torch.bfloat16, device="cuda")
+    shard32 = torch.empty(b.shard, dtype=torch.float32, device="cuda")
+    p16_ptrs = [p + b.arena_off * 2 for p in eng.peer_p16] if hasattr(eng, "peer_p16") else None
+    g_ptrs = list(eng.peer_gslots[0])
+    out = {"bucket_bytes": S, "n_ranks": N}
+
+    def timed(fn):
+        comm.device_barrier(channel=3)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return comm.allreduce_max(e0.elapsed_time(e1) / iters)
+
+    def bus(ms):
+        return round(S * (N - 1) / N / (ms / 1e3) / 1e9, 1)
+
+    if p16_ptrs is not None:
+        ms = timed(lambda: K.allgather(p16_ptrs, b.shard, full, b.numel))
+        out["allgather_p2p_ms"], out["allgather_p2p_busbw_gbs"] = round(ms, 4), bus(ms)
+        ms = timed(lambda: K.allgather(p16_ptrs, b.shard, full, b.numel, use_copy_engine=True))
+        out["allgather_ce_ms"], out["allgather_ce_busbw_gbs"] = round(ms, 4), bus(ms)
+    r = comm.rank
+    ms = timed(lambda: K.reduce_scatter_cast(g_ptrs, r * b.shard, b.shard, b.numel, 1.0 / N,
+                                             torch.bfloat16, shard32))
+    out["reduce_scatter_p2p_ms"], out["reduce_scatter_p2p_busbw_gbs"] = round(ms, 4), bus(ms)
+    mine = eng.p16[0, b.arena_off:b.arena_off + b.shard]
+    ms = timed(lambda: dist.all_gather_into_tensor(full, mine))
+    out["allgather_nccl_ms"], out["allgather_nccl_busbw_gbs"] = round(ms, 4), bus(ms)
+    out["nvlink_ref_gbs"] = 770.0
+    return out
 
 
 def host_link_peak(nbytes: int = 1 << 30) -> dict:
