@@ -152,9 +152,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # ZINF_BENCH_SAME_GPU=1 (tests only): every rank on cuda:0 with gloo as the
+    # process-group backend, to exercise the multi-process path on one GPU
+    same_gpu = os.environ.get("ZINF_BENCH_SAME_GPU") == "1"
+    torch.cuda.set_device(0 if same_gpu else local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         comm = DistComm()
     else:
         comm = LocalComm(1)
@@ -351,9 +357,10 @@ def collective_leg(eng, comm, iters: int = 10) -> dict:
     ms = timed(lambda: K.reduce_scatter_cast(g_ptrs, r * b.shard, b.shard, b.numel, 1.0 / N,
                                              torch.bfloat16, shard32))
     out["reduce_scatter_p2p_ms"], out["reduce_scatter_p2p_busbw_gbs"] = round(ms, 4), bus(ms)
-    mine = eng.p16[0, b.arena_off:b.arena_off + b.shard]
-    ms = timed(lambda: dist.all_gather_into_tensor(full, mine))
-    out["allgather_nccl_ms"], out["allgather_nccl_busbw_gbs"] = round(ms, 4), bus(ms)
+    if comm.backend == "nccl":
+        mine = eng.p16[0, b.arena_off:b.arena_off + b.shard]
+        ms = timed(lambda: dist.all_gather_into_tensor(full, mine))
+        out["allgather_nccl_ms"], out["allgather_nccl_busbw_gbs"] = round(ms, 4), bus(ms)
     out["nvlink_ref_gbs"] = 770.0
     return out
 
