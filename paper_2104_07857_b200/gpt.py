@@ -157,7 +157,7 @@ class GPTZeroEngine:
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool = False,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
-                 overlap_opt: bool = True):
+                 overlap_opt: bool = True, act_ckpt: str | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -175,6 +175,9 @@ class GPTZeroEngine:
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
         self.overlap_opt = overlap_opt
+        if act_ckpt not in (None, "device", "host"):
+            raise ValueError("act_ckpt must be None, 'device' or 'host'")
+        self.act_ckpt = act_ckpt
         self.prefetch = prefetch
         self.copy_engine_gather = copy_engine_gather
         self.dev = torch.device("cuda", torch.cuda.current_device())
@@ -327,6 +330,17 @@ class GPTZeroEngine:
         self.offload = self.placement.optim is TierKind.HOST
         self.opt_stream = torch.cuda.Stream(self.dev)
         self._pending_free = None
+        # activation checkpoints: block inputs in pinned host DRAM + a 2-slot HBM ring
+        self._ckpt_saved, self._ckpt_loaded, self.ckpt_bytes = {}, {}, 0
+        if self.act_ckpt == "host":
+            from .store import _PinnedBuffer
+            per = c.tokens * c.hd
+            self._ckpt_buf = _PinnedBuffer(nloc * c.nl * per * 2)
+            flat = self._ckpt_buf.tensor.view(torch.bfloat16)
+            self.ckpt_host = [[flat[(li * c.nl + i) * per:(li * c.nl + i + 1) * per]
+                               for i in range(c.nl)] for li in range(nloc)]
+            self.ckpt_ring = [[torch.empty(c.tokens, c.hd, dtype=torch.bfloat16, device=self.dev)
+                               for _ in range(2)] for _ in range(nloc)]
         self.gfree = {}          # grad slot -> event: optimizer finished reading it
         if self.offload:
             C = self.offload_chunk
@@ -738,6 +752,47 @@ class GPTZeroEngine:
         ev_free.record(opt)
         self.gfree["embed" if b.key == "embed" else slot] = ev_free
 
+    # ------------------------------------------------- activation checkpoints (PAPER §5.1.2)
+    def _ckpt_save(self, li: int, i: int, x_in: torch.Tensor):
+        """Keep block i's input as its checkpoint: in HBM, or D2H to pinned host."""
+        if self.act_ckpt == "device":
+            return x_in
+        d2h, cur = self.d2h_stream, torch.cuda.current_stream()
+        d2h.wait_stream(cur)                      # x_in is produced on the compute stream
+        with torch.cuda.stream(d2h):
+            t0 = self._tmark(d2h)
+            self.ckpt_host[li][i].copy_(x_in.view(-1), non_blocking=True)
+            self._tspan(self.buckets[1 + i].op, "grad_offload", t0, self._tmark(d2h))
+            ev = torch.cuda.Event()
+            ev.record(d2h)
+        x_in.record_stream(d2h)                   # no reuse of its memory before the copy
+        self._ckpt_saved[(li, i)] = ev
+        self.ckpt_bytes += x_in.numel() * x_in.element_size()
+        return None
+
+    def _ckpt_prefetch(self, li: int, i: int) -> None:
+        """H2D of block i's checkpoint into its ring slot, one block ahead of use."""
+        h2d, cur = self.h2d_stream, torch.cuda.current_stream()
+        dst = self.ckpt_ring[li][i % 2]
+        h2d.wait_stream(cur)                      # the slot's previous block is recomputed
+        with torch.cuda.stream(h2d):
+            h2d.wait_event(self._ckpt_saved.pop((li, i)))
+            t0 = self._tmark(h2d)
+            dst.view(-1).copy_(self.ckpt_host[li][i], non_blocking=True)
+            self._tspan(self.buckets[1 + i].op, "cg", t0, self._tmark(h2d))
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        self._ckpt_loaded[(li, i)] = ev
+        self.ckpt_bytes += dst.numel() * dst.element_size()
+
+    def _ckpt_get(self, li: int, i: int, cached):
+        if self.act_ckpt == "device":
+            return cached
+        if (li, i) not in self._ckpt_loaded:      # the last block: not prefetched yet
+            self._ckpt_prefetch(li, i)
+        torch.cuda.current_stream().wait_event(self._ckpt_loaded.pop((li, i)))
+        return self.ckpt_ring[li][i % 2]
+
     def _wait_gslot(self, slot) -> None:
         """Before overwriting a gradient slot: the optimizer stream must be done reading it."""
         ev = self.gfree.pop(slot, None)
@@ -776,6 +831,8 @@ class GPTZeroEngine:
         # end) and must not leak into a graph capture
         self.gfree.clear()
         self.events.clear()
+        self._ckpt_saved.clear()
+        self._ckpt_loaded.clear()
         self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
@@ -799,7 +856,10 @@ class GPTZeroEngine:
             P = self._params(b, full)
             c0 = self._tmark(cur)
             for li in range(nloc):
-                xs[li], caches[li][i] = self._block_fwd(xs[li], P)
+                x_in = xs[li]
+                xs[li], caches[li][i] = self._block_fwd(x_in, P)
+                if self.act_ckpt is not None:   # keep only the block input (checkpoint)
+                    caches[li][i] = self._ckpt_save(li, i, x_in)
             self._tspan(b.op, "compute", c0, self._tmark(cur))
         fslot = len(blocks) % 2
         if not blocks:
@@ -831,11 +891,17 @@ class GPTZeroEngine:
                 self._fetch(blocks[j - 1], (j - 1) % 2, gs)
             P = self._params(b, full)
             self._wait_gslot(slot)
+            if self.act_ckpt == "host" and j - 1 >= 0:
+                for li in range(nloc):          # prefetch the next checkpoint (cg lane)
+                    self._ckpt_prefetch(li, j - 1)
             c0 = self._tmark(cur)
             for li in range(nloc):
                 G, flat = self._grad_views(li, b, slot)
-                xs[li] = self._block_bwd(xs[li], caches[li][j], P, G)
-                caches[li][j] = None
+                cache = caches[li][j]
+                if self.act_ckpt is not None:   # recompute the block from its checkpoint
+                    _, cache = self._block_fwd(self._ckpt_get(li, j, cache), P)
+                xs[li] = self._block_bwd(xs[li], cache, P, G)
+                caches[li][j] = cache = None
                 self._finish_grad(li, b, slot, flat)
             self._tspan(b.op, "compute", c0, self._tmark(cur))
             self._reduce_update(b, slot, consts)
@@ -857,7 +923,7 @@ class GPTZeroEngine:
             self._finish_grad(li, E, 0, flat)
         self._reduce_update(E, 0, consts)
         cur.wait_stream(self.opt_stream)  # the step ends when the last bucket is updated
-        if self.offload:  # ... and its optimizer chunks are back in host DRAM
+        if self.offload or self.act_ckpt == "host":  # ... and every host transfer landed
             cur.wait_stream(self.d2h_stream)
             cur.wait_stream(self.h2d_stream)
         if gs is not cur:

@@ -117,6 +117,24 @@ def test_device_adam_constants_match_host_folding():
         assert np.array_equal(st.consts.cpu().numpy(), want), t
 
 
+@pytest.mark.parametrize("mode", ["device", "host"])
+def test_activation_checkpointing_matches(mode):
+    """Recompute from checkpoints (kept in HBM or offloaded to pinned host) gives the
+    same step as keeping every activation."""
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, act_ckpt=mode, trace=(mode == "host"))
+    for step in range(3):
+        bs = batches_for(SMALL, 2, step)
+        la, lb = a.step(bs).item(), b.step(bs).item()
+        assert abs(la - lb) <= 1e-5 * abs(la), (step, la, lb)
+    for key in a.by_key:
+        torch.testing.assert_close(a.shard(key, 1)["p32"], b.shard(key, 1)["p32"], rtol=0, atol=5e-5)
+    if mode == "host":
+        assert b.ckpt_bytes > 0
+        stages = {e[1] for e in b.timeline().events}
+        assert {"cg", "grad_offload", "compute"} <= stages
+
+
 def test_fused_kernels_match_torch_path():
     """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path."""
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True)
