@@ -436,6 +436,31 @@ def offload_leg(cfg, args) -> dict:
                         "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)}}
     del eng
     torch.cuda.empty_cache()
+    # activation checkpoints offloaded to pinned host (PAPER §5.1.2): forward keeps each
+    # block input (D2H), backward prefetches it one block ahead and recomputes the block
+    eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, act_ckpt="host")
+    for w in range(2):
+        eng.step_graphed([bs[w % 2]])
+    torch.cuda.synchronize()
+    t0.record()
+    for s in range(steps):
+        eng.step_graphed([bs[s % 2]])
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    eng.trace = True
+    eng.step([bs[0]])
+    tl = eng.timeline()
+    T, P = cfg.tokens, eg.param_count(cfg)
+    out["act_ckpt_host"] = {
+        "ms_per_step": round(ms, 2),
+        "model_tflops": round(eg.model_flops_per_step(cfg) / (ms / 1e3) / 1e12, 1),
+        "hw_tflops_8TP": round((8.0 * T * P + 8 * 2 * cfg.batch * cfg.seq ** 2 * cfg.hd * cfg.nl)
+                               / (ms / 1e3) / 1e12, 1),
+        "ckpt_bytes_per_step": 2 * cfg.nl * T * cfg.hd * 2,
+        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)}
+    del eng
+    torch.cuda.empty_cache()
     return out
 
 
