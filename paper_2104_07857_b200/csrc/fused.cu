@@ -94,14 +94,21 @@ __device__ __forceinline__ float row_reduce(float v, float* sm) {
   return v;
 }
 
+// CTA size: 256 threads, or one whole row when a row needs more (H = 4096 / 8192)
 template <int TPR>
-__global__ void __launch_bounds__(256)
+struct RowCta {
+  static constexpr int NT = TPR > 256 ? TPR : 256;
+  static constexpr int RPC = NT / TPR;
+};
+
+template <int TPR>
+__global__ void __launch_bounds__(RowCta<TPR>::NT)
 ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
               uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
               const uint16_t* __restrict__ b, uint16_t* __restrict__ y, float* __restrict__ mean,
               float* __restrict__ rstd, int T, float eps) {
-  constexpr int H = 8 * TPR, RPC = 256 / TPR;
-  __shared__ float sm[8];
+  constexpr int H = 8 * TPR, RPC = RowCta<TPR>::RPC;
+  __shared__ float sm[32];
   const int t = threadIdx.x % TPR;
   float wf[8], bv[8];
   ld_row<8>(w + t * 8, wf);
@@ -145,13 +152,13 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
 // dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w,
 // plus dres (residual gradient) if given.
 template <int TPR>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(RowCta<TPR>::NT)
 ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
                  const uint16_t* __restrict__ w, const float* __restrict__ mean,
                  const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
                  uint16_t* __restrict__ dx, int T) {
-  constexpr int H = 8 * TPR, RPC = 256 / TPR;
-  __shared__ float sm[8];
+  constexpr int H = 8 * TPR, RPC = RowCta<TPR>::RPC;
+  __shared__ float sm[32];
   const int t = threadIdx.x % TPR;
   float wf[8];
   ld_row<8>(w + t * 8, wf);
@@ -391,12 +398,15 @@ using namespace zi::fused;
     case 64: KERNEL<64><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
     case 128: KERNEL<128><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
     case 256: KERNEL<256><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    default: zi::set_error("LayerNorm: hidden size %d not in {128..2048, power of 2}", H); \
+    case 512: KERNEL<512><<<GRID, 512, 0, STREAM>>>(__VA_ARGS__); break;                   \
+    case 1024: KERNEL<1024><<<GRID, 1024, 0, STREAM>>>(__VA_ARGS__); break;                \
+    default: zi::set_error("LayerNorm: hidden size %d not in {128..8192, power of 2}", H); \
       return ZI_EINVAL;                                                                    \
   }
 
 static int ln_grid(int T, int H) {
-  const int rpc = 256 / (H / 8);
+  const int tpr = H / 8;
+  const int rpc = tpr >= 256 ? 1 : 256 / tpr;
   const int need = (T + rpc - 1) / rpc;
   const int cap = sm_count() * 8;
   return need < cap ? need : cap;
@@ -409,7 +419,7 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
   ZI_CHECK_ARG(x && w && b && y && mean && rstd && T > 0, "zi_ln_fwd: bad arguments");
   ZI_CHECK_ARG(!resid || xsum, "zi_ln_fwd: resid needs xsum");
   cudaStream_t s = (cudaStream_t)stream;
-  ZI_CHECK_ARG(H >= 128 && H <= 2048 && (H & (H - 1)) == 0, "zi_ln_fwd: H must be 128..2048, power of 2");
+  ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_fwd: H must be 128..8192, power of 2");
   const int grid = ln_grid(T, H);
   TPR_DISPATCH(H, ln_fwd_kernel, grid, s, (const uint16_t*)x, (const uint16_t*)resid,
                (uint16_t*)xsum, (const uint16_t*)w, (const uint16_t*)b, (uint16_t*)y, mean, rstd,
@@ -451,7 +461,7 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
               const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
               size_t work_elems, int T, int H, void* stream) {
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
-  ZI_CHECK_ARG(H >= 128 && H <= 2048 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..2048, power of 2");
+  ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..8192, power of 2");
   cudaStream_t s = (cudaStream_t)stream;
   const int grid = ln_grid(T, H);
   TPR_DISPATCH(H, ln_bwd_dx_kernel, grid, s, (const uint16_t*)dy, (const uint16_t*)x,

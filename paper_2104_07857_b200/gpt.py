@@ -197,7 +197,8 @@ class GPTZeroEngine:
         self.adam = kernels.DeviceAdamState(lr, betas, eps, device=self.dev)
         self._graph = None
         # bf16 path: LayerNorm / bias-grad / GELU-bwd / softmax-CE on libzinf kernels
-        self.fused = (self.cdt == torch.bfloat16 and cfg.hd in (128, 256, 512, 1024, 2048)
+        self.fused = (self.cdt == torch.bfloat16
+                      and cfg.hd in (128, 256, 512, 1024, 2048, 4096, 8192)
                       and fused)
         self.ws = kernels.Workspace(max(4 << 20, 2 * 148 * cfg.hd, 600 * 4 * cfg.hd),
                                     device=self.dev) if self.fused else None

@@ -20,7 +20,8 @@ def close(a, b, rtol=2 ** -7, atol=1e-2):
     assert bad == 0, f"{bad} mismatches, max err {(a - b).abs().max().item()}"
 
 
-@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048), (513, 1024)])
+@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048), (513, 1024), (300, 4096),
+                                 (257, 8192)])
 @pytest.mark.parametrize("resid", [False, True])
 def test_ln_fwd(T, H, resid):
     g = torch.Generator(device="cuda").manual_seed(T + H)
@@ -41,7 +42,7 @@ def test_ln_fwd(T, H, resid):
     torch.testing.assert_close(mean, xin.float().mean(-1), rtol=1e-5, atol=1e-5)
 
 
-@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048)])
+@pytest.mark.parametrize("T,H", [(64, 128), (1000, 256), (8192, 2048), (300, 4096), (257, 8192)])
 @pytest.mark.parametrize("dres", [False, True])
 def test_ln_bwd(T, H, dres):
     g = torch.Generator(device="cuda").manual_seed(T * H)

@@ -135,6 +135,20 @@ def test_activation_checkpointing_matches(mode):
         assert {"cg", "grad_offload", "compute"} <= stages
 
 
+@pytest.mark.parametrize("hd,heads", [(4096, 32), (8192, 64)])
+def test_10b_70b_layer_shapes(hd, heads):
+    """One block at the 10B / 70B widths (BASELINE configs 3 and 5): the libzinf path
+    agrees with the torch-op path."""
+    c = eg.GPTConfig(nl=1, hd=hd, heads=heads, seq=64, vocab=512, batch=1)
+    a = eg.GPTZeroEngine(c, LocalComm(1), lr=1e-4, fused=True)
+    la = a.step([eg.synthetic_tokens(c, 7, 0)]).item()
+    del a
+    torch.cuda.empty_cache()
+    b = eg.GPTZeroEngine(c, LocalComm(1), lr=1e-4, fused=False)
+    lb = b.step([eg.synthetic_tokens(c, 7, 0)]).item()
+    assert np.isfinite(la) and abs(la - lb) <= 2e-3 * abs(lb)
+
+
 def test_fused_kernels_match_torch_path():
     """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path."""
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True)
