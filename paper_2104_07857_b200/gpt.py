@@ -157,7 +157,8 @@ class GPTZeroEngine:
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool = False,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
-                 overlap_opt: bool = True, act_ckpt: str | None = None):
+                 overlap_opt: bool = True, act_ckpt: str | None = None,
+                 nvme_root: str | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -169,9 +170,12 @@ class GPTZeroEngine:
         self.half = half_dtype
         self.cdt = compute_dtype or half_dtype
         self.placement = placement or Placement()
-        for t in (self.placement.params, self.placement.optim):
-            if t not in (TierKind.DEVICE, TierKind.HOST):
-                raise NotImplementedError("GPT engine tiers: DEVICE or HOST (NVMe: harness / store)")
+        if self.placement.params not in (TierKind.DEVICE, TierKind.HOST):
+            raise NotImplementedError("bf16 params: DEVICE or HOST tier")
+        self.nvme = self.placement.optim is TierKind.NVME
+        if self.nvme and (self.placement.params is not TierKind.DEVICE or not self.comm.is_local):
+            raise NotImplementedError("NVMe optimizer states: params in HBM, simulated ranks")
+        self.nvme_root = nvme_root
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
         self.overlap_opt = overlap_opt
@@ -258,6 +262,15 @@ class GPTZeroEngine:
             self.p16 = mk(self.half, hp)
         else:  # peers gather from it over NVLink: an IPC-shareable allocation
             self.p16 = self.comm.alloc((nloc, A), self.half)
+        if self.nvme:  # optimizer states live in .shard files (nvme_opt.NvmeOptimizerStreamer)
+            import tempfile
+            from .nvme_opt import NvmeOptimizerStreamer
+            from .store import TierStore
+            root = self.nvme_root or tempfile.mkdtemp(prefix="zinf-nvme-")
+            self.store = TierStore(0, 0, nvme_root=root, workers=8)
+            self.streamer = NvmeOptimizerStreamer(self, self.store)
+            self.p32 = self.m = self.v = None
+            return
         self.p32 = mk(torch.float32, ho)
         self.m = mk(torch.float32, ho)
         self.v = mk(torch.float32, ho)
@@ -271,9 +284,9 @@ class GPTZeroEngine:
                 lo, hi = r * b.shard, min((r + 1) * b.shard, b.numel)
                 if hi <= lo:
                     continue
-                # stage on device when the tiers are host, then copy down
-                p32 = torch.empty(b.shard, dtype=torch.float32, device=self.dev) if ho else \
-                    self.p32[li, b.arena_off:b.arena_off + b.shard]
+                # stage on device when the tiers are host / NVMe, then copy down
+                p32 = torch.zeros(b.shard, dtype=torch.float32, device=self.dev) \
+                    if (ho or self.nvme) else self.p32[li, b.arena_off:b.arena_off + b.shard]
                 p16 = torch.empty(b.shard, dtype=self.half, device=self.dev) if hp else \
                     self.p16[li, b.arena_off:b.arena_off + b.shard]
                 for name, off, n, stream, init in b.segments():
@@ -289,6 +302,9 @@ class GPTZeroEngine:
                         kernels.fill(d32, d16, float(init[1]))
                 if ho:
                     self.p32[li, b.arena_off:b.arena_off + b.shard].copy_(p32)
+                if self.nvme:
+                    torch.cuda.synchronize()
+                    self.streamer.put_initial(b.key, r, p32)
                 if hp:
                     self.p16[li, b.arena_off:b.arena_off + b.shard].copy_(p16)
         torch.cuda.synchronize()
@@ -659,6 +675,14 @@ class GPTZeroEngine:
         if self.offload:
             self._reduce_update_offload(b, slot, consts, contribs, scale)
             return
+        if self.nvme:  # the streamer thread runs nc -> cg -> RS+Adam -> D2H -> nc
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            self._nvme_wait[key] = [
+                self.streamer.submit(b, li, r, contribs, scale, ready,
+                                     self._shard_view(self.p16, li, b))
+                for li, r in enumerate(self.ranks)]
+            return
         host_params = self.placement.params is TierKind.HOST
         with torch.cuda.stream(os_):
             for li, r in enumerate(self.ranks):
@@ -796,6 +820,9 @@ class GPTZeroEngine:
 
     def _wait_gslot(self, slot) -> None:
         """Before overwriting a gradient slot: the optimizer stream must be done reading it."""
+        for done in self._nvme_wait.pop(slot, ()):   # NVMe streamer jobs still using it
+            done.wait()
+            torch.cuda.current_stream().wait_event(done.ev)
         ev = self.gfree.pop(slot, None)
         if ev is not None:
             torch.cuda.current_stream().wait_event(ev)
@@ -834,6 +861,7 @@ class GPTZeroEngine:
         self.events.clear()
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
+        self._nvme_wait = {}
         self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
@@ -923,8 +951,10 @@ class GPTZeroEngine:
                 self.launches += 2
             self._finish_grad(li, E, 0, flat)
         self._reduce_update(E, 0, consts)
+        if self.nvme:
+            self.streamer.drain()         # every bucket's states are back on NVMe
         cur.wait_stream(self.opt_stream)  # the step ends when the last bucket is updated
-        if self.offload or self.act_ckpt == "host":  # ... and every host transfer landed
+        if self.offload or self.nvme or self.act_ckpt == "host":  # ... and host transfers landed
             cur.wait_stream(self.d2h_stream)
             cur.wait_stream(self.h2d_stream)
         if gs is not cur:
@@ -945,6 +975,8 @@ class GPTZeroEngine:
         steps (real training steps) and captures; every call then replays.
         """
         cur = torch.cuda.current_stream()
+        if self.nvme:   # host-thread NVMe streaming cannot live inside a graph
+            return self.step(batches)
         if self._graph is None:
             if self.trace:
                 raise ValueError("tracing is not supported under graph capture")
@@ -988,6 +1020,13 @@ class GPTZeroEngine:
 
     def shard(self, key: str, li: int = 0) -> dict:
         b = self.by_key[key]
+        if self.nvme:   # fp32 states read back from their .shard files
+            from .store import TierKind as TK
+            r = self.ranks[li]
+            out = {n: self.store.read(self.streamer.key(key, n, r), TK.NVME).wait()
+                   for n in ("p32", "m", "v")}
+            out["p16"] = self._shard_view(self.p16, li, b)
+            return out
         return {n: self._shard_view(a, li, b) for n, a in
                 (("p16", self.p16), ("p32", self.p32), ("m", self.m), ("v", self.v))}
 
