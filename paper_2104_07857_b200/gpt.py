@@ -1030,6 +1030,13 @@ class GPTZeroEngine:
         return {n: self._shard_view(a, li, b) for n, a in
                 (("p16", self.p16), ("p32", self.p32), ("m", self.m), ("v", self.v))}
 
+    def close(self) -> None:
+        """Stop the NVMe streamer thread (it references the engine) and its store."""
+        if self.nvme and self.streamer is not None:
+            self.streamer.close()
+            self.store.close()
+            self.streamer = None
+
 
 def synthetic_tokens(cfg: GPTConfig, seed: int, rank: int, step: int = 0, device="cuda"):
     """Uniform token ids on [0, V) per (rank, step) — same generator as the oracle."""

@@ -85,6 +85,10 @@ class NvmeOptimizerStreamer:
         torch.cuda.set_device(self.e.dev)
         while True:
             job = self.q.get()
+            if job is None:                        # close(): drop the engine reference
+                self.q.task_done()
+                self.e = None
+                return
             try:
                 if self.err is None:
                     self._bucket(*job)
@@ -155,5 +159,12 @@ class NvmeOptimizerStreamer:
         done.set()
 
     def close(self):
+        """Stop the thread (it holds the engine) and free the pinned slots."""
+        if self.t.is_alive():
+            self.q.put(None)
+            self.t.join()
+        self.e = None
+        self.S = None
         for b in self._bufs:
             b.free()
+        self._bufs = []

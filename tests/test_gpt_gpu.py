@@ -222,6 +222,7 @@ def test_nvme_optimizer_states_match_hbm(tmp_path):
     assert "h0.p32%2Frank1.shard" in files
     assert (tmp_path / "h0.m%2Frank0.shard").read_bytes()[:4] == SHARD_MAGIC
     assert b.streamer.bytes > 0
+    b.close()
 
 
 def test_traced_timeline():
