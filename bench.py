@@ -419,6 +419,12 @@ def offload_leg(cfg, args) -> dict:
     eng.trace = True          # one extra traced step for the overlap Timeline
     eng.step([bs[0]])
     tl = eng.timeline()
+    cal = {}
+    for name, duplex in (("half_duplex", False), ("duplex", True)):
+        sim = eng.simulated_step(duplex)
+        cal["measured_step_s"] = round(sim["measured_s"], 4)
+        cal[f"predicted_{name}_s"] = round(sim["predicted_s"], 4)
+        cal[f"rel_error_{name}"] = round(sim["rel_error"], 4)
     eng.trace = False
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "offload_timeline.csv"), "w") as f:
@@ -433,7 +439,8 @@ def offload_leg(cfg, args) -> dict:
            "timeline": {"pcie_busy_s": round(tl.lane_busy_s("pcie"), 4),
                         "compute_busy_s": round(tl.lane_busy_s("compute"), 4),
                         "traced_step_s": round(tl.total_s, 4),
-                        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)}}
+                        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)},
+           "simulator_calibration": cal}
     del eng
     torch.cuda.empty_cache()
     # activation checkpoints offloaded to pinned host (PAPER §5.1.2): forward keeps each
@@ -451,6 +458,7 @@ def offload_leg(cfg, args) -> dict:
     eng.trace = True
     eng.step([bs[0]])
     tl = eng.timeline()
+    sim = eng.simulated_step()
     T, P = cfg.tokens, eg.param_count(cfg)
     out["act_ckpt_host"] = {
         "ms_per_step": round(ms, 2),
@@ -458,7 +466,10 @@ def offload_leg(cfg, args) -> dict:
         "hw_tflops_8TP": round((8.0 * T * P + 8 * 2 * cfg.batch * cfg.seq ** 2 * cfg.hd * cfg.nl)
                                / (ms / 1e3) / 1e12, 1),
         "ckpt_bytes_per_step": 2 * cfg.nl * T * cfg.hd * 2,
-        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4)}
+        "pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4),
+        "simulator_calibration": {"measured_step_s": round(sim["measured_s"], 4),
+                                  "predicted_s": round(sim["predicted_s"], 4),
+                                  "rel_error": round(sim["rel_error"], 4)}}
     del eng
     torch.cuda.empty_cache()
     if not args.no_nvme:

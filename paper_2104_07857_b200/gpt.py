@@ -384,15 +384,63 @@ class GPTZeroEngine:
 
     def _tspan(self, op: int, stage: str, e0, e1) -> None:
         if e0 is not None and e1 is not None:
-            self._spans.append((op, stage, e0, e1))
+            self._spans.append((op, stage, e0, e1, self._phase))
 
-    def timeline(self) -> Timeline:
-        """Timeline of the last traced step, seconds from step start."""
+    def timeline(self, phase: str | None = None) -> Timeline:
+        """Timeline of the last traced step, seconds from step start.
+
+        ``phase`` = "forward" | "backward" keeps only that pass's spans (the
+        head's fused forward + backward counts as the first backward op).
+        """
         torch.cuda.synchronize()
-        tl = Timeline()
-        for op, stage, e0, e1 in self._spans:
-            tl.add(op, stage, self._t0.elapsed_time(e0) / 1e3, self._t0.elapsed_time(e1) / 1e3)
+        tl = Timeline(t0=0.0)
+        for op, stage, e0, e1, ph in self._spans:
+            if phase is None or ph == phase:
+                tl.add(op, stage, self._t0.elapsed_time(e0) / 1e3, self._t0.elapsed_time(e1) / 1e3)
         return tl
+
+    def simulated_step(self, duplex: bool = False, lanes: dict | None = None) -> dict:
+        """Replay the last traced step's measured per-op stage costs through the lane simulator.
+
+        This is the calibration of SURVEY §8 f4. ``costs_from_timeline`` takes
+        each op's measured stage durations. ``simulate`` / ``simulate_backward``
+        schedule them with the engine's plan: one-op-ahead fetches, so depths
+        (1, 1, 1); the head is the first backward op and the embedding the
+        last. Comparing with the measured step tests the simulator's lane model.
+
+        In the offload placement a bucket's optimizer-state H2D and D2H chunks
+        run after its compute. With ``duplex=False`` (the SPEC's single pcie
+        lane) both count as that op's ``grad_offload``. With ``duplex=True`` the
+        H2D half becomes the op's post-compute ``reduce_scatter`` stage on lane
+        ``pcie_h2d`` and the D2H half stays ``grad_offload`` on ``pcie_d2h``.
+        That models the two copy engines of a full-duplex link.
+        """
+        from .schedule import (Op, OperatorSequence, costs_from_timeline, plan_prefetch,
+                               simulate, simulate_backward)
+        E, FB, blocks = self.buckets[0], self.buckets[-1], self.buckets[1:-1]
+        fwd_ops = [E.op] + [b.op for b in blocks]
+        bwd_ops = [FB.op] + [b.op for b in reversed(blocks)] + [E.op]
+
+        def plan(ids):
+            return plan_prefetch(OperatorSequence(tuple(Op(i, (), 1, 1) for i in ids),
+                                                 "backward"), (1, 1, 1))
+        fwd_tl, bwd_tl = self.timeline("forward"), self.timeline("backward")
+        smap = None
+        if self.offload:
+            smap = {"cg": "reduce_scatter" if duplex else "grad_offload"}
+        if duplex:
+            lanes = dict({"reduce_scatter": "pcie_h2d" if self.offload else "d2d",
+                          "grad_offload": "pcie_d2h"}, **(lanes or {}))
+        fc = costs_from_timeline(fwd_tl, fwd_ops)
+        bc = costs_from_timeline(bwd_tl, bwd_ops, smap)
+        sf = simulate(plan(fwd_ops), fc, lanes=lanes)
+        sb = simulate_backward(plan(bwd_ops), bc, lanes=lanes)
+        measured = self.timeline().total_s
+        predicted = sf.total_s + sb.total_s
+        return {"measured_s": measured, "predicted_s": predicted,
+                "rel_error": (predicted - measured) / measured if measured else 0.0,
+                "forward_predicted_s": sf.total_s, "backward_predicted_s": sb.total_s,
+                "serial_s": sf.serial_s + sb.serial_s, "forward": sf, "backward": sb}
 
     def _fetch(self, b: Bucket, slot: int, stream):
         """Issue the gather of bucket b into ring slot `slot` on `stream`."""
@@ -685,6 +733,7 @@ class GPTZeroEngine:
             return
         host_params = self.placement.params is TierKind.HOST
         with torch.cuda.stream(os_):
+            t0 = self._tmark(os_)
             for li, r in enumerate(self.ranks):
                 p16 = self._shard_view(self.p16, li, b)
                 ph = torch.empty(b.shard, dtype=self.half, device=self.dev) if host_params else p16
@@ -696,6 +745,7 @@ class GPTZeroEngine:
                 if host_params:  # updated bf16 shard back to its pinned home (D2H)
                     p16.copy_(ph, non_blocking=True)
                 self.launches += 1
+            self._tspan(b.op, "reduce_scatter", t0, self._tmark(os_))
             if self.comm.is_local and os_ is not cur:
                 ev = torch.cuda.Event()
                 ev.record(os_)
@@ -862,6 +912,7 @@ class GPTZeroEngine:
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
         self._nvme_wait = {}
+        self._phase = "forward"
         self._t0 = self._tmark(cur)
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
@@ -871,7 +922,9 @@ class GPTZeroEngine:
         if blocks:
             self._fetch(blocks[0], 0, gs)
         PE = self._params(E, self._full(E, 0))
+        c0 = self._tmark(cur)
         xs = [self._embed_fwd(PE, batches[li][0]) for li in range(nloc)]
+        self._tspan(E.op, "compute", c0, self._tmark(cur))
         caches = [[None] * len(blocks) for _ in range(nloc)]
         for i, b in enumerate(blocks):
             slot = i % 2
@@ -881,7 +934,9 @@ class GPTZeroEngine:
                 self._fetch(blocks[i + 1], (i + 1) % 2, gs)
             else:
                 gs.wait_stream(cur)
+                self._phase = "backward"     # the head is the first backward op
                 self._fetch(FB, (i + 1) % 2, gs)
+                self._phase = "forward"
             P = self._params(b, full)
             c0 = self._tmark(cur)
             for li in range(nloc):
@@ -891,6 +946,7 @@ class GPTZeroEngine:
                     caches[li][i] = self._ckpt_save(li, i, x_in)
             self._tspan(b.op, "compute", c0, self._tmark(cur))
         fslot = len(blocks) % 2
+        self._phase = "backward"
         if not blocks:
             self._fetch(FB, 0, gs)
         PF = self._params(FB, self._full(FB, fslot))
@@ -936,6 +992,7 @@ class GPTZeroEngine:
             self._reduce_update(b, slot, consts)
         # ---- embedding backward: tied wte = head part + scatter of dx
         self._wait_gslot("embed")
+        c0 = self._tmark(cur)
         for li in range(nloc):
             G, flat = self._grad_views(li, E, 0)
             tok = batches[li][0].reshape(-1)
@@ -950,6 +1007,7 @@ class GPTZeroEngine:
                 kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
                 self.launches += 2
             self._finish_grad(li, E, 0, flat)
+        self._tspan(E.op, "compute", c0, self._tmark(cur))
         self._reduce_update(E, 0, consts)
         if self.nvme:
             self.streamer.drain()         # every bucket's states are back on NVMe

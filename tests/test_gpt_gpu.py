@@ -239,6 +239,17 @@ def test_traced_timeline():
         assert e >= s >= 0
     assert 0.0 <= tl.hidden_fraction() <= 1.0
     assert tl.to_csv().count("\n") == len(tl.events) + 1
+    # calibration: measured per-op costs replayed through the simulator
+    fwd, bwd = eng.timeline("forward"), eng.timeline("backward")
+    assert len(fwd.events) + len(bwd.events) == len(tl.events)
+    assert {e[0] for e in fwd.events if e[1] == "compute"} == {b.op for b in eng.buckets[:-1]}
+    from paper_2104_07857_b200.schedule import verify_timeline
+    for duplex in (False, True):
+        sim = eng.simulated_step(duplex)
+        verify_timeline(sim["forward"])
+        verify_timeline(sim["backward"])
+        assert 0 < sim["predicted_s"] <= sim["serial_s"] + 1e-12
+        assert sim["measured_s"] == tl.total_s
 
 
 def test_copy_engine_gather_same_result():
