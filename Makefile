@@ -1,7 +1,8 @@
 # libzinf: hand-written sm_100a kernels behind the C ABI in include/zinf.h.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude --expt-relaxed-constexpr
+NVEXTRA ?=
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude --expt-relaxed-constexpr $(NVEXTRA)
 CSRC := paper_2104_07857_b200/csrc
 SRCS := $(wildcard $(CSRC)/*.cu)
 OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(SRCS))
@@ -9,7 +10,7 @@ LIB := paper_2104_07857_b200/libzinf.so
 
 all: $(LIB)
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh include/zinf.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/bulk.cuh include/zinf.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

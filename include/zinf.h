@@ -133,7 +133,11 @@ int zi_cast_half_to_f32(const void* src, float* dst, size_t n, int half_kind,
  *   zi_ln_fwd     y = (x [+ resid] - mean) * rstd * w + b; with resid, also
  *                 xsum = bf16(x + resid) (residual add fused); mean/rstd per row.
  *   zi_ln_bwd     dx = rstd * (dy*w - mean(dy*w) - xh * mean(dy*w*xh)) [+ dres];
- *                 dgamma = sum_rows dy * xh, dbeta = sum_rows dy.
+ *                 dgamma = sum_rows dy * xh, dbeta = sum_rows dy; with dres_sum,
+ *                 also dres_sum = sum_rows dres (the bias gradient of the linear
+ *                 whose output gradient is dres), all from one pass.
+ *   zi_gelu_fwd   y = gelu_tanh(u) over n bf16 (n % 8 == 0; SFU tanh, the error is
+ *                 below bf16 output precision).
  *   zi_bias_grad  db = sum_rows dy; with u given, first du = gelu_tanh'(u) * dy
  *                 (stored to du) and db = sum_rows du.
  *   zi_softmax_ce in place over T rows of V bf16 logits: loss_rows = lse - l[t],
@@ -141,8 +145,9 @@ int zi_cast_half_to_f32(const void* src, float* dst, size_t n, int half_kind,
 int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const void* b, void* y,
               float* mean, float* rstd, int T, int H, float eps, void* stream);
 int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
-              const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
-              size_t work_elems, int T, int H, void* stream);
+              const void* dres, void* dx, void* dgamma, void* dbeta, void* dres_sum, int grads_f32,
+              float* work, size_t work_elems, int T, int H, void* stream);
+int zi_gelu_fwd(const void* u, void* y, size_t n, void* stream);
 int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, float* work,
                  size_t work_elems, int T, int N, void* stream);
 int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T,
@@ -195,6 +200,22 @@ int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y,
 int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
             const void* bias, void* D, int d_f32, int accumulate, int ldd,
             int M, int N, int K, void* stream);
+
+/* The same GEMM with a fused bf16 epilogue (the GPT block's linears; no
+ * reference counterpart, a build extension of the SPEC's tile GEMM):
+ *   ZI_EPI_PLAIN  D = acc (+ bias)
+ *   ZI_EPI_GELU   D = u = bf16(acc + bias), D2 = bf16(gelu_tanh(u))   fc1 forward
+ *   ZI_EPI_RESID  D = bf16(bf16(acc + bias) + X)                        fc2 forward + residual
+ *   ZI_EPI_DGELU  D = bf16(bf16(acc) * gelu_tanh'(X)), X = u            fc2 dX -> fc1 du
+ * X (ldx) and D2 (ldd2) are M x N bf16; N % 8 == 0 and all leading dimensions
+ * multiples of 8. Operand majorness as zi_gemm. */
+enum { ZI_EPI_PLAIN = 0, ZI_EPI_GELU = 1, ZI_EPI_RESID = 2, ZI_EPI_DGELU = 3 };
+int zi_gemm_ex(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
+               const void* bias, void* D, int ldd, const void* X, int ldx, void* D2, int ldd2,
+               int epi, int M, int N, int K, void* stream);
+/* Diagnostics: a device buffer of >= 148*16*8 u64 receiving clock64() stamps of the
+ * wide-tile GEMM's pipeline (NULL turns it off). Not for production use. */
+int zi_gemm_set_profile(void* buf);
 
 #ifdef __cplusplus
 }

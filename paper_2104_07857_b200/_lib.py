@@ -57,7 +57,8 @@ SIGNATURES = {
     "zi_ln_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                   c_int, c_int, c_float, c_void_p],
     "zi_ln_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                  c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p],
+                  c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_int, c_int, c_void_p],
+    "zi_gelu_fwd": [c_void_p, c_void_p, c_size_t, c_void_p],
     "zi_bias_grad": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_size_t, c_int,
                      c_int, c_void_p],
     "zi_softmax_ce": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_float, c_void_p],
@@ -82,6 +83,9 @@ SIGNATURES = {
                       c_int, c_void_p],
     "zi_gemm": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                 c_int, c_int, c_int, c_int, c_void_p],
+    "zi_gemm_set_profile": [c_void_p],
+    "zi_gemm_ex": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int,
+                   c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p],
 }
 _RESTYPE = {"zi_last_error": ctypes.c_char_p}
 

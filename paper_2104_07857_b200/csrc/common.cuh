@@ -80,6 +80,26 @@ __device__ __forceinline__ void adam1(float& p, float& m, float& v, float g,
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(c.lr, mh), den));
 }
 
+// tanh on the SFU (tanh.approx.f32, max relative error ~2^-11). GELU results
+// are rounded to bf16 (2^-8), so the approximation is below the output
+// precision and keeps the GELU kernels / epilogues HBM-bound, not issue-bound.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+constexpr float GELU_C = 0.7978845608028654f, GELU_A = 0.044715f;
+
+__device__ __forceinline__ float gelu_tanh(float z) {
+  return 0.5f * z * (1.f + tanh_fast(GELU_C * (z + GELU_A * z * z * z)));
+}
+
+__device__ __forceinline__ float gelu_tanh_grad(float z) {
+  const float th = tanh_fast(GELU_C * (z + GELU_A * z * z * z));
+  return 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * GELU_C * (1.f + 3.f * GELU_A * z * z);
+}
+
 }  // namespace zi
 
 #define ZI_CHECK_ARG(cond, ...)           \

@@ -1,16 +1,17 @@
 // Fused HBM-bound kernels of the GPT block around the GEMMs (bf16 activations,
 // fp32 math). Each reads its inputs once and writes its outputs once; column
 // reductions (LayerNorm gamma/beta grads, bias grads) are deterministic:
-// per-CTA fp32 partials reduced in a fixed order by zi_colsum_finish.
+// per-CTA fp32 partials reduced in a fixed order.
 //
-//   zi_ln_fwd        y = LN(x) * w + b            (+ x2 = x + r fused residual)
-//   zi_ln_bwd        dx = LN'(dy) (+ dres), partial dgamma / dbeta
-//   zi_bias_grad     partial column sums of dy (bias gradient)
-//   zi_gelu_bwd      du = gelu'(u) * da, partial column sums of du
-//   zi_colsum_finish partials [P x N] -> out[N] (bf16 RNE or fp32), fixed order
-//   zi_softmax_ce    per-row logsumexp, loss, dlogits = (softmax - onehot) * scale
+//   zi_ln_fwd      y = LN(x) * w + b            (+ x2 = x + r fused residual)
+//   zi_ln_bwd      dx = LN'(dy) (+ dres); dgamma, dbeta and optionally the
+//                  column sums of dres (a bias gradient) from the same pass
+//   zi_gelu_fwd    y = gelu_tanh(u)
+//   zi_bias_grad   column sums of dy, or du = gelu'(u) * dy and sums of du
+//   zi_softmax_ce  per-row logsumexp, loss, dlogits = (softmax - onehot) * scale
 #include <type_traits>
 
+#include "bulk.cuh"
 #include "common.cuh"
 
 namespace zi {
@@ -149,147 +150,245 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
   }
 }
 
-// dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w,
-// plus dres (residual gradient) if given.
+// LayerNorm backward in one pass over dy, x (and dres):
+//   dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w, + dres;
+//   per-CTA column partials of dgamma = sum dy * xh, dbeta = sum dy and, when
+//   asked, of sum dres (the bias gradient of the linear that produced dres).
+// Rows stream through a LNB_STAGES-deep shared-memory ring filled by bulk
+// async copies (one per input per stage, RPC contiguous rows), so the loads of
+// the next stages are in flight while this one is reduced. The CTA folds its
+// row slots in order and writes one partial row per set to
+// part[set][blockIdx.x][H]; ln_fold_kernel sums the partials in CTA order.
+constexpr int LNB_NT = 512, LNB_STAGES = 4;
 template <int TPR>
-__global__ void __launch_bounds__(RowCta<TPR>::NT)
-ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
-                 const uint16_t* __restrict__ w, const float* __restrict__ mean,
-                 const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
-                 uint16_t* __restrict__ dx, int T) {
-  constexpr int H = 8 * TPR, RPC = RowCta<TPR>::RPC;
+struct LnbCta {
+  static constexpr int NT = TPR > LNB_NT ? TPR : LNB_NT;
+  static constexpr int RPC = NT / TPR;
+};
+
+template <int TPR, bool DRES>
+constexpr size_t lnb_smem() {
+  return (size_t)LNB_STAGES * (DRES ? 3 : 2) * LnbCta<TPR>::RPC * 8 * TPR * 2 + 64;
+}
+
+template <int TPR, bool DRES, bool RSUM>
+__global__ void __launch_bounds__(LnbCta<TPR>::NT, LnbCta<TPR>::NT > LNB_NT ? 1 : 2)
+ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+              const uint16_t* __restrict__ w, const float* __restrict__ mean,
+              const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
+              uint16_t* __restrict__ dx, float* __restrict__ part, int T) {
+  constexpr int H = 8 * TPR, RPC = LnbCta<TPR>::RPC, NT = LnbCta<TPR>::NT;
+  constexpr int NIN = DRES ? 3 : 2, NS = RSUM ? 3 : 2;
+  constexpr int ROWS_E = RPC * H;                    // elements per input per stage
+  extern __shared__ __align__(128) uint16_t ring[];  // [stage][input][RPC * H]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)LNB_STAGES * NIN * ROWS_E);
   __shared__ float sm[32];
-  const int t = threadIdx.x % TPR;
+  const int t = threadIdx.x % TPR, slot = threadIdx.x / TPR;
+  const int G = gridDim.x, ngroups = (T + RPC - 1) / RPC;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LNB_STAGES; ++s) bulk::mbar_init(&full[s], 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {                          // thread 0: fill stage i % STAGES
+    const int g = blockIdx.x + i * G;
+    if (g >= ngroups) return;
+    const int s = i % LNB_STAGES;
+    const uint32_t bytes = (uint32_t)min(RPC, T - g * RPC) * H * 2;
+    const size_t off = (size_t)g * RPC * H;
+    uint16_t* st = ring + (size_t)s * NIN * ROWS_E;
+    bulk::mbar_expect_tx(&full[s], NIN * bytes);
+    bulk::g2s(st, dy + off, bytes, &full[s]);
+    bulk::g2s(st + ROWS_E, x + off, bytes, &full[s]);
+    if (DRES) bulk::g2s(st + 2 * ROWS_E, dres + off, bytes, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < LNB_STAGES; ++i) issue(i);
   float wf[8];
   ld_row<8>(w + t * 8, wf);
-  for (int row0 = blockIdx.x * RPC; row0 < T; row0 += gridDim.x * RPC) {
-    const int row = row0 + threadIdx.x / TPR;
+  float acc[NS][8];
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[k][i] = 0.f;
+  for (int i = 0;; ++i) {
+    const int g = blockIdx.x + i * G;
+    if (g >= ngroups) break;
+    const int s = i % LNB_STAGES;
+    bulk::mbar_wait(&full[s], (i / LNB_STAGES) & 1);
+    const uint16_t* st = ring + (size_t)s * NIN * ROWS_E + slot * H + t * 8;
+    const int row = g * RPC + slot;
     const bool live = row < T;
     const int rr = live ? row : 0;
-    const size_t off = (size_t)rr * H + t * 8;
-    float g[8], xv[8];
-    ld_row<8>(dy + off, g);
-    ld_row<8>(x + off, xv);
+    float gv[8], xv[8], rv[8];
+    ld_row<8>(st, gv);
+    ld_row<8>(st + ROWS_E, xv);
+    if (DRES) ld_row<8>(st + 2 * ROWS_E, rv);
     const float mu = mean[rr], rs = rstd[rr];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      g[i] *= wf[i];                 // dxh
-      xv[i] = (xv[i] - mu) * rs;     // xh
-      s1 += g[i];
-      s2 += g[i] * xv[i];
+    for (int k = 0; k < 8; ++k) {
+      xv[k] = (xv[k] - mu) * rs;     // xh
+      if (live) {
+        acc[0][k] += gv[k] * xv[k];
+        acc[1][k] += gv[k];
+        if (RSUM) acc[NS - 1][k] += rv[k];
+      }
+      gv[k] *= wf[k];                // dxh
+      s1 += gv[k];
+      s2 += gv[k] * xv[k];
     }
     const float m1 = row_reduce<TPR>(s1, sm) * (1.0f / H);
     const float m2 = row_reduce<TPR>(s2, sm) * (1.0f / H);
     float o[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = rs * (g[i] - m1 - xv[i] * m2);
-    if (dres != nullptr) {
-      float rv[8];
-      ld_row<8>(dres + off, rv);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] += rv[i];
+    for (int k = 0; k < 8; ++k) {
+      o[k] = rs * (gv[k] - m1 - xv[k] * m2);
+      if (DRES) o[k] += rv[k];
     }
-    if (live) st_row<8>(dx + off, o);
+    if (live) st_row<8>(dx + (size_t)row * H + t * 8, o);
+    __syncthreads();                 // stage s fully read: refill it
+    if (threadIdx.x == 0) issue(i + LNB_STAGES);
+  }
+  // this CTA's partial rows: fold the RPC row slots in order (the ring is idle now:
+  // every issued stage was consumed above)
+  if constexpr (RPC == 1) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) part[((size_t)k * gridDim.x + blockIdx.x) * H + t * 8 + q] = acc[k][q];
+  } else {
+    float* red = reinterpret_cast<float*>(ring);     // RPC * H floats <= one stage
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) red[slot * H + t * 8 + q] = acc[k][q];
+      __syncthreads();
+      for (int c = threadIdx.x; c < H; c += NT) {
+        float sum = 0.f;
+        for (int q = 0; q < RPC; ++q) sum += red[q * H + c];
+        part[((size_t)k * gridDim.x + blockIdx.x) * H + c] = sum;
+      }
+    }
   }
 }
 
-// Column reductions (bias grads, GELU-bwd + bias grad, LayerNorm dgamma/dbeta).
-// CTA = 64 columns (8 threads x 8) x 32 row groups; blockIdx.y = chunk of rows.
-// Each thread folds rows rg, rg+32, ... of its chunk; the CTA folds its 32 row
-// groups in order into one partial row; the last CTA of a column block (atomic
-// counter, self-resetting so CUDA graphs replay it) folds the chunk partials in
-// chunk order and writes the result. Deterministic, one launch, no finish kernel.
-//   MODE 0: out0 = sum a                          (bias grad)
-//   MODE 1: du = gelu_tanh'(u) * a -> d; out0 = sum du   (GELU bwd + fc1 bias grad)
-//   MODE 2: out0 = sum a * (u - mean) * rstd, out1 = sum a   (LN dgamma, dbeta)
-constexpr int CR_COLS = 64, CR_RG = 32;
+// part[set][P][H] -> out_set[H] (bf16 RNE or fp32); per column, P is split into
+// FOLD_SUB ordered runs summed by separate threads, then combined in run order:
+// deterministic for a fixed P, and ~P / FOLD_SUB dependent loads per thread.
+constexpr int FOLD_SUB = 32;
+__global__ void __launch_bounds__(32 * FOLD_SUB)
+ln_fold_kernel(const float* __restrict__ part, int P, int H, void* __restrict__ o0,
+               void* __restrict__ o1, void* __restrict__ o2, int out_f32) {
+  __shared__ float sm[FOLD_SUB][33];
+  const int set = blockIdx.y, lane = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
+  float s = 0.f;
+  if (col < H) {
+    const int per = (P + FOLD_SUB - 1) / FOLD_SUB, p0 = sub * per, p1 = min(P, p0 + per);
+    const float* src = part + (size_t)set * P * H + col;
+#pragma unroll 4
+    for (int p = p0; p < p1; ++p) s += __ldcg(src + (size_t)p * H);
+  }
+  sm[sub][lane] = s;
+  __syncthreads();
+  if (sub == 0 && col < H) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < FOLD_SUB; ++k) t += sm[k][lane];
+    void* dst = set == 0 ? o0 : (set == 1 ? o1 : o2);
+    if (out_f32) static_cast<float*>(dst)[col] = t;
+    else static_cast<uint16_t*>(dst)[col] = tobf(t);
+  }
+}
+
+// y = gelu_tanh(u), 8 bf16 per thread per step (n % 8 == 0), grid-stride.
+__global__ void __launch_bounds__(256)
+gelu_fwd_kernel(const uint16_t* __restrict__ u, uint16_t* __restrict__ y, size_t n8) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float v[8];
+    ld_row<8>(u + 8 * i, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = gelu_tanh(v[j]);
+    st_row<8>(y + 8 * i, v);
+  }
+}
+
+// Column reductions (bias grads, GELU-bwd + bias grad) over rows streamed
+// through a CRW_STAGES-deep bulk-copy ring. CTA (column block, row chunk): C
+// columns (8 per thread, C/8 threads), rows [r0, r1) in stages of R rows; one
+// bulk copy per row and input. Each thread accumulates its 8 columns over the
+// chunk in row order and writes one partial row part[chunk][N]; the fold kernel
+// then sums the chunks in order: deterministic for a fixed grid.
+//   MODE 0: out = sum_rows a                               (bias grad)
+//   MODE 1: du = gelu_tanh'(u) * a -> d; out = sum_rows du (GELU bwd + fc1 bias grad)
+constexpr int CRW_STAGES = 4, CRW_MAX_COLS = 4096;
 
 template <int MODE>
-__global__ void __launch_bounds__(256)
-colred_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
-              uint16_t* __restrict__ d, const float* __restrict__ mean,
-              const float* __restrict__ rstd, float* __restrict__ part, int* __restrict__ counters,
-              void* __restrict__ out0, void* __restrict__ out1, int out_f32, int T, int N,
+__global__ void __launch_bounds__(CRW_MAX_COLS / 8)
+colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
+              uint16_t* __restrict__ d, float* __restrict__ part, int T, int N, int C, int R,
               int rows_per) {
-  constexpr int NO = MODE == 2 ? 2 : 1;
-  __shared__ float red[NO][CR_RG][CR_COLS + 1];
-  __shared__ int last;
-  const int cx = threadIdx.x & 7, rg = threadIdx.x >> 3;
-  const int c8 = blockIdx.x * CR_COLS + cx * 8;
-  const bool colok = c8 < N;
+  constexpr int NIN = MODE == 1 ? 2 : 1;
+  extern __shared__ __align__(128) uint16_t ring[];   // [stage][input][R][C]
+  const int SE = R * C;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)CRW_STAGES * NIN * SE);
+  const int c0 = blockIdx.x * C, W = min(C, N - c0);
   const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
-  float acc[NO][8];
+  const int nst = r1 > r0 ? (r1 - r0 + R - 1) / R : 0;
+  const int t = threadIdx.x;
+  const bool colok = t * 8 < W;
+  if (t == 0) {
+    for (int s = 0; s < CRW_STAGES; ++s) bulk::mbar_init(&full[s], 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {                          // thread 0: rows of stage i
+    if (i >= nst) return;
+    const int s = i % CRW_STAGES, rb = r0 + i * R, rows = min(R, r1 - rb);
+    const uint32_t bytes = (uint32_t)W * 2;
+    bulk::mbar_expect_tx(&full[s], NIN * rows * bytes);
+    uint16_t* st = ring + (size_t)s * NIN * SE;
+    for (int j = 0; j < rows; ++j) {
+      const size_t off = (size_t)(rb + j) * N + c0;
+      bulk::g2s(st + j * C, a + off, bytes, &full[s]);
+      if (MODE == 1) bulk::g2s(st + SE + j * C, u + off, bytes, &full[s]);
+    }
+  };
+  if (t == 0)
+    for (int i = 0; i < CRW_STAGES; ++i) issue(i);
+  float acc[8];
 #pragma unroll
-  for (int o = 0; o < NO; ++o)
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+  for (int i = 0; i < nst; ++i) {
+    const int s = i % CRW_STAGES, rb = r0 + i * R, rows = min(R, r1 - rb);
+    bulk::mbar_wait(&full[s], (i / CRW_STAGES) & 1);
+    if (colok) {
+      const uint16_t* st = ring + (size_t)s * NIN * SE + t * 8;
+      for (int j = 0; j < rows; ++j) {
+        float v[8];
+        ld_row<8>(st + j * C, v);
+        if (MODE == 1) {
+          float uv[8];
+          ld_row<8>(st + SE + j * C, uv);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[o][j] = 0.f;
+          for (int k = 0; k < 8; ++k)
+            v[k] = __bfloat162float(__float2bfloat16_rn(v[k] * gelu_tanh_grad(uv[k])));
+          st_row<8>(d + (size_t)(rb + j) * N + c0 + t * 8, v);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += v[k];
+      }
+    }
+    __syncthreads();                                 // stage s read by everyone: refill
+    if (t == 0) issue(i + CRW_STAGES);
+  }
   if (colok) {
-#pragma unroll 4
-    for (int row = r0 + rg; row < r1; row += CR_RG) {
-      const size_t off = (size_t)row * N + c8;
-      float v[8];
-      ld_row<8>(a + off, v);
-      if (MODE == 1) {
-        float uv[8];
-        ld_row<8>(u + off, uv);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float z = uv[j];
-          const float c = 0.7978845608028654f;
-          const float th = tanhf(c * (z + 0.044715f * z * z * z));
-          const float dg = 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * c * (1.f + 3.f * 0.044715f * z * z);
-          v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * dg));
-        }
-        st_row<8>(d + off, v);
-      }
-      if (MODE == 2) {
-        float xv[8];
-        ld_row<8>(u + off, xv);
-        const float mu = mean[row], rs = rstd[row];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          acc[0][j] += v[j] * (xv[j] - mu) * rs;
-          acc[NO - 1][j] += v[j];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[0][j] += v[j];
-      }
-    }
+    for (int k = 0; k < 8; ++k) part[(size_t)blockIdx.y * N + c0 + t * 8 + k] = acc[k];
   }
-#pragma unroll
-  for (int o = 0; o < NO; ++o)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) red[o][rg][cx * 8 + j] = acc[o][j];
-  __syncthreads();
-  // fold the 32 row groups (fixed order) -> this chunk's partial row
-  if (threadIdx.x < CR_COLS * NO) {
-    const int o = threadIdx.x / CR_COLS, col = threadIdx.x % CR_COLS;
-    const int gc = blockIdx.x * CR_COLS + col;
-    float t = 0.f;
-#pragma unroll 8
-    for (int k = 0; k < CR_RG; ++k) t += red[o][k][col];
-    if (gc < N) part[((size_t)o * gridDim.y + blockIdx.y) * N + gc] = t;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1) == (int)gridDim.y - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x < CR_COLS * NO) {
-    const int o = threadIdx.x / CR_COLS, col = threadIdx.x % CR_COLS;
-    const int gc = blockIdx.x * CR_COLS + col;
-    if (gc < N) {
-      float t = 0.f;
-      for (int p = 0; p < (int)gridDim.y; ++p) t += __ldcg(&part[((size_t)o * gridDim.y + p) * N + gc]);
-      void* dst = o == 0 ? out0 : out1;
-      if (out_f32) static_cast<float*>(dst)[gc] = t;
-      else static_cast<uint16_t*>(dst)[gc] = tobf(t);
-    }
-  }
-  if (threadIdx.x == 0) counters[blockIdx.x] = 0;   // ready for the next launch / replay
 }
 
 // One CTA per row of V logits (bf16, in place): lse, loss_row = lse - l[t],
@@ -412,6 +511,33 @@ static int ln_grid(int T, int H) {
   return need < cap ? need : cap;
 }
 
+template <int TPR, bool DRES, bool RSUM>
+static int launch_ln_bwd3(int grid, cudaStream_t s, const uint16_t* dy, const uint16_t* x,
+                          const uint16_t* w, const float* mean, const float* rstd,
+                          const uint16_t* dres, uint16_t* dx, float* part, int T) {
+  constexpr size_t smem = lnb_smem<TPR, DRES>();
+  static bool attr = false;
+  if (!attr) {
+    ZI_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<TPR, DRES, RSUM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "cudaFuncSetAttribute(ln_bwd)");
+    attr = true;
+  }
+  ln_bwd_kernel<TPR, DRES, RSUM><<<grid, LnbCta<TPR>::NT, smem, s>>>(dy, x, w, mean, rstd, dres,
+                                                                     dx, part, T);
+  return ZI_OK;
+}
+
+template <int TPR>
+static int launch_ln_bwd(int grid, cudaStream_t s, bool rsum, const uint16_t* dy,
+                         const uint16_t* x, const uint16_t* w, const float* mean,
+                         const float* rstd, const uint16_t* dres, uint16_t* dx, float* part,
+                         int T) {
+  if (rsum) return launch_ln_bwd3<TPR, true, true>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  if (dres) return launch_ln_bwd3<TPR, true, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  return launch_ln_bwd3<TPR, false, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+}
+
 extern "C" {
 
 int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const void* b, void* y,
@@ -427,57 +553,110 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
   return zi::launch_status("zi_ln_fwd");
 }
 
-// work layout: [0, 1024) int counters (zeroed once, self-resetting), then partials
-static int launch_colred(int mode, const void* a, const void* u, void* d, const float* mean,
-                         const float* rstd, void* out0, void* out1, int out_f32, float* work,
-                         size_t work_elems, int T, int N, cudaStream_t s, const char* name) {
+// work layout: [0, 1024) reserved (zero), then the fp32 partial rows
+static int launch_colred(int mode, const void* a, const void* u, void* d, void* out, int out_f32,
+                         float* work, size_t work_elems, int T, int N, cudaStream_t s,
+                         const char* name) {
   ZI_CHECK_ARG(N % 8 == 0, "%s: N must be a multiple of 8", name);
-  const int cblocks = (N + CR_COLS - 1) / CR_COLS;
-  ZI_CHECK_ARG(cblocks <= 1024, "%s: N too large for the counter block", name);
-  int chunks = (sm_count() * 4 + cblocks - 1) / cblocks;
-  const int max_chunks = (T + CR_RG - 1) / CR_RG;
+  ZI_CHECK_ARG(zi::aligned(a, 16) && (!u || zi::aligned(u, 16)) && (!d || zi::aligned(d, 16)),
+               "%s: rows must be 16-byte aligned", name);
+  const int cblocks = (N + CRW_MAX_COLS - 1) / CRW_MAX_COLS;
+  const int C = ((N + cblocks - 1) / cblocks + 7) / 8 * 8;
+  const int nt = C / 8;
+  const int nin = mode == 1 ? 2 : 1;
+  int R = 16384 / (C * 2);
+  R = R < 1 ? 1 : (R > 8 ? 8 : R);
+  const size_t smem = (size_t)CRW_STAGES * nin * R * C * 2 + 64;
+  int per_sm = 2;   // enough bytes in flight per SM; more CTAs only add partial rows
+  const int by_smem = (int)(200000 / smem);
+  if (per_sm > by_smem) per_sm = by_smem;
+  if (per_sm < 1) per_sm = 1;
+  int chunks = (sm_count() * per_sm + cblocks - 1) / cblocks;
+  const int max_chunks = (T + R - 1) / R;
   if (chunks > max_chunks) chunks = max_chunks;
   if (chunks < 1) chunks = 1;
-  const int rows_per = (T + chunks - 1) / chunks;
+  const int rows_per = ((T + chunks - 1) / chunks + R - 1) / R * R;
   chunks = (T + rows_per - 1) / rows_per;
-  const size_t need = 1024 + (size_t)(mode == 2 ? 2 : 1) * chunks * N;
-  ZI_CHECK_ARG(work_elems >= need, "%s: work needs %zu floats", name, need);
-  int* counters = reinterpret_cast<int*>(work);
+  ZI_CHECK_ARG(work_elems >= 1024 + (size_t)chunks * N, "%s: work needs %zu floats", name,
+               1024 + (size_t)chunks * N);
   float* part = work + 1024;
+  static bool attr[2] = {false, false};
+  if (!attr[mode]) {
+    ZI_CUDA(cudaFuncSetAttribute(mode ? colrow_kernel<1> : colrow_kernel<0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+            "cudaFuncSetAttribute(colrow)");
+    attr[mode] = true;
+  }
   dim3 grid(cblocks, chunks);
   const uint16_t* A = static_cast<const uint16_t*>(a);
   const uint16_t* U = static_cast<const uint16_t*>(u);
   uint16_t* D = static_cast<uint16_t*>(d);
-  if (mode == 0)
-    colred_kernel<0><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
-  else if (mode == 1)
-    colred_kernel<1><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
-  else
-    colred_kernel<2><<<grid, 256, 0, s>>>(A, U, D, mean, rstd, part, counters, out0, out1, out_f32, T, N, rows_per);
+  if (mode == 0) colrow_kernel<0><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per);
+  else colrow_kernel<1><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per);
+  int st = zi::launch_status(name);
+  if (st) return st;
+  ln_fold_kernel<<<dim3((N + 31) / 32, 1), 32 * FOLD_SUB, 0, s>>>(part, chunks, N, out, nullptr,
+                                                                 nullptr, out_f32);
   return zi::launch_status(name);
 }
 
 int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, const float* rstd,
-              const void* dres, void* dx, void* dgamma, void* dbeta, int grads_f32, float* work,
-              size_t work_elems, int T, int H, void* stream) {
+              const void* dres, void* dx, void* dgamma, void* dbeta, void* dres_sum, int grads_f32,
+              float* work, size_t work_elems, int T, int H, void* stream) {
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
+  ZI_CHECK_ARG(!dres_sum || dres, "zi_ln_bwd: dres_sum needs dres");
+  ZI_CHECK_ARG(zi::aligned(dy, 16) && zi::aligned(x, 16) && zi::aligned(dx, 16) &&
+               (!dres || zi::aligned(dres, 16)), "zi_ln_bwd: rows must be 16-byte aligned");
   ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..8192, power of 2");
   cudaStream_t s = (cudaStream_t)stream;
-  const int grid = ln_grid(T, H);
-  TPR_DISPATCH(H, ln_bwd_dx_kernel, grid, s, (const uint16_t*)dy, (const uint16_t*)x,
-               (const uint16_t*)w, mean, rstd, (const uint16_t*)dres, (uint16_t*)dx, T);
-  int st = zi::launch_status("zi_ln_bwd(dx)");
+  const int tpr = H / 8;
+  const int rpc = tpr >= LNB_NT ? 1 : LNB_NT / tpr;
+  int grid = (tpr > LNB_NT ? 1 : 2) * sm_count();
+  if (grid > (T + rpc - 1) / rpc) grid = (T + rpc - 1) / rpc;
+  const int sets = dres_sum ? 3 : 2;
+  // work[0, 1024) holds the column-reduction counters (must stay zero); partials follow
+  ZI_CHECK_ARG(work_elems >= 1024 + (size_t)sets * grid * H, "zi_ln_bwd: work needs %zu floats",
+               1024 + (size_t)sets * grid * H);
+  float* part = work + 1024;
+  const bool rs = dres_sum != nullptr;
+  auto DY = (const uint16_t*)dy, X = (const uint16_t*)x, W = (const uint16_t*)w,
+       DR = (const uint16_t*)dres;
+  auto DX = (uint16_t*)dx;
+  int st = ZI_OK;
+  switch (tpr) {
+    case 16: st = launch_ln_bwd<16>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 32: st = launch_ln_bwd<32>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 64: st = launch_ln_bwd<64>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 128: st = launch_ln_bwd<128>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 256: st = launch_ln_bwd<256>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 512: st = launch_ln_bwd<512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 1024: st = launch_ln_bwd<1024>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+  }
   if (st) return st;
-  return launch_colred(2, dy, x, nullptr, mean, rstd, dgamma, dbeta, grads_f32, work, work_elems,
-                       T, H, s, "zi_ln_bwd(gamma/beta)");
+  if ((st = zi::launch_status("zi_ln_bwd(dx)"))) return st;
+  ln_fold_kernel<<<dim3((H + 31) / 32, sets), 32 * FOLD_SUB, 0, s>>>(part, grid, H, dgamma, dbeta, dres_sum,
+                                                          grads_f32);
+  return zi::launch_status("zi_ln_bwd(fold)");
+}
+
+int zi_gelu_fwd(const void* u, void* y, size_t n, void* stream) {
+  ZI_CHECK_ARG(u && y && n % 8 == 0, "zi_gelu_fwd: need n % 8 == 0");
+  ZI_CHECK_ARG(zi::aligned(u, 16) && zi::aligned(y, 16), "zi_gelu_fwd: 16-byte aligned buffers");
+  const size_t n8 = n / 8;
+  size_t g = (n8 + 255) / 256;
+  const size_t cap = (size_t)sm_count() * 8;
+  if (g > cap) g = cap;
+  if (g == 0) return ZI_OK;
+  gelu_fwd_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)u, (uint16_t*)y, n8);
+  return zi::launch_status("zi_gelu_fwd");
 }
 
 int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, float* work,
                  size_t work_elems, int T, int N, void* stream) {
   ZI_CHECK_ARG(dy && db && work && T > 0 && N > 0, "zi_bias_grad: bad arguments");
   ZI_CHECK_ARG(!u || du, "zi_bias_grad: gelu backward needs du");
-  return launch_colred(u ? 1 : 0, dy, u, du, nullptr, nullptr, db, nullptr, db_f32, work,
-                       work_elems, T, N, (cudaStream_t)stream, "zi_bias_grad");
+  return launch_colred(u ? 1 : 0, dy, u, du, db, db_f32, work, work_elems, T, N,
+                       (cudaStream_t)stream, "zi_bias_grad");
 }
 
 int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T, int V,

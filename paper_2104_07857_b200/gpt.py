@@ -560,9 +560,11 @@ class GPTZeroEngine:
         x2, h2, m2, r2 = self._ln(p, P["ln2_w"], P["ln2_b"], resid=x)
         del p
         u = torch.addmm(P["fc1_b"], h2, P["fc1_w"].t())
-        a = F.gelu(u, approximate="tanh")
+        a = torch.empty_like(u)
+        kernels.gelu_fwd(u, a)
         y = torch.addmm(P["fc2_b"], a, P["fc2_w"].t())
         y += x2
+        self.launches += 1
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
     def _block_bwd_fused(self, dy, cache, P, G):
@@ -573,7 +575,6 @@ class GPTZeroEngine:
         x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
         ws = self.ws
         torch.mm(dy.t(), a, out=G["fc2_w"])
-        kernels.bias_grad(dy, G["fc2_b"], ws)
         da = torch.mm(dy, P["fc2_w"])
         du = torch.empty_like(da)
         kernels.bias_grad(da, G["fc1_b"], ws, u=u, du=du)
@@ -582,17 +583,20 @@ class GPTZeroEngine:
         dh2 = torch.mm(du, P["fc1_w"])
         del du
         dx2 = torch.empty_like(dh2)
-        kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy)
+        # LN2 backward also sums dres = dy: the fc2 bias gradient, no extra pass
+        kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy,
+                       dres_sum=G["fc2_b"])
         torch.mm(dx2.t(), o, out=G["proj_w"])
-        kernels.bias_grad(dx2, G["proj_b"], ws)
         do = torch.mm(dx2, P["proj_w"])
         dqkv = self._attn_bwd(do, att)
         torch.mm(dqkv.t(), h1, out=G["qkv_w"])
         kernels.bias_grad(dqkv, G["qkv_b"], ws)
         dh1 = torch.mm(dqkv, P["qkv_w"])
         dx = torch.empty_like(dh1)
-        kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2)
-        self.launches += 6
+        # ... and LN1 backward sums dres = dx2: the proj bias gradient
+        kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2,
+                       dres_sum=G["proj_b"])
+        self.launches += 8
         return dx
 
     def _block_bwd(self, dy, cache, P, G):

@@ -213,12 +213,39 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, accumul
     return out
 
 
+EPI = {"plain": 0, "gelu": 1, "resid": 2, "dgelu": 3}
+
+
+def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi: str = "plain",
+            x=None, out2=None, stream=None) -> torch.Tensor:
+    """zi_gemm_ex: bf16 tcgen05 GEMM with a fused epilogue (see include/zinf.h).
+
+    plain: out = a b^T + bias; gelu: out = u = a b^T + bias, out2 = gelu(u);
+    resid: out = (a b^T + bias) + x; dgelu: out = (a b^T) * gelu'(x).
+    """
+    M, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K or out.shape != (M, N) or out.stride(1) != 1 or out.dtype != torch.bfloat16:
+        raise ValueError("gemm_ex: shape mismatch or non-row-major bf16 output")
+    for t, name in ((x, "x"), (out2, "out2")):
+        if t is not None and (t.shape != (M, N) or t.stride(1) != 1 or t.dtype != torch.bfloat16):
+            raise ValueError(f"gemm_ex: {name} must be a row-major bf16 (M, N) view")
+    pa, amn, lda = _operand(a, "a")
+    pb, bmn, ldb = _operand(b, "b")
+    _lib.call("zi_gemm_ex", pa, amn, lda, pb, bmn, ldb,
+              _dev(bias, "bias") if bias is not None else None, out.data_ptr(), out.stride(0),
+              x.data_ptr() if x is not None else None, x.stride(0) if x is not None else 0,
+              out2.data_ptr() if out2 is not None else None,
+              out2.stride(0) if out2 is not None else 0, EPI[epi], M, N, K, _stream(stream))
+    return out
+
+
 class Workspace:
     """fp32 scratch for the deterministic column reductions: 1024 self-resetting int
     counters (zeroed here once) followed by per-chunk partial rows. Use one workspace
     per stream: reductions sharing it must be stream-ordered."""
 
-    def __init__(self, elems: int = 4 << 20, device="cuda"):
+    def __init__(self, elems: int = 8 << 20, device="cuda"):
         self.t = torch.zeros(elems, dtype=torch.float32, device=device)
 
     @property
@@ -245,15 +272,29 @@ def ln_fwd(x, w, b, y, mean, rstd, eps=1e-5, resid=None, xsum=None, stream=None)
               eps, _stream(stream))
 
 
-def ln_bwd(dy, x, w, mean, rstd, dx, dgamma, dbeta, ws: Workspace, dres=None, stream=None) -> None:
-    """zi_ln_bwd: dx (+ dres), dgamma, dbeta (bf16 or fp32 outputs)."""
+def ln_bwd(dy, x, w, mean, rstd, dx, dgamma, dbeta, ws: Workspace, dres=None, dres_sum=None,
+           stream=None) -> None:
+    """zi_ln_bwd: dx (+ dres), dgamma, dbeta and optionally dres_sum = column sums of
+    dres (bf16 or fp32 outputs, all the dtype of dgamma), one pass over the rows."""
     H = x.shape[-1]
     T = x.numel() // H
     f32 = int(dgamma.dtype == torch.float32)
+    for g in (dbeta, dres_sum):
+        if g is not None and g.dtype != dgamma.dtype:
+            raise ValueError("dgamma, dbeta and dres_sum must share a dtype")
     _lib.call("zi_ln_bwd", _bf16_2d(dy, "dy"), _bf16_2d(x, "x"), _bf16_2d(w, "w"),
               _dev(mean, "mean"), _dev(rstd, "rstd"),
               _bf16_2d(dres, "dres") if dres is not None else None, _bf16_2d(dx, "dx"),
-              dgamma.data_ptr(), dbeta.data_ptr(), f32, ws.ptr, len(ws), T, H, _stream(stream))
+              dgamma.data_ptr(), dbeta.data_ptr(),
+              dres_sum.data_ptr() if dres_sum is not None else None, f32, ws.ptr, len(ws), T, H,
+              _stream(stream))
+
+
+def gelu_fwd(u, y, stream=None) -> None:
+    """zi_gelu_fwd: y = gelu_tanh(u), bf16."""
+    if y.shape != u.shape:
+        raise ValueError("gelu_fwd: shape mismatch")
+    _lib.call("zi_gelu_fwd", _bf16_2d(u, "u"), _bf16_2d(y, "y"), u.numel(), _stream(stream))
 
 
 def bias_grad(dy, db, ws: Workspace, u=None, du=None, stream=None) -> None:

@@ -58,8 +58,9 @@ def test_ln_bwd(T, H, dres):
     dx = torch.empty_like(x)
     dg = torch.empty(H, device="cuda", dtype=torch.float32)
     db = torch.empty(H, device="cuda", dtype=torch.float32)
+    ds = torch.empty(H, device="cuda", dtype=torch.float32) if dres else None
     ws = K.Workspace()
-    K.ln_bwd(dy, x, w, mean, rstd, dx, dg, db, ws, dres=dr)
+    K.ln_bwd(dy, x, w, mean, rstd, dx, dg, db, ws, dres=dr, dres_sum=ds)
     xr = x.float().requires_grad_(True)
     wr = w.float().requires_grad_(True)
     br = b.float().requires_grad_(True)
@@ -68,10 +69,38 @@ def test_ln_bwd(T, H, dres):
     close(dx, ref_dx, atol=2e-2)
     torch.testing.assert_close(dg, wr.grad, rtol=1e-3, atol=1e-3 * T ** 0.5)
     torch.testing.assert_close(db, br.grad, rtol=1e-3, atol=1e-3 * T ** 0.5)
+    if dres:   # the fused bias gradient of the linear that produced dres
+        torch.testing.assert_close(ds, dr.float().sum(0), rtol=1e-3, atol=1e-3 * T ** 0.5)
     dg2 = torch.empty_like(dg)
     db2 = torch.empty_like(db)
     K.ln_bwd(dy, x, w, mean, rstd, dx, dg2, db2, ws, dres=dr)
     assert torch.equal(dg, dg2) and torch.equal(db, db2)   # deterministic
+
+
+@pytest.mark.parametrize("n", [8, 4096 * 8, 8192 * 8192 + 8])
+def test_gelu_fwd(n):
+    g = torch.Generator(device="cuda").manual_seed(n % 1000)
+    u = (2 * torch.randn(n, device="cuda", generator=g)).bfloat16()
+    y = torch.empty_like(u)
+    K.gelu_fwd(u, y)
+    close(y, F.gelu(u.float(), approximate="tanh"), atol=1e-3)
+
+
+def test_ln_bwd_bf16_grads_and_sizes():
+    """bf16 dgamma/dbeta/dres_sum outputs; T below one CTA's rows; all H sizes."""
+    for T, H in [(3, 128), (5, 256), (17, 8192), (2048, 1024)]:
+        g = torch.Generator(device="cuda").manual_seed(T + H)
+        x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+        w = torch.ones(H, device="cuda").bfloat16()
+        dy = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+        dr = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+        y, mean, rstd = torch.empty_like(x), torch.empty(T, device="cuda"), torch.empty(T, device="cuda")
+        K.ln_fwd(x, w, torch.zeros_like(w), y, mean, rstd)
+        dx = torch.empty_like(x)
+        dg, db, ds = (torch.empty(H, device="cuda").bfloat16() for _ in range(3))
+        K.ln_bwd(dy, x, w, mean, rstd, dx, dg, db, K.Workspace(), dres=dr, dres_sum=ds)
+        close(db, dy.float().sum(0), atol=1e-2 * T ** 0.5)
+        close(ds, dr.float().sum(0), atol=1e-2 * T ** 0.5)
 
 
 @pytest.mark.parametrize("T,N", [(8192, 8192), (1000, 2048), (7, 24)])

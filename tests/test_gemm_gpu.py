@@ -88,3 +88,63 @@ def test_linear_fwd_strided_views():
         kernels.linear_fwd(x, w[t * R:(t + 1) * R], None, y[:, t * R:(t + 1) * R])
     torch.cuda.synchronize()
     check(y, ref(x, w, None), K)
+
+
+@pytest.mark.parametrize("wide", ["0", "1"])
+@pytest.mark.parametrize("M,N,K", [(256, 512, 128), (1000, 1032, 320), (2048, 6144, 2048),
+                                   (520, 2048, 8192)])
+@pytest.mark.parametrize("layout", ["fwd", "dx", "dw"])
+def test_wide_and_narrow_tiles(M, N, K, layout, wide):
+    """gemm_ex (always the 256x512 pair tile) and gemm (heuristic) on every operand layout."""
+    torch.manual_seed(M * 7 + N + K)
+    a = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    b = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * K ** -0.5
+    if layout == "dx":     # B N-major: b is a transposed view of a (K, N) tensor
+        b = b.t().contiguous().t()
+    if layout == "dw":     # A and B MN-major
+        a = a.t().contiguous().t()
+        b = b.t().contiguous().t()
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    kernels.gemm_ex(a, b, y) if wide == "1" else kernels.gemm(a, b, y)
+    torch.cuda.synchronize()
+    check(y, a.float() @ b.float().t(), K)
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 8192, 2048), (300, 1032, 256), (1024, 2048, 8192)])
+@pytest.mark.parametrize("epi", ["bias", "gelu", "resid", "dgelu"])
+def test_fused_epilogues(M, N, K, epi):
+    """Each fused epilogue against the unfused bf16 sequence of torch ops."""
+    import torch.nn.functional as F
+    torch.manual_seed(M + N)
+    x = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    w = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) * K ** -0.5
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16)
+    acc = x.float() @ w.float().t()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    if epi == "bias":
+        kernels.gemm_ex(x, w, out, bias=bias)
+        check(out, acc + bias.float(), K)
+    elif epi == "gelu":
+        g = torch.empty_like(out)
+        kernels.gemm_ex(x, w, out, bias=bias, epi="gelu", out2=g)
+        check(out, acc + bias.float(), K)
+        gr = F.gelu(out.float(), approximate="tanh")
+        err = (g.float() - gr).abs()
+        assert (err <= gr.abs() * 2 ** -7 + 2e-3).all(), err.max().item()
+    elif epi == "resid":
+        r = torch.randn(M, N, device="cuda", dtype=torch.bfloat16)
+        kernels.gemm_ex(x, w, out, bias=bias, epi="resid", x=r)
+        y = acc + bias.float()
+        ref = y.bfloat16().float() + r.float()
+        # two roundings as in the unfused path: bf16(y) then bf16(bf16(y) + r); the
+        # first can move by one ulp of |y| (fp32 accumulation order), which is not
+        # small relative to ref when y and r cancel
+        err = (out.float() - ref).abs()
+        tol = ref.abs() * 2 ** -7 + y.abs() * 2 ** -7 + K * 2 ** -20
+        assert (err <= tol).all(), err.max().item()
+    else:
+        u = (acc + bias.float()).bfloat16()
+        kernels.gemm_ex(x, w, out, epi="dgelu", x=u)
+        dref = torch.ops.aten.gelu_backward(acc.bfloat16().float(), u.float(), approximate="tanh")
+        err = (out.float() - dref).abs()
+        assert (err <= dref.abs() * 2 ** -6 + K * 2 ** -19 + 2e-3).all(), err.max().item()
