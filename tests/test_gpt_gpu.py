@@ -149,11 +149,13 @@ def test_10b_70b_layer_shapes(hd, heads):
     assert np.isfinite(la) and abs(la - lb) <= 2e-3 * abs(lb)
 
 
-def test_fused_kernels_match_torch_path():
-    """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path."""
-    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True)
+@pytest.mark.parametrize("fused_gemm", [False, True])
+def test_fused_kernels_match_torch_path(fused_gemm):
+    """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path (and optionally the
+    GELU / dGELU GEMM epilogues) vs the torch-op path."""
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True, fused_gemm=fused_gemm)
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=False)
-    assert a.fused and not b.fused
+    assert a.fused and not b.fused and a.fused_gemm == fused_gemm
     a.capture_grads = b.capture_grads = True
     bs = batches_for(SMALL, 2)
     la, lb = a.step(bs).item(), b.step(bs).item()
