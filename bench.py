@@ -412,6 +412,7 @@ def offload_leg(cfg, args) -> dict:
     t0.record()
     for s in range(steps):
         eng.step([bs[s % 2]])
+    eng.flush()          # the last step's deferred write-back is inside the timed region
     t1.record()
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
@@ -472,9 +473,73 @@ def offload_leg(cfg, args) -> dict:
                                   "rel_error": round(sim["rel_error"], 4)}}
     del eng
     torch.cuda.empty_cache()
+    out["config3_equiv"] = offload_equiv_leg(args)
     if not args.no_nvme:
         out["nvme_optimizer"] = nvme_leg(cfg, args, bs, steps)
     return out
+
+
+def offload_equiv_leg(args, batch: int = 64) -> dict:
+    """Config 3's per-GPU balance on one GPU: 1.3B with ``batch`` sequences per step.
+
+    BASELINE config 3 (10B, N=8) gives each GPU 8*8192*10.28e9 = 6.7e14 step flops and a
+    1.28 G-element optimizer shard (31.5 GB of master/m/v traffic per step). The 1.3B model
+    at 64 sequences has the same per-GPU flops (8*65536*1.31e9 = 6.9e14) and exactly the
+    same optimizer traffic, so its step shows whether the offload hides behind the backward
+    at config 3's compute-to-transfer ratio. Hidden fraction by the SURVEY §8(d) formula:
+    1 - (t_offload - t_hbm) / t_transfer, t_transfer = bytes / measured duplex peak; the
+    traced Timeline's overlap is reported beside it."""
+    import dataclasses
+    import torch
+    from paper_2104_07857_b200 import gpt as eg
+    from paper_2104_07857_b200.comm import LocalComm
+    from paper_2104_07857_b200.store import TierKind
+    cfg = dataclasses.replace(eg.GPT_1P3B, batch=batch)
+    peak = host_link_peak()
+    bs = [eg.synthetic_tokens(cfg, 7, 0, s) for s in range(2)]
+    steps = max(2, min(args.steps, 3))
+    res = {}
+    for name, optim in (("hbm", TierKind.DEVICE), ("offload", TierKind.HOST)):
+        eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4,
+                               placement=eg.Placement(TierKind.DEVICE, optim))
+        for w in range(2):
+            eng.step([bs[w % 2]])
+        torch.cuda.synchronize()
+        b0 = getattr(eng, "offload_bytes", 0)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for s in range(steps):
+            loss = eng.step([bs[s % 2]])
+        eng.flush()      # deferred optimizer-state write-back lands inside the timed region
+        t1.record()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1) / steps
+        res[name] = {"ms": ms, "bytes": (getattr(eng, "offload_bytes", 0) - b0) / steps, "loss": float(loss.item())}
+        if optim is TierKind.HOST:
+            eng.trace = True
+            eng.step([bs[0]])
+            tl = eng.timeline()
+            res[name]["tl_hidden"] = tl.hidden_fraction(("pcie",))
+            res[name]["pcie_busy_s"] = tl.lane_busy_s("pcie")
+            eng.trace = False
+        del eng
+        torch.cuda.empty_cache()
+    moved = res["offload"]["bytes"]
+    t_xfer = moved / (peak["duplex_gbs"] * 1e9) * 1e3
+    exposed = res["offload"]["ms"] - res["hbm"]["ms"]
+    fl = eg.model_flops_per_step(cfg)
+    return {"workload": f"GPT-1.3B x {batch} seq/GPU (config 3 per-GPU flops and optimizer "
+                        "traffic), fp32 optimizer state in pinned host DRAM",
+            "ms_per_step_hbm": round(res["hbm"]["ms"], 2),
+            "ms_per_step_offload": round(res["offload"]["ms"], 2),
+            "tflops_offload": round(fl / (res["offload"]["ms"] / 1e3) / 1e12, 1),
+            "host_bytes_per_step": int(moved),
+            "transfer_ms_at_duplex_peak": round(t_xfer, 2),
+            "exposed_ms": round(exposed, 2),
+            "hidden_fraction": round(max(0.0, 1.0 - exposed / t_xfer), 4) if t_xfer > 0 else None,
+            "timeline_pcie_hidden_behind_compute": round(res["offload"]["tl_hidden"], 4),
+            "timeline_pcie_busy_s": round(res["offload"]["pcie_busy_s"], 4),
+            "loss_hbm": res["hbm"]["loss"], "loss_offload": res["offload"]["loss"]}
 
 
 def nvme_leg(cfg, args, bs, steps) -> dict:

@@ -160,7 +160,8 @@ class GPTZeroEngine:
                  prefetch: bool = True, copy_engine_gather: bool = False,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
-                 nvme_root: str | None = None, fused_gemm: bool | None = None):
+                 nvme_root: str | None = None, fused_gemm: bool | None = None,
+                 offload_slots: int = 12):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -180,6 +181,7 @@ class GPTZeroEngine:
         self.nvme_root = nvme_root
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
+        self.offload_slots = offload_slots
         self.overlap_opt = overlap_opt
         if act_ckpt not in (None, "device", "host"):
             raise ValueError("act_ckpt must be None, 'device' or 'host'")
@@ -370,13 +372,33 @@ class GPTZeroEngine:
                                for _ in range(2)] for _ in range(nloc)]
         self.gfree = {}          # grad slot -> event: optimizer finished reading it
         if self.offload:
+            # The step's optimizer-state chunks in the order the backward consumes them
+            # (head bucket, blocks last-to-first, embed), every local rank's shard in
+            # balanced chunks. They stream through a ring of NS HBM staging slots:
+            # chunk q lives in slot (base + q) % NS, its H2D is issued NS-1 chunks
+            # ahead of its rs_adam and waits only for the D2H that last drained the slot.
             C = self.offload_chunk
-            NS = 3  # staging slots: H2D(c+2) || rs_adam(c+1) || D2H(c)
+            self._ochunks, self._obucket = [], {}
+            order = [self.buckets[-1]] + self.buckets[1:-1][::-1] + [self.buckets[0]]
+            for b in order:
+                idx = []
+                for li in range(nloc):
+                    L = b.shard
+                    nch = -(-L // C)
+                    cs = -(-L // nch)                 # balanced chunks, no runt tail
+                    for s0 in range(0, L, cs):
+                        idx.append(len(self._ochunks))
+                        self._ochunks.append((b, li, s0, min(cs, L - s0)))
+                self._obucket[b.key] = idx
+            # NS <= chunks per step: the in-order D2H stream then guarantees that chunk
+            # q's previous-step write-back landed before its next H2D (slot reuse events)
+            NS = max(3, min(self.offload_slots, len(self._ochunks)))
             self.stage = [[torch.empty(C, dtype=torch.float32, device=self.dev) for _ in range(3)]
                           for _ in range(NS)]
             self.stage16 = [torch.empty(C, dtype=self.half, device=self.dev) for _ in range(NS)]
             self.ev_d2h = [None] * NS
-            self._stage_ctr = 0
+            self._obase = 0          # global index of this step's chunk 0
+            self._oh2d = {}          # chunk -> H2D-complete event (this step)
             self.offload_bytes = 0
 
     # ------------------------------------------------------------- fetch/release
@@ -776,81 +798,94 @@ class GPTZeroEngine:
                 ev.record(os_)
                 self.gfree[key] = ev
 
+    def _ostate_h2d(self, q: int) -> None:
+        """Issue the H2D of this step's optimizer-state chunk q into its staging slot
+        (the cg lane), behind the D2H that last drained the slot."""
+        if q >= len(self._ochunks) or q in self._oh2d:
+            return
+        b, li, s, n = self._ochunks[q]
+        k = (self._obase + q) % len(self.stage)
+        h2d = self.h2d_stream
+        with torch.cuda.stream(h2d):
+            if self.ev_d2h[k] is not None:
+                h2d.wait_event(self.ev_d2h[k])     # staging slot drained
+            t0 = self._tmark(h2d)
+            for dst, a in zip(self.stage[k], (self.p32, self.m, self.v)):
+                dst[:n].copy_(self._shard_view(a, li, b)[s:s + n], non_blocking=True)
+            self._tspan(b.op, "cg", t0, self._tmark(h2d))
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        self._oh2d[q] = ev
+
     def _reduce_update_offload(self, b: Bucket, slot: int, consts, contribs, scale: float):
         """Optimizer states in pinned host DRAM (PAPER §5.1.1).
 
-        The shard streams through two HBM staging slots in chunks:
-        H2D(c+1) on the h2d stream || zi_rs_adam(c) on the optimizer stream ||
-        D2H(c-1) on the d2h stream — three engines busy at once, the compute
-        stream never waits on PCIe. The bf16 param shard is updated in place
-        in HBM (or staged back to host when params are offloaded too).
+        The bucket's chunks stream through the HBM staging ring:
+        H2D(q+NS-1) on the h2d stream || zi_rs_adam(q) on the optimizer stream ||
+        D2H(q-1) on the d2h stream — three engines busy at once, the compute
+        stream never waits on PCIe. The first NS-1 chunks of a step are
+        prefetched when the step starts (during the forward), and the last
+        chunks' D2H drains during the next forward (``defer_writeback``), so
+        the PCIe lanes stay busy across the step boundary. The bf16 param shard
+        is updated in place in HBM (or staged back to host when params are
+        offloaded too).
         """
         cur = torch.cuda.current_stream()
-        opt, h2d, d2h = self.opt_stream, self.h2d_stream, self.d2h_stream
+        opt, d2h = self.opt_stream, self.d2h_stream
         opt.wait_stream(cur)                 # grads of bucket b are complete
-        # (the host state of this bucket was settled by the previous step's
-        # final D2H: step() orders h2d after it once per step, not per bucket,
-        # so consecutive buckets stream back to back)
         host_params = self.placement.params is TierKind.HOST
-        C = self.offload_chunk
         NS = len(self.stage)
-        for li, r in enumerate(self.ranks):
+        for q in self._obucket[b.key]:
+            _, li, s, n = self._ochunks[q]
+            r = self.ranks[li]
             L = b.shard
             hp, hm, hv = (self._shard_view(a, li, b) for a in (self.p32, self.m, self.v))
             p16 = self._shard_view(self.p16, li, b)
-            nch = -(-L // C)
-            cs = -(-L // nch)                 # balanced chunks, no runt tail
-            chunks = [(s, min(cs, L - s)) for s in range(0, L, cs)]
-            slots = []                        # staging slot of each chunk (rolling, global)
-            for _ in chunks:
-                slots.append(self._stage_ctr % NS)
-                self._stage_ctr += 1
-            ev_h2d = {}
-
-            def issue(ci):
-                k = slots[ci]
-                s, n = chunks[ci]
-                with torch.cuda.stream(h2d):
-                    if self.ev_d2h[k] is not None:
-                        h2d.wait_event(self.ev_d2h[k])   # staging slot drained
-                    t0 = self._tmark(h2d)
-                    for dst, src in zip(self.stage[k], (hp, hm, hv)):
-                        dst[:n].copy_(src[s:s + n], non_blocking=True)
-                    self._tspan(b.op, "cg", t0, self._tmark(h2d))
-                    ev = torch.cuda.Event()
-                    ev.record(h2d)
-                ev_h2d[ci] = ev
-
-            for ci in range(min(NS - 1, len(chunks))):
-                issue(ci)
-            for ci, (s, n) in enumerate(chunks):
-                k = slots[ci]
-                if ci + NS - 1 < len(chunks):
-                    issue(ci + NS - 1)
-                sp, sm, sv = (x[:n] for x in self.stage[k])
-                with torch.cuda.stream(opt):
-                    opt.wait_event(ev_h2d.pop(ci))
-                    ph = self.stage16[k][:n] if host_params else p16[s:s + n]
-                    kernels.rs_adam_dc(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph,
-                                       self.adam)
-                    self.launches += 1
-                    ev_c = torch.cuda.Event()
-                    ev_c.record(opt)
-                with torch.cuda.stream(d2h):
-                    d2h.wait_event(ev_c)
-                    t0 = self._tmark(d2h)
-                    for dst, src in zip((hp, hm, hv), (sp, sm, sv)):
-                        dst[s:s + n].copy_(src, non_blocking=True)
-                    if host_params:
-                        p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
-                    self._tspan(b.op, "grad_offload", t0, self._tmark(d2h))
-                    ev_d = torch.cuda.Event()
-                    ev_d.record(d2h)
-                self.ev_d2h[k] = ev_d
-                self.offload_bytes += 2 * 12 * n + (2 if host_params else 0) * n
+            k = (self._obase + q) % NS
+            self._ostate_h2d(q)
+            self._ostate_h2d(q + NS - 1)
+            sp, sm, sv = (x[:n] for x in self.stage[k])
+            with torch.cuda.stream(opt):
+                opt.wait_event(self._oh2d.pop(q))
+                ph = self.stage16[k][:n] if host_params else p16[s:s + n]
+                kernels.rs_adam_dc(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph,
+                                   self.adam)
+                self.launches += 1
+                ev_c = torch.cuda.Event()
+                ev_c.record(opt)
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_c)
+                t0 = self._tmark(d2h)
+                for dst, src in zip((hp, hm, hv), (sp, sm, sv)):
+                    dst[s:s + n].copy_(src, non_blocking=True)
+                if host_params:
+                    p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
+                self._tspan(b.op, "grad_offload", t0, self._tmark(d2h))
+                ev_d = torch.cuda.Event()
+                ev_d.record(d2h)
+            self.ev_d2h[k] = ev_d
+            self.offload_bytes += 2 * 12 * n + (2 if host_params else 0) * n
         ev_free = torch.cuda.Event()
         ev_free.record(opt)
         self.gfree["embed" if b.key == "embed" else slot] = ev_free
+
+    @property
+    def defer_writeback(self) -> bool:
+        """Optimizer-offload steps end when the last rs_adam is done, not when its
+        D2H landed: the fp32 write-back drains during the next forward, which reads
+        only the bf16 params (updated in HBM). Not with params on the host (the next
+        gather reads the written-back bf16 shards), host checkpoints (d2h stream
+        shared), or under graph capture (every side stream must rejoin)."""
+        return (self.offload and self.placement.params is TierKind.DEVICE
+                and self.act_ckpt != "host"
+                and not torch.cuda.is_current_stream_capturing())
+
+    def flush(self) -> None:
+        """Order the current stream after every in-flight host transfer (the deferred
+        optimizer-state write-back); host-side readers then synchronize as usual."""
+        cur = torch.cuda.current_stream()
+        cur.wait_stream(self.d2h_stream)
+        cur.wait_stream(self.h2d_stream)
 
     # ------------------------------------------------- activation checkpoints (PAPER §5.1.2)
     def _ckpt_save(self, li: int, i: int, x_in: torch.Tensor):
@@ -927,7 +962,10 @@ class GPTZeroEngine:
             self.comm.device_barrier()  # peers' previous-step Adam writes are done
             self.launches += 1
         if self.offload:
-            self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
+            if not self.defer_writeback:
+                self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
+            self._obase += len(self._ochunks)
+            self._oh2d = {}
         self._spans = []
         self._pending_free = None
         # events of the previous step are complete (cur joined every side stream at its
@@ -937,8 +975,12 @@ class GPTZeroEngine:
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
         self._nvme_wait = {}
-        self._phase = "forward"
         self._t0 = self._tmark(cur)
+        if self.offload:      # cg prefetch of the backward's first chunks, during the forward
+            self._phase = "backward"
+            for q in range(len(self.stage) - 1):
+                self._ostate_h2d(q)
+        self._phase = "forward"
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
         E, FB = self.buckets[0], self.buckets[-1]
@@ -1037,8 +1079,8 @@ class GPTZeroEngine:
         if self.nvme:
             self.streamer.drain()         # every bucket's states are back on NVMe
         cur.wait_stream(self.opt_stream)  # the step ends when the last bucket is updated
-        if self.offload or self.nvme or self.act_ckpt == "host":  # ... and host transfers landed
-            cur.wait_stream(self.d2h_stream)
+        if (self.offload and not self.defer_writeback) or self.nvme or self.act_ckpt == "host":
+            cur.wait_stream(self.d2h_stream)  # ... and host transfers landed
             cur.wait_stream(self.h2d_stream)
         if gs is not cur:
             cur.wait_stream(gs)       # join the gather stream (required for graph capture)
@@ -1110,6 +1152,9 @@ class GPTZeroEngine:
                    for n in ("p32", "m", "v")}
             out["p16"] = self._shard_view(self.p16, li, b)
             return out
+        if self.offload:
+            self.flush()
+            torch.cuda.current_stream().synchronize()   # host states: write-back landed
         return {n: self._shard_view(a, li, b) for n, a in
                 (("p16", self.p16), ("p32", self.p32), ("m", self.m), ("v", self.v))}
 

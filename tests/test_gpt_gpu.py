@@ -178,15 +178,20 @@ def test_loss_decreases_and_world_sizes_agree():
     assert np.isfinite(out[1]).all() and np.isfinite(out[2]).all()
 
 
-@pytest.mark.parametrize("params_host", [False, True])
-def test_offload_matches_hbm(params_host):
+@pytest.mark.parametrize("params_host,slots", [(False, 3), (False, 12), (False, 10_000),
+                                               (True, 12)])
+def test_offload_matches_hbm(params_host, slots):
     """Optimizer states (and optionally bf16 params) in pinned host DRAM, streamed in
-    small chunks through the staging pipeline: same result as all-in-HBM."""
+    small chunks through the staging ring (prefetched across the step boundary, write-back
+    deferred into the next forward): same result as all-in-HBM. slots=10_000 clamps the
+    ring to the step's chunk count, the edge of the slot-reuse ordering argument."""
     from paper_2104_07857_b200.gpt import Placement
     from paper_2104_07857_b200.store import TierKind
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
     pl = Placement(params=TierKind.HOST if params_host else TierKind.DEVICE, optim=TierKind.HOST)
-    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007)
+    b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007,
+                         offload_slots=slots)
+    assert len(b.stage) <= len(b._ochunks)
     assert not b.p32.is_cuda and b.p32.is_pinned()
     for step in range(3):
         bs = batches_for(SMALL, 2, step)
