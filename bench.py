@@ -42,6 +42,16 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def _ncu_traffic(kernel: str):
+    """DRAM read+write bytes per launch of ``kernel`` from the committed ncu --set full
+    capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -304,7 +314,7 @@ def run_ours(args):
                          "frac": round(achieved / hbm, 4),
                          "bytes_per_launch": big, "avg_launch_ms": round(avg_ms, 4),
                          "share_of_step": round(rs_share, 4),
-                         "traffic": None},
+                         "traffic": _ncu_traffic("zi_rs_adam_dc")},
             "clocks": clocks.summary(),
             "offload": offload,
             "collectives": collectives,
