@@ -9,7 +9,8 @@
  *   - Every call returns a zi_status; on failure zi_last_error() holds a
  *     thread-local message. Status codes map to the reference exception tree
  *     (store.py:54-71): ZI_ECAPACITY -> CapacityExceeded, ZI_ENOTFOUND ->
- *     KeyNotFound, ZI_EINVAL -> ValueError, ZI_ECUDA/ZI_ENCCL -> StoreError.
+ *     KeyNotFound, ZI_EINVAL -> ValueError, ZI_EEXHAUSTED -> PoolExhausted,
+ *     ZI_ECUDA/ZI_ENCCL -> StoreError.
  *   - All device work is asynchronous on the caller's `stream`
  *     (a cudaStream_t passed as void*). Callers own every buffer; the
  *     library owns nothing but its error string.
@@ -33,7 +34,8 @@ typedef enum {
   ZI_ECAPACITY = 2,
   ZI_ENOTFOUND = 3,
   ZI_ECUDA = 4,
-  ZI_ENCCL = 5
+  ZI_ENCCL = 5,
+  ZI_EEXHAUSTED = 6
 } zi_status;
 
 enum { ZI_HALF_FP16 = 0, ZI_HALF_BF16 = 1 };
@@ -171,6 +173,26 @@ int zi_event_query(void* ev);                         /* ZI_OK done, ZI_ENOTFOUN
 int zi_event_sync(void* ev);
 int zi_stream_wait_event(void* stream, void* ev);
 
+/* Staging-buffer pool: the reference BufferPool (store.py:81-123). buffer_count
+ * buffers of buffer_bytes, pinned (cudaHostAlloc) or pageable (pinned = 0, hosts
+ * without a GPU). acquire hands out buffer indices LIFO; when none is free it
+ * blocks (blocking = 1; counted in waits) or returns ZI_EEXHAUSTED. release
+ * returns ZI_EINVAL for an index outside the pool ("does not belong") or when
+ * every buffer is already free ("over-released"). Thread-safe. */
+int zi_pool_create(size_t buffer_bytes, int buffer_count, int blocking, int pinned, void** pool);
+int zi_pool_destroy(void* pool);
+int zi_pool_buffer(void* pool, int index, void** ptr);
+int zi_pool_acquire(void* pool, int* index);
+int zi_pool_release(void* pool, int index);
+int zi_pool_stats(void* pool, int* free_count, uint64_t* waits);
+
+/* The offload lanes: one async copy on `stream`, then `event`
+ * (nullable, a zi_event_create event) recorded behind it — the IoTicket of
+ * store.py:126-153. H2D = cg-transfer (host tier -> HBM prefetch slot),
+ * D2H = grad / optimizer-state offload. Pinned host memory for full speed. */
+int zi_h2d_async(void* dst, const void* src, size_t bytes, void* stream, void* event);
+int zi_d2h_async(void* dst, const void* src, size_t bytes, void* stream, void* event);
+
 /* ---- CUDA IPC (peer buffers for the P2P collectives) ---------------------
  * Buffers that peers map are plain cudaMalloc allocations (zi_device_alloc)
  * so the IPC handle names exactly that buffer (offset 0). */
@@ -188,6 +210,20 @@ int zi_ipc_close(void* dptr);
  * (ldy). Requires K % 64 == 0, ldx/ldw/ldy % 8 == 0, 16-byte aligned bases. */
 int zi_linear_fwd(const void* x, const void* w, const void* bias, void* y,
                   int M, int N, int K, int ldx, int ldw, int ldy, void* stream);
+
+/* One tile of TiledLinear, the §8(b) names. Tile t holds rows
+ * [s, e) of W, so N_t = e - s:
+ *   fwd: y_t[m, n] = sum_k x[m, k] w_t[n, k] + b_t[n]       (zi_linear_fwd)
+ *   bwd: dw_t[n, k] = sum_m dy_t[m, n] x[m, k]               (bf16, ld lddw; NULL skips)
+ *        dx_acc[m, k] += sum_n dy_t[m, n] w_t[n, k]          (fp32, ld lddx; NULL skips)
+ *        db_t[n] = sum_m dy_t[m, n]                          (fp32, fixed order; NULL skips)
+ * dy_t is the tile's column block of the upstream gradient (ld lddy), so tiles
+ * are processed in order with dx accumulated sequentially. */
+int zi_linear_tile_fwd(const void* x, const void* w_t, const void* b_t, void* y, int M, int K,
+                       int N_t, int ldx, int ldw, int ldy, void* stream);
+int zi_linear_tile_bwd(const void* x, int ldx, const void* w_t, int ldw, const void* dy_t,
+                       int lddy, void* dw_t, int lddw, float* dx_acc, int lddx, float* db_t,
+                       int M, int K, int N_t, void* stream);
 
 /* General tcgen05 GEMM behind the tiled linear's forward and backward:
  *   D[m, n] = sum_k A(m, k) * B(n, k) (+ bias[n]) (+ D[m, n] if accumulate)

@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libzinf.so")
 
-ZI_OK, ZI_EINVAL, ZI_ECAPACITY, ZI_ENOTFOUND, ZI_ECUDA, ZI_ENCCL = range(6)
+ZI_OK, ZI_EINVAL, ZI_ECAPACITY, ZI_ENOTFOUND, ZI_ECUDA, ZI_ENCCL, ZI_EEXHAUSTED = range(7)
 HALF_FP16, HALF_BF16 = 0, 1
 DT_F32, DT_F16, DT_F64, DT_BF16 = 0, 1, 2, 3
 
@@ -74,6 +74,18 @@ SIGNATURES = {
     "zi_event_query": [c_void_p],
     "zi_event_sync": [c_void_p],
     "zi_stream_wait_event": [c_void_p, c_void_p],
+    "zi_pool_create": [c_size_t, c_int, c_int, c_int, ctypes.POINTER(c_void_p)],
+    "zi_pool_destroy": [c_void_p],
+    "zi_pool_buffer": [c_void_p, c_int, ctypes.POINTER(c_void_p)],
+    "zi_pool_acquire": [c_void_p, ctypes.POINTER(c_int)],
+    "zi_pool_release": [c_void_p, c_int],
+    "zi_pool_stats": [c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(c_uint64)],
+    "zi_h2d_async": [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p],
+    "zi_d2h_async": [c_void_p, c_void_p, c_size_t, c_void_p, c_void_p],
+    "zi_linear_tile_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                           c_int, c_int, c_void_p],
+    "zi_linear_tile_bwd": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
+                           c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p],
     "zi_device_alloc": [c_size_t, ctypes.POINTER(c_void_p)],
     "zi_device_free": [c_void_p],
     "zi_ipc_get_handle": [c_void_p, ctypes.c_char_p],
@@ -124,7 +136,9 @@ def check(status: int, what: str) -> None:
     if status == ZI_OK:
         return
     msg = f"{what}: {last_error()}"
-    from .store import CapacityExceeded, KeyNotFound  # late import: no cycle at load
+    from .store import CapacityExceeded, KeyNotFound, PoolExhausted  # late: no cycle at load
+    if status == ZI_EEXHAUSTED:
+        raise PoolExhausted(msg)
     if status == ZI_ECAPACITY:
         raise CapacityExceeded(msg)
     if status == ZI_ENOTFOUND:

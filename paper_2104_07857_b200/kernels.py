@@ -325,6 +325,39 @@ def linear_fwd(x: torch.Tensor, w: torch.Tensor, bias, y: torch.Tensor, stream=N
     for t in (x, w, y):
         if t.dtype != torch.bfloat16 or t.stride(-1) != 1:
             raise ValueError("linear_fwd: bf16 row-major operands required")
-    _lib.call("zi_linear_fwd", x.data_ptr(), w.data_ptr(),
-              _dev(bias, "bias") if bias is not None else None, y.data_ptr(), M, N, K,
+    _lib.call("zi_linear_tile_fwd", x.data_ptr(), w.data_ptr(),
+              _dev(bias, "bias") if bias is not None else None, y.data_ptr(), M, K, N,
               x.stride(0), w.stride(0), y.stride(0), _stream(stream))
+
+
+def linear_tile_bwd(x: torch.Tensor, w_t: torch.Tensor, dy_t: torch.Tensor, dw_t=None,
+                    dx_acc=None, db_t=None, stream=None) -> None:
+    """zi_linear_tile_bwd: one tile's backward on tcgen05.
+
+    dw_t (bf16 [N_t, K]) = dy_t^T x; dx_acc (fp32 [M, K]) += dy_t w_t;
+    db_t (fp32 [N_t]) = column sums of dy_t in a fixed order. ``dy_t`` may be a
+    column block of the full upstream gradient (row stride = its width).
+    """
+    M, K = x.shape
+    N = w_t.shape[0]
+    if w_t.shape[1] != K or dy_t.shape != (M, N):
+        raise ValueError("linear_tile_bwd: shape mismatch")
+    for t in (x, w_t, dy_t):
+        if t.dtype != torch.bfloat16 or t.stride(-1) != 1 or not t.is_cuda:
+            raise ValueError("linear_tile_bwd: bf16 row-major CUDA operands required")
+    if dw_t is not None and (dw_t.shape != (N, K) or dw_t.dtype != torch.bfloat16
+                             or dw_t.stride(1) != 1):
+        raise ValueError("linear_tile_bwd: dw_t must be a row-major bf16 (N_t, K) view")
+    if dx_acc is not None and (dx_acc.shape != (M, K) or dx_acc.dtype != torch.float32
+                               or dx_acc.stride(1) != 1):
+        raise ValueError("linear_tile_bwd: dx_acc must be a row-major fp32 (M, K) view")
+    if db_t is not None and (db_t.shape != (N,) or db_t.dtype != torch.float32
+                             or not db_t.is_contiguous()):
+        raise ValueError("linear_tile_bwd: db_t must be a contiguous fp32 (N_t,) tensor")
+    _lib.call("zi_linear_tile_bwd", x.data_ptr(), x.stride(0), w_t.data_ptr(), w_t.stride(0),
+              dy_t.data_ptr(), dy_t.stride(0),
+              dw_t.data_ptr() if dw_t is not None else None,
+              dw_t.stride(0) if dw_t is not None else 0,
+              dx_acc.data_ptr() if dx_acc is not None else None,
+              dx_acc.stride(0) if dx_acc is not None else 0,
+              db_t.data_ptr() if db_t is not None else None, M, K, N, _stream(stream))

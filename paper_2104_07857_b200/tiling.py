@@ -172,12 +172,14 @@ def backward_tiled(tl: TiledLinear, x: torch.Tensor, gy: torch.Tensor, store: Ti
         s, e = tl.rows[t]
         g = gy[:, s:e]
         if x.dtype == torch.bfloat16:
-            # tcgen05: dW_t = g^T x (both operands MN-major), dx += g W_t (fp32 accumulate)
-            dW[t] = kernels.gemm(g.t(), x.t(), torch.empty(e - s, tl.in_dim, dtype=x.dtype,
-                                                           device=x.device))
-            kernels.gemm(g, W_t.t(), dx, accumulate=True)
+            # zi_linear_tile_bwd on tcgen05: dW_t = g^T x, dx += g W_t (fp32 accumulate,
+            # tiles in order), db_t = fixed-order column sums of g
+            dW[t] = torch.empty(e - s, tl.in_dim, dtype=x.dtype, device=x.device)
+            dbt = torch.empty(e - s, dtype=torch.float32, device=x.device)
+            kernels.linear_tile_bwd(x, W_t, g, dw_t=dW[t], dx_acc=dx, db_t=dbt)
+            db[t] = dbt.to(x.dtype)
         else:
             dW[t] = g.t() @ x
             dx += g @ W_t
-        db[t] = g.sum(0)
+            db[t] = g.sum(0)
     return dW, db, dx.to(x.dtype)

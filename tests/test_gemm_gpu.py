@@ -148,3 +148,50 @@ def test_fused_epilogues(M, N, K, epi):
         dref = torch.ops.aten.gelu_backward(acc.bfloat16().float(), u.float(), approximate="tanh")
         err = (out.float() - dref).abs()
         assert (err <= dref.abs() * 2 ** -6 + K * 2 ** -19 + 2e-3).all(), err.max().item()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,K,N_t,width", [(256, 128, 192, 384), (300, 256, 136, 200)])
+def test_linear_tile_bwd(M, K, N_t, width):
+    """zi_linear_tile_bwd on a column block of the upstream grad (the tiled backward's
+    access pattern) against fp32 torch: dW_t, dx accumulate, db_t (fixed-order sums)."""
+    torch.manual_seed(1)
+    x = torch.randn(M, K, device="cuda").bfloat16()
+    w = torch.randn(N_t, K, device="cuda").bfloat16()
+    gy = torch.randn(M, width, device="cuda").bfloat16()
+    s0 = width - N_t
+    g = gy[:, s0:]
+    dw = torch.empty(N_t, K, device="cuda", dtype=torch.bfloat16)
+    dx0 = torch.randn(M, K, device="cuda")
+    dx = dx0.clone()
+    db = torch.empty(N_t, device="cuda")
+    kernels.linear_tile_bwd(x, w, g, dw_t=dw, dx_acc=dx, db_t=db)
+    db2 = torch.empty_like(db)
+    kernels.linear_tile_bwd(x, w, g, db_t=db2)
+    torch.cuda.synchronize()
+    gf, xf, wf = g.float(), x.float(), w.float()
+    torch.testing.assert_close(dw.float(), gf.t() @ xf, rtol=1e-2, atol=1e-2 * M ** 0.5)
+    torch.testing.assert_close(dx, dx0 + gf @ wf, rtol=1e-3, atol=1e-3 * N_t ** 0.5)
+    torch.testing.assert_close(db, gf.sum(0), rtol=1e-5, atol=1e-4)
+    assert torch.equal(db, db2)    # deterministic
+
+
+@pytest.mark.gpu
+def test_h2d_d2h_async_with_event():
+    from paper_2104_07857_b200 import _lib
+    from paper_2104_07857_b200 import store as S
+    import ctypes
+    pool = S.BufferPool(1 << 20, 2, pinned=True)
+    a, b = pool.acquire(), pool.acquire()
+    S._buf_tensor(a)[:] = torch.randint(0, 255, (1 << 20,), dtype=torch.uint8)
+    d = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    ev = ctypes.c_void_p()
+    _lib.call("zi_event_create", ctypes.byref(ev))
+    s = torch.cuda.Stream()
+    _lib.call("zi_h2d_async", d.data_ptr(), a.ptr, 1 << 20, s.cuda_stream, ev)
+    _lib.call("zi_d2h_async", b.ptr, d.data_ptr(), 1 << 20, s.cuda_stream, ev)
+    _lib.call("zi_event_sync", ev)
+    assert torch.equal(S._buf_tensor(a), S._buf_tensor(b))
+    _lib.call("zi_event_destroy", ev)
+    pool.release(a)
+    pool.release(b)

@@ -109,6 +109,33 @@ def test_buffer_pool_contract():
     assert p.free_count == 2
 
 
+def test_buffer_pool_native_blocking_waits():
+    """The native pool (zi_pool_*) parks a blocked acquire in C and counts it in waits."""
+    import threading
+    import time
+    p = S.BufferPool(buffer_bytes=32, buffer_count=1, blocking=True, pinned=False)
+    a = p.acquire()
+    got = []
+    t = threading.Thread(target=lambda: got.append(p.acquire()))
+    t.start()
+    time.sleep(0.2)
+    assert not got and p.waits == 1      # parked, GIL released
+    p.release(a)
+    t.join(5)
+    assert got == [a] and p.free_count == 0
+    p.release(a)
+    assert p.free_count == 1
+    # LIFO hand-out like the reference's list.pop()
+    q = S.BufferPool(buffer_bytes=8, buffer_count=3, blocking=False, pinned=False)
+    x, y = q.acquire(), q.acquire()
+    q.release(x)
+    assert q.acquire() is x
+    v = S._buf_view(y)
+    v[:3] = b"abc"
+    assert bytes(S._buf_tensor(y)[:3].numpy()) == b"abc"
+    q.close()
+
+
 def test_errors_and_visibility(tmp_path):
     st = S.TierStore(0, 1024, nvme_root=str(tmp_path), sync_io=True)
     with pytest.raises(S.KeyNotFound):
