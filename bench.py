@@ -531,6 +531,10 @@ def offload_equiv_leg(args, batch: int = 64) -> dict:
             tl = eng.timeline()
             res[name]["tl_hidden"] = tl.hidden_fraction(("pcie",))
             res[name]["pcie_busy_s"] = tl.lane_busy_s("pcie")
+            sim = eng.simulated_step(duplex=True)
+            res[name]["sim"] = {"measured_step_s": round(sim["measured_s"], 4),
+                                "predicted_duplex_s": round(sim["predicted_s"], 4),
+                                "rel_error_duplex": round(sim["rel_error"], 4)}
             eng.trace = False
         del eng
         torch.cuda.empty_cache()
@@ -549,6 +553,7 @@ def offload_equiv_leg(args, batch: int = 64) -> dict:
             "hidden_fraction": round(max(0.0, 1.0 - exposed / t_xfer), 4) if t_xfer > 0 else None,
             "timeline_pcie_hidden_behind_compute": round(res["offload"]["tl_hidden"], 4),
             "timeline_pcie_busy_s": round(res["offload"]["pcie_busy_s"], 4),
+            "simulator_calibration": res["offload"]["sim"],
             "loss_hbm": res["hbm"]["loss"], "loss_offload": res["offload"]["loss"]}
 
 

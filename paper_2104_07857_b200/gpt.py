@@ -440,12 +440,15 @@ class GPTZeroEngine:
         (1, 1, 1); the head is the first backward op and the embedding the
         last. Comparing with the measured step tests the simulator's lane model.
 
-        In the offload placement a bucket's optimizer-state H2D and D2H chunks
-        run after its compute. With ``duplex=False`` (the SPEC's single pcie
-        lane) both count as that op's ``grad_offload``. With ``duplex=True`` the
-        H2D half becomes the op's post-compute ``reduce_scatter`` stage on lane
-        ``pcie_h2d`` and the D2H half stays ``grad_offload`` on ``pcie_d2h``.
-        That models the two copy engines of a full-duplex link.
+        In the offload placement a bucket's optimizer-state H2D is its ``cg``
+        stage, prefetched through the staging ring: the ring runs NS-1 chunks
+        ahead, i.e. ``d`` ops at the block buckets' chunk count, so the backward
+        plan has depths (d, d, 1). Its D2H is the post-compute ``grad_offload``.
+        With ``duplex=False`` both share the SPEC's single ``pcie`` lane; with
+        ``duplex=True`` they run on ``pcie_h2d`` / ``pcie_d2h``, the two copy
+        engines of a full-duplex link. The simulator runs the forward and the
+        backward back to back, so the ring's prefetch during the forward and the
+        write-back drained into the next forward are outside its model.
         """
         from .schedule import (Op, OperatorSequence, costs_from_timeline, plan_prefetch,
                                simulate, simulate_backward)
@@ -453,20 +456,21 @@ class GPTZeroEngine:
         fwd_ops = [E.op] + [b.op for b in blocks]
         bwd_ops = [FB.op] + [b.op for b in reversed(blocks)] + [E.op]
 
-        def plan(ids):
+        def plan(ids, depths=(1, 1, 1)):
             return plan_prefetch(OperatorSequence(tuple(Op(i, (), 1, 1) for i in ids),
-                                                 "backward"), (1, 1, 1))
+                                                 "backward"), depths)
         fwd_tl, bwd_tl = self.timeline("forward"), self.timeline("backward")
-        smap = None
+        bwd_depths = (1, 1, 1)
         if self.offload:
-            smap = {"cg": "reduce_scatter" if duplex else "grad_offload"}
+            per_op = len(self._obucket[(blocks[0] if blocks else FB).key])
+            d = max(1, -(-(len(self.stage) - 1) // max(1, per_op)))
+            bwd_depths = (d, d, 1)
         if duplex:
-            lanes = dict({"reduce_scatter": "pcie_h2d" if self.offload else "d2d",
-                          "grad_offload": "pcie_d2h"}, **(lanes or {}))
+            lanes = dict({"cg": "pcie_h2d", "grad_offload": "pcie_d2h"}, **(lanes or {}))
         fc = costs_from_timeline(fwd_tl, fwd_ops)
-        bc = costs_from_timeline(bwd_tl, bwd_ops, smap)
+        bc = costs_from_timeline(bwd_tl, bwd_ops)
         sf = simulate(plan(fwd_ops), fc, lanes=lanes)
-        sb = simulate_backward(plan(bwd_ops), bc, lanes=lanes)
+        sb = simulate_backward(plan(bwd_ops, bwd_depths), bc, lanes=lanes)
         measured = self.timeline().total_s
         predicted = sf.total_s + sb.total_s
         return {"measured_s": measured, "predicted_s": predicted,
