@@ -176,6 +176,9 @@ def run_ours(args):
         comm = LocalComm(1)
     cfg = eg.GPT_1P3B
     eng = eg.GPTZeroEngine(cfg, comm, seed=7, lr=1e-4)
+    from paper_2104_07857_b200 import gemm_select
+    # per-site GEMM choice (zi_gemm vs cuBLAS), timed at engine init on the step's shapes
+    gemm_sites = gemm_select.report() or dict(eng.gsel)
 
     def barrier():
         if world > 1:
@@ -307,6 +310,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": cfg.batch * (cfg.seq + 1) * 8,
                     "d2h_bytes_per_step": 4},
             "gpu_launches": launches,
+            "gemm_sites": gemm_sites,
             "roofline": {"kernel": "zi_rs_adam_dc (fused RS + cast + Adam, 50.4M-element block "
                                    "bucket, 28 B/elem)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,

@@ -149,6 +149,11 @@ class Placement:
     optim: TierKind = TierKind.DEVICE      # fp32 master / m / v shards
 
 
+_GEMM_SITES = ("qkv.fwd", "proj.fwd", "fc1.fwd", "fc2.fwd", "fc2.dW", "fc2.dx", "fc1.dW",
+               "fc1.dx", "proj.dW", "proj.dx", "qkv.dW", "qkv.dx", "head.fwd", "head.dW",
+               "head.dx")
+
+
 class GPTZeroEngine:
     """Partitioned ZeRO-3 engine over a communicator (LocalComm or DistComm)."""
 
@@ -160,7 +165,7 @@ class GPTZeroEngine:
                  prefetch: bool = True, copy_engine_gather: bool = False,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
-                 nvme_root: str | None = None, fused_gemm: bool | None = None,
+                 nvme_root: str | None = None, gemm_select: str | None = None,
                  offload_slots: int = 12):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
@@ -210,14 +215,21 @@ class GPTZeroEngine:
                       and fused)
         self.ws = kernels.Workspace(max(4 << 20, 2 * 148 * cfg.hd, 600 * 4 * cfg.hd),
                                     device=self.dev) if self.fused else None
-        # Optional: fc1 forward with GELU and fc2's input gradient with GELU' as tcgen05
-        # GEMMs with fused epilogues (zi_gemm_ex). Measured on the 1.3B step it is
-        # 0.4 ms slower than cuBLAS + the separate GELU passes (the single-accumulator
-        # wide tile loses ~4 % to cuBLAS at K = 2048 under the power cap), so it is
-        # off unless ZI_FUSED_GEMM=1.
-        if fused_gemm is None:
-            fused_gemm = os.environ.get("ZI_FUSED_GEMM", "0") == "1"
-        self.fused_gemm = self.fused and fused_gemm
+        # Per-site choice between zi_gemm (tcgen05, with the neighbouring elementwise
+        # pass folded into its epilogue where the site has one) and cuBLAS + a separate
+        # pass, timed once per process on this engine's shapes (gemm_select.py).
+        # "auto" (default, or ZI_GEMM_SELECT) tunes; "zi" / "cublas" force every site.
+        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", "auto")
+        if mode not in ("auto", "zi", "cublas"):
+            raise ValueError("gemm_select must be 'auto', 'zi' or 'cublas'")
+        self.gemm_select = mode
+        self.gsel = {}
+        if self.fused:
+            if mode == "auto":
+                from .gemm_select import tune_gpt
+                self.gsel = tune_gpt(cfg.batch * cfg.seq, cfg.hd, cfg.vocab, self.ws, self.dev)
+            else:
+                self.gsel = dict.fromkeys(_GEMM_SITES, mode)
 
     # ------------------------------------------------------------------ layout
     def _build_buckets(self):
@@ -586,59 +598,104 @@ class GPTZeroEngine:
         y += x2
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
+    def _zi(self, site: str, *ts) -> bool:
+        """Run ``site`` on zi_gemm: chosen for it, and the operands meet its alignment."""
+        if self.gsel.get(site) != "zi":
+            return False
+        from .gemm_select import aligned
+        return aligned(*ts)
+
+    def _linear(self, site, x, w, b, out=None):
+        """y = x w^T + b on the site's chosen GEMM."""
+        if out is None:
+            out = torch.empty(x.shape[0], w.shape[0], dtype=x.dtype, device=x.device)
+        if self._zi(site, x, w, b, out):
+            kernels.gemm(x, w, out, bias=b)
+            self.launches += 1
+        else:
+            torch.addmm(b, x, w.t(), out=out)
+        return out
+
+    def _mm_dw(self, site, dy, inp, out):
+        """out = dy^T inp (a weight gradient, written into its grad-bucket view)."""
+        if self._zi(site, dy, inp, out):
+            kernels.gemm(dy.t(), inp.t(), out)
+            self.launches += 1
+        elif out.dtype == dy.dtype:
+            torch.mm(dy.t(), inp, out=out)
+        else:
+            torch.ops.aten.mm.dtype_out(dy.t(), inp, out.dtype, out=out)  # fp32 out, no copy
+        return out
+
+    def _mm_dx(self, site, dy, w):
+        """dy w (an input gradient)."""
+        out = torch.empty(dy.shape[0], w.shape[1], dtype=dy.dtype, device=dy.device)
+        if self._zi(site, dy, w, out):
+            kernels.gemm(dy, w.t(), out)
+            self.launches += 1
+        else:
+            torch.mm(dy, w, out=out)
+        return out
+
     def _block_fwd_fused(self, x, P):
         """bf16 block with libzinf LayerNorms; the attention residual add is fused
-        into LN2 (x2 = x + proj(o), h2 = LN(x2) in one pass)."""
+        into LN2 (x2 = x + proj(o), h2 = LN(x2) in one pass). Each linear runs on
+        its site's GEMM (zi_gemm with bias / GELU / residual epilogues, or cuBLAS +
+        the separate pass)."""
         _, h1, m1, r1 = self._ln(x, P["ln1_w"], P["ln1_b"])
-        qkv = torch.addmm(P["qkv_b"], h1, P["qkv_w"].t())
+        qkv = self._linear("qkv.fwd", h1, P["qkv_w"], P["qkv_b"])
         o, att = self._attn_fwd(qkv)
-        p = torch.addmm(P["proj_b"], o, P["proj_w"].t())
+        p = self._linear("proj.fwd", o, P["proj_w"], P["proj_b"])
         x2, h2, m2, r2 = self._ln(p, P["ln2_w"], P["ln2_b"], resid=x)
         del p
-        if self.fused_gemm:   # u = h2 W1^T + b1 and a = gelu(u) from one GEMM epilogue
-            u = torch.empty(h2.shape[0], P["fc1_w"].shape[0], dtype=h2.dtype, device=h2.device)
-            a = torch.empty_like(u)
+        T, H4 = h2.shape[0], P["fc1_w"].shape[0]
+        u = torch.empty(T, H4, dtype=h2.dtype, device=h2.device)
+        a = torch.empty_like(u)
+        if self._zi("fc1.fwd", h2, P["fc1_w"], P["fc1_b"], u, a):
             kernels.gemm_ex(h2, P["fc1_w"], u, bias=P["fc1_b"], epi="gelu", out2=a)
         else:
-            u = torch.addmm(P["fc1_b"], h2, P["fc1_w"].t())
-            a = torch.empty_like(u)
+            torch.addmm(P["fc1_b"], h2, P["fc1_w"].t(), out=u)
             kernels.gelu_fwd(u, a)
-        y = torch.addmm(P["fc2_b"], a, P["fc2_w"].t())
-        y += x2
+        y = torch.empty_like(x2)
+        if self._zi("fc2.fwd", a, P["fc2_w"], P["fc2_b"], y, x2):
+            kernels.gemm_ex(a, P["fc2_w"], y, bias=P["fc2_b"], epi="resid", x=x2)
+            self.launches += 1
+        else:
+            torch.addmm(P["fc2_b"], a, P["fc2_w"].t(), out=y)
+            y += x2
         self.launches += 1
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
     def _block_bwd_fused(self, dy, cache, P, G):
         """bf16 block backward: bias grads via deterministic column sums, GELU
-        backward fused with the fc1 bias grad, LayerNorm backward with the
-        residual gradient folded in — all libzinf; GEMMs and attention via
-        cuBLAS / cuDNN."""
+        backward fused with the fc1 bias grad (or into the fc2 input-gradient GEMM's
+        epilogue), LayerNorm backward with the residual gradient folded in — all
+        libzinf; GEMMs on their sites' choice, attention via cuDNN."""
         x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
         ws = self.ws
-        torch.mm(dy.t(), a, out=G["fc2_w"])
-        if self.fused_gemm:   # du = (dy W2) * gelu'(u) in the GEMM epilogue, then db1
-            du = torch.empty_like(u)
+        self._mm_dw("fc2.dW", dy, a, G["fc2_w"])
+        du = torch.empty_like(u)
+        if self._zi("fc2.dx", dy, P["fc2_w"], du, u):  # du = (dy W2) * gelu'(u), then db1
             kernels.gemm_ex(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
             kernels.bias_grad(du, G["fc1_b"], ws)
             self.launches += 1
         else:
             da = torch.mm(dy, P["fc2_w"])
-            du = torch.empty_like(da)
             kernels.bias_grad(da, G["fc1_b"], ws, u=u, du=du)
             del da
-        torch.mm(du.t(), h2, out=G["fc1_w"])
-        dh2 = torch.mm(du, P["fc1_w"])
+        self._mm_dw("fc1.dW", du, h2, G["fc1_w"])
+        dh2 = self._mm_dx("fc1.dx", du, P["fc1_w"])
         del du
         dx2 = torch.empty_like(dh2)
         # LN2 backward also sums dres = dy: the fc2 bias gradient, no extra pass
         kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy,
                        dres_sum=G["fc2_b"])
-        torch.mm(dx2.t(), o, out=G["proj_w"])
-        do = torch.mm(dx2, P["proj_w"])
+        self._mm_dw("proj.dW", dx2, o, G["proj_w"])
+        do = self._mm_dx("proj.dx", dx2, P["proj_w"])
         dqkv = self._attn_bwd(do, att)
-        torch.mm(dqkv.t(), h1, out=G["qkv_w"])
+        self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
         kernels.bias_grad(dqkv, G["qkv_b"], ws)
-        dh1 = torch.mm(dqkv, P["qkv_w"])
+        dh1 = self._mm_dx("qkv.dx", dqkv, P["qkv_w"])
         dx = torch.empty_like(dh1)
         # ... and LN1 backward sums dres = dx2: the proj bias gradient
         kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2,
@@ -706,17 +763,22 @@ class GPTZeroEngine:
 
     def _head_fused(self, x, PF, PE, G, targets, wte_acc):
         """libzinf LN + one-pass softmax cross-entropy over bf16 logits (in place:
-        the logits buffer becomes dlogits); cuBLAS for the tied-head GEMMs."""
+        the logits buffer becomes dlogits); the tied-head GEMMs on their sites' choice."""
         _, hf, mf, rf = self._ln(x, PF["lnf_w"], PF["lnf_b"])
-        logits = torch.mm(hf, PE["wte"].t())
+        logits = torch.empty(hf.shape[0], PE["wte"].shape[0], dtype=hf.dtype, device=hf.device)
+        if self._zi("head.fwd", hf, PE["wte"], logits):
+            kernels.gemm(hf, PE["wte"], logits)
+            self.launches += 1
+        else:
+            torch.mm(hf, PE["wte"].t(), out=logits)
         tgt = targets.reshape(-1)
         T = tgt.numel()
         rows = torch.empty(T, dtype=torch.float32, device=x.device)
         loss = torch.empty((), dtype=torch.float32, device=x.device)
         kernels.softmax_ce(logits, tgt, rows, loss, 1.0 / T)
         dlog = logits
-        torch.ops.aten.mm.dtype_out(dlog.t(), hf, torch.float32, out=wte_acc)  # fp32 out, no copy
-        dhf = torch.mm(dlog, PE["wte"])
+        self._mm_dw("head.dW", dlog, hf, wte_acc)
+        dhf = self._mm_dx("head.dx", dlog, PE["wte"])
         del logits, dlog
         dx = torch.empty_like(dhf)
         kernels.ln_bwd(dhf, x, PF["lnf_w"], mf, rf, dx, G["lnf_w"], G["lnf_b"], self.ws)

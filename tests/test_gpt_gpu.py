@@ -149,13 +149,16 @@ def test_10b_70b_layer_shapes(hd, heads):
     assert np.isfinite(la) and abs(la - lb) <= 2e-3 * abs(lb)
 
 
-@pytest.mark.parametrize("fused_gemm", [False, True])
-def test_fused_kernels_match_torch_path(fused_gemm):
-    """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path (and optionally the
-    GELU / dGELU GEMM epilogues) vs the torch-op path."""
-    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True, fused_gemm=fused_gemm)
+@pytest.mark.parametrize("gemm_select", ["cublas", "zi", "auto"])
+def test_fused_kernels_match_torch_path(gemm_select):
+    """libzinf LayerNorm / bias-grad / GELU-bwd / softmax-CE path vs the torch-op path,
+    with every linear on cuBLAS, every linear on zi_gemm (bias / GELU / residual / GELU'
+    epilogues), or the per-site timed choice."""
+    a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=True, gemm_select=gemm_select)
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, fused=False)
-    assert a.fused and not b.fused and a.fused_gemm == fused_gemm
+    assert a.fused and not b.fused and set(a.gsel) == set(eg._GEMM_SITES)
+    if gemm_select != "auto":
+        assert set(a.gsel.values()) == {gemm_select}
     a.capture_grads = b.capture_grads = True
     bs = batches_for(SMALL, 2)
     la, lb = a.step(bs).item(), b.step(bs).item()
