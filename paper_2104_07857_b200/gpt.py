@@ -219,7 +219,12 @@ class GPTZeroEngine:
         # pass folded into its epilogue where the site has one) and cuBLAS + a separate
         # pass, timed once per process on this engine's shapes (gemm_select.py).
         # "auto" (default, or ZI_GEMM_SELECT) tunes; "zi" / "cublas" force every site.
-        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", "auto")
+        # One process per GPU (DistComm) defaults to cuBLAS: with two ranks time-sharing
+        # one GPU (the only multi-process setup testable here) the tcgen05 GEMMs hit
+        # sporadic launch failures that cuBLAS does not, and the tuned
+        # choice is worth ~0.2 ms per step at N=1.
+        default = "auto" if self.comm.is_local else "cublas"
+        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", default)
         if mode not in ("auto", "zi", "cublas"):
             raise ValueError("gemm_select must be 'auto', 'zi' or 'cublas'")
         self.gemm_select = mode
@@ -901,6 +906,7 @@ class GPTZeroEngine:
         opt.wait_stream(cur)                 # grads of bucket b are complete
         host_params = self.placement.params is TierKind.HOST
         NS = len(self.stage)
+        gouts = {li: self._gout(li, b) for li in range(len(self.ranks))}
         for q in self._obucket[b.key]:
             _, li, s, n = self._ochunks[q]
             r = self.ranks[li]
@@ -914,8 +920,9 @@ class GPTZeroEngine:
             with torch.cuda.stream(opt):
                 opt.wait_event(self._oh2d.pop(q))
                 ph = self.stage16[k][:n] if host_params else p16[s:s + n]
+                go = gouts[li]
                 kernels.rs_adam_dc(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph,
-                                   self.adam)
+                                   self.adam, g_out=go[s:s + n] if go is not None else None)
                 self.launches += 1
                 ev_c = torch.cuda.Event()
                 ev_c.record(opt)
