@@ -125,6 +125,112 @@ def cpu_sample(steps: int = 1):
     return flops / dt / 1e12, dt, desc, len(os.sched_getaffinity(0))
 
 
+def cpu_components() -> dict:
+    """SURVEY §8(d)'s per-path CPU baselines on the host cores, each a bounded sample:
+    the reference tier store itself (baseline/_ref, unmodified) host- and NVMe-tier
+    write/read GB/s, and the numpy oracle's Adam, reduce-scatter and tiled linear."""
+    import tempfile
+    import numpy as np
+    from oracle import numerics as nx
+    from oracle.adam import AdamConsts, adam_update
+    from oracle.partition import reduce_scatter_cast
+    from oracle.tiling import forward_tiled
+    out = {}
+
+    def best(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    # reference store (pkg/src/infinisim/store.py) through its own public API
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    try:
+        sys.path.insert(0, ref)
+        from infinisim import store as R  # noqa: E402
+        a = np.random.default_rng(0).standard_normal(32 << 20).astype(np.float32)  # 128 MiB
+        nb = a.nbytes
+        with tempfile.TemporaryDirectory() as d:
+            st = R.TierStore(0, 4 * nb, nvme_root=d, nvme_capacity=4 * nb)
+            for tier, name in ((R.TierKind.HOST, "host"), (R.TierKind.NVME, "nvme")):
+                tw = best(lambda: st.flush([st.write("x", a, tier)]))
+                tr = best(lambda: st.read("x", tier).wait())
+                out[f"reference_store_{name}_write_gbs"] = round(nb / tw / 1e9, 2)
+                out[f"reference_store_{name}_read_gbs"] = round(nb / tr / 1e9, 2)
+                st.delete("x", tier)
+            st.close()
+        out["reference_store_sample"] = "128 MiB f32 array, best of 3 (NVMe tier: OS page cache)"
+    except Exception as e:  # noqa: BLE001
+        out["reference_store"] = f"unavailable: {e!r}"[:200]
+    finally:
+        if sys.path and sys.path[0] == ref:
+            sys.path.pop(0)
+    rng = np.random.default_rng(1)
+    n = 16 << 20
+    p, m, g = (rng.standard_normal(n).astype(np.float32) for _ in range(3))
+    v = np.abs(rng.standard_normal(n)).astype(np.float32)
+    c = AdamConsts.make(1e-4, 0.9, 0.999, 1e-8, 3)
+    t = best(lambda: adam_update(p, m, v, g, c))
+    out["oracle_adam_gbs"] = round(n * 30 / t / 1e9, 2)
+    out["oracle_adam_melem_s"] = round(n / t / 1e6, 1)
+    world, n = 8, 4 << 20
+    cs = [nx.half_bits_to_f32(nx.f32_to_half_bits(rng.standard_normal(n).astype(np.float32),
+                                                  nx.HALF_BF16), nx.HALF_BF16)
+          for _ in range(world)]
+    t = best(lambda: reduce_scatter_cast(cs, world, 1.0 / world))
+    out["oracle_reduce_scatter_gbs"] = round(world * n * 2 / t / 1e9, 2)
+    W = rng.standard_normal((4096, 4096)).astype(np.float32)
+    b = rng.standard_normal(4096).astype(np.float32)
+    x = rng.standard_normal((1024, 4096)).astype(np.float32)
+    t = best(lambda: forward_tiled(W, b, x, 4))
+    out["oracle_tiled_linear_gflops"] = round(2 * 1024 * 4096 * 4096 / t / 1e9, 1)
+    out["components_sample"] = ("Adam 16M fp32 elems (30 B/elem); RS 8 ranks x 4M bf16 "
+                                "(bus bytes = 8*n*2); tiled linear M=1024, 4096->4096, T=4 fp32")
+    return out
+
+
+def store_leg() -> dict:
+    """The tier store through the reference API on the GPU box, on
+    the same 128 MiB f32 sample as cpu_components' reference-store numbers: HOST tier
+    (pinned DRAM) and NVME tier (.shard files via the native pinned pool) from a numpy
+    array, DEVICE tier (HBM) from a CUDA tensor. Host wall clock, best of 3."""
+    import tempfile
+    import numpy as np
+    import torch
+    from paper_2104_07857_b200 import store as S
+    a = np.random.default_rng(0).standard_normal(32 << 20).astype(np.float32)
+    nb = a.nbytes
+    out = {}
+
+    def best(fn, reps=3):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    with tempfile.TemporaryDirectory() as d:
+        with S.TierStore(4 * nb, 4 * nb, nvme_root=d, nvme_capacity=4 * nb) as st:
+            src = {S.TierKind.HOST: a, S.TierKind.NVME: a,
+                   S.TierKind.DEVICE: torch.from_numpy(a).cuda()}
+            for tier, name in ((S.TierKind.DEVICE, "device"), (S.TierKind.HOST, "host"),
+                               (S.TierKind.NVME, "nvme")):
+                def rd():
+                    st.read("x", tier).wait()
+                    torch.cuda.synchronize()
+                tw = best(lambda: (st.flush([st.write("x", src[tier], tier)]),
+                                   torch.cuda.synchronize()))
+                tr = best(rd)
+                out[f"{name}_write_gbs"] = round(nb / tw / 1e9, 2)
+                out[f"{name}_read_gbs"] = round(nb / tr / 1e9, 2)
+                st.delete("x", tier)
+    out["sample"] = "128 MiB f32 array, best of 3, host wall clock; NVMe tier: OS page cache"
+    return out
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle of the path on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -283,12 +389,23 @@ def run_ours(args):
         torch.cuda.empty_cache()
         offload = offload_leg(cfg, args)
 
+    store = None
+    if world == 1 and not args.no_offload:
+        try:
+            store = store_leg()
+        except Exception as e:  # noqa: BLE001 — report, never lose the main line
+            store = {"error": repr(e)[:300]}
+
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         tf, dt, desc, cores = cpu_sample(1)
         cpu = {"value": round(tf, 6), "unit": "TFLOPS", "cores": cores, "kind": "port",
                "sample": desc, "sec_per_sample": round(dt, 3)}
+        try:
+            cpu["components"] = cpu_components()
+        except Exception as e:  # noqa: BLE001 — report, never lose the main line
+            cpu["components"] = {"error": repr(e)[:300]}
 
     if rank == 0:
         line = {
@@ -322,6 +439,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "offload": offload,
             "collectives": collectives,
+            "store": store,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
