@@ -150,6 +150,81 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
   }
 }
 
+// Warp-per-row LayerNorm forward for H = 256 * VPL (H <= 2048): each lane owns VPL
+// 8-column vectors (vector k at columns 256k + 8 * lane, so every k is one coalesced
+// 512-byte segment per warp), all of a row's loads are issued before the first use,
+// and the row statistics are warp shuffles only: no CTA barriers, so many rows'
+// loads are in flight per SM (the CTA-per-row kernel stalls on __syncthreads).
+// Same math as ln_fwd_kernel: bf16-rounded residual sum, two-pass mean / variance.
+template <int VPL>
+__global__ void __launch_bounds__(256)
+ln_fwd_warp_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
+                   uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
+                   const uint16_t* __restrict__ b, uint16_t* __restrict__ y,
+                   float* __restrict__ mean, float* __restrict__ rstd, int T, float eps) {
+  constexpr int H = 256 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < T; row += nwarps) {
+    const size_t base = (size_t)row * H + lane * 8;
+    uint4 xv[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) xv[k] = *reinterpret_cast<const uint4*>(x + base + k * 256);
+    if (r != nullptr) {
+      uint4 rv[VPL];
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) rv[k] = *reinterpret_cast<const uint4*>(r + base + k * 256);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        float a[8], c[8];
+        ld_row<8>(reinterpret_cast<const uint16_t*>(&xv[k]), a);
+        ld_row<8>(reinterpret_cast<const uint16_t*>(&rv[k]), c);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = a[i] + c[i];
+        st_row<8>(reinterpret_cast<uint16_t*>(&xv[k]), a);     // bf16(x + r)
+        *reinterpret_cast<uint4*>(xsum + base + k * 256) = xv[k];
+      }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      float a[8];
+      ld_row<8>(reinterpret_cast<const uint16_t*>(&xv[k]), a);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += a[i];
+    }
+    const float mu = warp_sum(s) * (1.0f / H);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      float a[8];
+      ld_row<8>(reinterpret_cast<const uint16_t*>(&xv[k]), a);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = a[i] - mu;
+        q += d * d;
+      }
+    }
+    const float rs = rsqrtf(warp_sum(q) * (1.0f / H) + eps);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      float a[8], wf[8], bv[8];
+      ld_row<8>(reinterpret_cast<const uint16_t*>(&xv[k]), a);
+      ld_row<8>(w + lane * 8 + k * 256, wf);
+      ld_row<8>(b + lane * 8 + k * 256, bv);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = (a[i] - mu) * rs * wf[i] + bv[i];
+      uint4 o;
+      st_row<8>(reinterpret_cast<uint16_t*>(&o), a);
+      *reinterpret_cast<uint4*>(y + base + k * 256) = o;
+    }
+    if (lane == 0) {
+      mean[row] = mu;
+      rstd[row] = rs;
+    }
+  }
+}
+
 // LayerNorm backward in one pass over dy, x (and dres):
 //   dx = rstd * (dxh - mean(dxh) - xh * mean(dxh * xh)) with dxh = dy * w, + dres;
 //   per-CTA column partials of dgamma = sum dy * xh, dbeta = sum dy and, when
@@ -215,16 +290,16 @@ ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
     const int g = blockIdx.x + i * G;
     if (g >= ngroups) break;
     const int s = i % LNB_STAGES;
-    bulk::mbar_wait(&full[s], (i / LNB_STAGES) & 1);
-    const uint16_t* st = ring + (size_t)s * NIN * ROWS_E + slot * H + t * 8;
     const int row = g * RPC + slot;
     const bool live = row < T;
     const int rr = live ? row : 0;
+    const float mu = mean[rr], rs = rstd[rr];   // issued before the stage wait
+    bulk::mbar_wait(&full[s], (i / LNB_STAGES) & 1);
+    const uint16_t* st = ring + (size_t)s * NIN * ROWS_E + slot * H + t * 8;
     float gv[8], xv[8], rv[8];
     ld_row<8>(st, gv);
     ld_row<8>(st + ROWS_E, xv);
     if (DRES) ld_row<8>(st + 2 * ROWS_E, rv);
-    const float mu = mean[rr], rs = rstd[rr];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -546,6 +621,16 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
   ZI_CHECK_ARG(!resid || xsum, "zi_ln_fwd: resid needs xsum");
   cudaStream_t s = (cudaStream_t)stream;
   ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_fwd: H must be 128..8192, power of 2");
+  if (H >= 512 && H <= 2048) {   // warp per row: 8 rows per 256-thread CTA
+    const int grid = (T + 7) / 8;
+    auto X = (const uint16_t*)x, R = (const uint16_t*)resid, W = (const uint16_t*)w,
+         B = (const uint16_t*)b;
+    auto XS = (uint16_t*)xsum, Y = (uint16_t*)y;
+    if (H == 512) ln_fwd_warp_kernel<2><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
+    else if (H == 1024) ln_fwd_warp_kernel<4><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
+    else ln_fwd_warp_kernel<8><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
+    return zi::launch_status("zi_ln_fwd");
+  }
   const int grid = ln_grid(T, H);
   TPR_DISPATCH(H, ln_fwd_kernel, grid, s, (const uint16_t*)x, (const uint16_t*)resid,
                (uint16_t*)xsum, (const uint16_t*)w, (const uint16_t*)b, (uint16_t*)y, mean, rstd,
