@@ -606,21 +606,25 @@ def offload_leg(cfg, args) -> dict:
     del eng
     torch.cuda.empty_cache()
     out["config3_equiv"] = offload_equiv_leg(args)
+    out["config5_equiv"] = offload_equiv_leg(args, batch=32, params_host=True)
     if not args.no_nvme:
         out["nvme_optimizer"] = nvme_leg(cfg, args, bs, steps)
     return out
 
 
-def offload_equiv_leg(args, batch: int = 64) -> dict:
-    """Config 3's per-GPU balance on one GPU: 1.3B with ``batch`` sequences per step.
+def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
+    """A BASELINE config's per-GPU balance on one GPU: 1.3B with ``batch`` sequences.
 
-    BASELINE config 3 (10B, N=8) gives each GPU 8*8192*10.28e9 = 6.7e14 step flops and a
-    1.28 G-element optimizer shard (31.5 GB of master/m/v traffic per step). The 1.3B model
-    at 64 sequences has the same per-GPU flops (8*65536*1.31e9 = 6.9e14) and exactly the
-    same optimizer traffic, so its step shows whether the offload hides behind the backward
-    at config 3's compute-to-transfer ratio. Hidden fraction by the SURVEY §8(d) formula:
-    1 - (t_offload - t_hbm) / t_transfer, t_transfer = bytes / measured duplex peak; the
-    traced Timeline's overlap is reported beside it."""
+    Config 3 (10B, N=8): each GPU has 8*8192*10.28e9 = 6.7e14 step flops and a 1.28 G-
+    element optimizer shard (31.5 GB of master/m/v traffic per step). The 1.3B model at 64
+    sequences has the same flops (8*65536*1.31e9 = 6.9e14) and exactly the same optimizer
+    traffic. Config 5 (70B, N=8, params + optimizer offloaded): per GPU 2.3e15 flops and
+    212 GB of optimizer + 35 GB of parameter-shard host traffic per step, 1.07e-4 B/flop;
+    the 1.3B model at 32 sequences with params and states on the host moves 36.7 GB per
+    3.4e14 flops, the same ratio (``params_host``). The leg shows whether the offload
+    hides behind compute at that ratio. Hidden fraction by the SURVEY §8(d) formula:
+    1 - (t_offload - t_hbm) / t_transfer, t_transfer = host bytes / measured duplex peak;
+    the traced Timeline's overlap is reported beside it."""
     import dataclasses
     import torch
     from paper_2104_07857_b200 import gpt as eg
@@ -631,13 +635,17 @@ def offload_equiv_leg(args, batch: int = 64) -> dict:
     bs = [eg.synthetic_tokens(cfg, 7, 0, s) for s in range(2)]
     steps = max(2, min(args.steps, 3))
     res = {}
-    for name, optim in (("hbm", TierKind.DEVICE), ("offload", TierKind.HOST)):
-        eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4,
-                               placement=eg.Placement(TierKind.DEVICE, optim))
+    H, D = TierKind.HOST, TierKind.DEVICE
+    for name, pl in (("hbm", eg.Placement(D, D)),
+                     ("offload", eg.Placement(H if params_host else D, H))):
+        eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, placement=pl)
         for w in range(2):
             eng.step([bs[w % 2]])
         torch.cuda.synchronize()
-        b0 = getattr(eng, "offload_bytes", 0)
+
+        def host_bytes():
+            return getattr(eng, "offload_bytes", 0) + getattr(eng, "fetch_bytes", 0)
+        b0 = host_bytes()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record()
         for s in range(steps):
@@ -646,8 +654,8 @@ def offload_equiv_leg(args, batch: int = 64) -> dict:
         t1.record()
         torch.cuda.synchronize()
         ms = t0.elapsed_time(t1) / steps
-        res[name] = {"ms": ms, "bytes": (getattr(eng, "offload_bytes", 0) - b0) / steps, "loss": float(loss.item())}
-        if optim is TierKind.HOST:
+        res[name] = {"ms": ms, "bytes": (host_bytes() - b0) / steps, "loss": float(loss.item())}
+        if name == "offload":
             eng.trace = True
             eng.step([bs[0]])
             tl = eng.timeline()
@@ -664,8 +672,9 @@ def offload_equiv_leg(args, batch: int = 64) -> dict:
     t_xfer = moved / (peak["duplex_gbs"] * 1e9) * 1e3
     exposed = res["offload"]["ms"] - res["hbm"]["ms"]
     fl = eg.model_flops_per_step(cfg)
-    return {"workload": f"GPT-1.3B x {batch} seq/GPU (config 3 per-GPU flops and optimizer "
-                        "traffic), fp32 optimizer state in pinned host DRAM",
+    what = ("config 5 per-GPU host-bytes-per-flop), bf16 params and fp32 optimizer state"
+            if params_host else "config 3 per-GPU flops and optimizer traffic), fp32 optimizer state")
+    return {"workload": f"GPT-1.3B x {batch} seq/GPU ({what} in pinned host DRAM",
             "ms_per_step_hbm": round(res["hbm"]["ms"], 2),
             "ms_per_step_offload": round(res["offload"]["ms"], 2),
             "tflops_offload": round(fl / (res["offload"]["ms"] / 1e3) / 1e12, 1),

@@ -166,7 +166,7 @@ class GPTZeroEngine:
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
-                 offload_slots: int = 12):
+                 offload_slots: int | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -186,6 +186,9 @@ class GPTZeroEngine:
         self.nvme_root = nvme_root
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
+        # staging ring depth (slots of offload_chunk fp32 p/m/v): 24 (4.6 GB at 16 M) with
+        # params in HBM; 12 with params on the host, whose own H2D the ring's prefetch
+        # would otherwise crowd out during the forward (measured: bench config legs)
         self.offload_slots = offload_slots
         self.overlap_opt = overlap_opt
         if act_ckpt not in (None, "device", "host"):
@@ -205,6 +208,8 @@ class GPTZeroEngine:
         self.gather_stream = torch.cuda.Stream(self.dev)
         self.h2d_stream = torch.cuda.Stream(self.dev)
         self.d2h_stream = torch.cuda.Stream(self.dev)
+        self.p16_stream = torch.cuda.Stream(self.dev)   # host params: bf16 write-back lane
+        self.p16_ready = {}                              # bucket -> its bf16 write-back landed
         self._alloc_work()
         self.launches = 0  # libzinf kernel launches issued by step()
         self.adam = kernels.DeviceAdamState(lr, betas, eps, device=self.dev)
@@ -409,7 +414,8 @@ class GPTZeroEngine:
                 self._obucket[b.key] = idx
             # NS <= chunks per step: the in-order D2H stream then guarantees that chunk
             # q's previous-step write-back landed before its next H2D (slot reuse events)
-            NS = max(3, min(self.offload_slots, len(self._ochunks)))
+            want = self.offload_slots or (12 if self.placement.params is TierKind.HOST else 24)
+            NS = max(3, min(want, len(self._ochunks)))
             self.stage = [[torch.empty(C, dtype=torch.float32, device=self.dev) for _ in range(3)]
                           for _ in range(NS)]
             self.stage16 = [torch.empty(C, dtype=self.half, device=self.dev) for _ in range(NS)]
@@ -501,7 +507,12 @@ class GPTZeroEngine:
             return
         dst = self.embed_slot if b.key == "embed" else self.slots[slot]
         with torch.cuda.stream(stream):
+            ev = self.p16_ready.pop(b.key, None)
+            if ev is not None:   # the previous step's updated bf16 shard is back in host DRAM
+                stream.wait_event(ev)
             t0 = self._tmark(stream)
+            if self.placement.params is TierKind.HOST:   # cg bytes over the host link
+                self.fetch_bytes = getattr(self, "fetch_bytes", 0) + b.shard * len(self.ranks) * 2
             if self.comm.is_local:
                 shards = [self._shard_view(self.p16, li, b) for li in range(len(self.ranks))]
                 kernels.allgather(shards, b.shard, dst, b.numel,
@@ -926,14 +937,21 @@ class GPTZeroEngine:
                 self.launches += 1
                 ev_c = torch.cuda.Event()
                 ev_c.record(opt)
+            if host_params:   # bf16 write-back on its own lane: the next fetch waits on it only
+                p16s = self.p16_stream
+                with torch.cuda.stream(p16s):
+                    p16s.wait_event(ev_c)
+                    p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
+                    ev_p = torch.cuda.Event()
+                    ev_p.record(p16s)
             with torch.cuda.stream(d2h):
                 d2h.wait_event(ev_c)
                 t0 = self._tmark(d2h)
                 for dst, src in zip((hp, hm, hv), (sp, sm, sv)):
                     dst[s:s + n].copy_(src, non_blocking=True)
-                if host_params:
-                    p16[s:s + n].copy_(self.stage16[k][:n], non_blocking=True)
                 self._tspan(b.op, "grad_offload", t0, self._tmark(d2h))
+                if host_params:
+                    d2h.wait_event(ev_p)      # slot k (stage16 too) is drained
                 ev_d = torch.cuda.Event()
                 ev_d.record(d2h)
             self.ev_d2h[k] = ev_d
@@ -941,16 +959,20 @@ class GPTZeroEngine:
         ev_free = torch.cuda.Event()
         ev_free.record(opt)
         self.gfree["embed" if b.key == "embed" else slot] = ev_free
+        if host_params:
+            ev = torch.cuda.Event()
+            ev.record(self.p16_stream)
+            self.p16_ready[b.key] = ev
 
     @property
     def defer_writeback(self) -> bool:
         """Optimizer-offload steps end when the last rs_adam is done, not when its
         D2H landed: the fp32 write-back drains during the next forward, which reads
-        only the bf16 params (updated in HBM). Not with params on the host (the next
-        gather reads the written-back bf16 shards), host checkpoints (d2h stream
-        shared), or under graph capture (every side stream must rejoin)."""
-        return (self.offload and self.placement.params is TierKind.DEVICE
-                and self.act_ckpt != "host"
+        only the bf16 params — updated in HBM, or, with params on the host, written
+        back on their own lane and awaited per bucket by the next fetch (p16_ready).
+        Not with host checkpoints (d2h stream shared) or under graph capture (every
+        side stream must rejoin)."""
+        return (self.offload and self.act_ckpt != "host"
                 and not torch.cuda.is_current_stream_capturing())
 
     def flush(self) -> None:
@@ -959,6 +981,7 @@ class GPTZeroEngine:
         cur = torch.cuda.current_stream()
         cur.wait_stream(self.d2h_stream)
         cur.wait_stream(self.h2d_stream)
+        cur.wait_stream(self.p16_stream)
 
     # ------------------------------------------------- activation checkpoints (PAPER §5.1.2)
     def _ckpt_save(self, li: int, i: int, x_in: torch.Tensor):
@@ -1045,6 +1068,8 @@ class GPTZeroEngine:
         # end) and must not leak into a graph capture
         self.gfree.clear()
         self.events.clear()
+        if torch.cuda.is_current_stream_capturing():
+            self.p16_ready.clear()    # host-side synchronized before capture; no external waits
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
         self._nvme_wait = {}
@@ -1155,6 +1180,8 @@ class GPTZeroEngine:
         if (self.offload and not self.defer_writeback) or self.nvme or self.act_ckpt == "host":
             cur.wait_stream(self.d2h_stream)  # ... and host transfers landed
             cur.wait_stream(self.h2d_stream)
+            cur.wait_stream(self.p16_stream)
+            self.p16_ready.clear()
         if gs is not cur:
             cur.wait_stream(gs)       # join the gather stream (required for graph capture)
         total = losses[0].float()
