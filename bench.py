@@ -387,7 +387,13 @@ def run_ours(args):
     if world == 1 and not args.no_offload:
         del eng
         torch.cuda.empty_cache()
-        offload = offload_leg(cfg, args)
+        try:
+            offload = offload_leg(cfg, args)
+        except Exception as e:  # noqa: BLE001 — report, never lose the main line
+            import traceback
+            traceback.print_exc()
+            offload = {"error": repr(e)[:300]}
+            torch.cuda.synchronize()
 
     store = None
     if world == 1 and not args.no_offload:
@@ -605,11 +611,24 @@ def offload_leg(cfg, args) -> dict:
                                   "rel_error": round(sim["rel_error"], 4)}}
     del eng
     torch.cuda.empty_cache()
-    out["config3_equiv"] = offload_equiv_leg(args)
-    out["config5_equiv"] = offload_equiv_leg(args, batch=32, params_host=True)
+    out["config3_equiv"] = _safe(offload_equiv_leg, args)
+    out["config5_equiv"] = _safe(offload_equiv_leg, args, batch=32, params_host=True)
     if not args.no_nvme:
-        out["nvme_optimizer"] = nvme_leg(cfg, args, bs, steps)
+        out["nvme_optimizer"] = _safe(nvme_leg, cfg, args, bs, steps)
     return out
+
+
+def _safe(fn, *a, **kw) -> dict:
+    """Run one bench sub-leg; a failure is reported in its slot, never loses the line."""
+    import torch
+    try:
+        return fn(*a, **kw)
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        traceback.print_exc()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return {"error": repr(e)[:300]}
 
 
 def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:

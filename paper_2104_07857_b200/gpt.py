@@ -200,6 +200,7 @@ class GPTZeroEngine:
         self.t = 0
         self.trace = trace
         self._spans, self._t0 = [], None
+        self._phase = "forward"
         self._build_buckets()
         self._alloc_state()
         self._init_state()
@@ -880,6 +881,14 @@ class GPTZeroEngine:
                 ev.record(os_)
                 self.gfree[key] = ev
 
+    def _ostate_prefetch(self) -> None:
+        """Issue the H2D of the backward's first NS-1 optimizer-state chunks (cg lane)."""
+        ph = self._phase
+        self._phase = "backward"
+        for q in range(len(self.stage) - 1):
+            self._ostate_h2d(q)
+        self._phase = ph
+
     def _ostate_h2d(self, q: int) -> None:
         """Issue the H2D of this step's optimizer-state chunk q into its staging slot
         (the cg lane), behind the D2H that last drained the slot."""
@@ -1074,10 +1083,9 @@ class GPTZeroEngine:
         self._ckpt_loaded.clear()
         self._nvme_wait = {}
         self._t0 = self._tmark(cur)
-        if self.offload:      # cg prefetch of the backward's first chunks, during the forward
-            self._phase = "backward"
-            for q in range(len(self.stage) - 1):
-                self._ostate_h2d(q)
+        host_params = self.placement.params is TierKind.HOST
+        if self.offload and not host_params:   # state prefetch for the backward, during the forward
+            self._ostate_prefetch()
         self._phase = "forward"
         gs.wait_stream(cur)
         blocks = self.buckets[1:-1]
@@ -1101,6 +1109,10 @@ class GPTZeroEngine:
                 gs.wait_stream(cur)
                 self._phase = "backward"     # the head is the first backward op
                 self._fetch(FB, (i + 1) % 2, gs)
+                if self.offload and host_params:
+                    # with params on the host the forward's H2D lane carries their fetches;
+                    # the state prefetch starts behind the last of them
+                    self._ostate_prefetch()
                 self._phase = "forward"
             P = self._params(b, full)
             c0 = self._tmark(cur)
@@ -1180,8 +1192,9 @@ class GPTZeroEngine:
         if (self.offload and not self.defer_writeback) or self.nvme or self.act_ckpt == "host":
             cur.wait_stream(self.d2h_stream)  # ... and host transfers landed
             cur.wait_stream(self.h2d_stream)
-            cur.wait_stream(self.p16_stream)
-            self.p16_ready.clear()
+            if self.offload and self.placement.params is TierKind.HOST:
+                cur.wait_stream(self.p16_stream)
+                self.p16_ready.clear()
         if gs is not cur:
             cur.wait_stream(gs)       # join the gather stream (required for graph capture)
         total = losses[0].float()
