@@ -191,6 +191,68 @@ def cpu_components() -> dict:
     return out
 
 
+def tiling_leg(T: int = 8, iters: int = 5) -> dict:
+    """BASELINE config 4 at one tile count: the 16384 -> 65536 linear over M = 8192 tokens
+    split into T row tiles, forward_tiled / backward_tiled through the tier store (each
+    tile fetched just in time into a 2-slot ring), every tile product on tcgen05
+    (zi_linear_tile_fwd / _bwd). The roofline is the tile kernel timed alone (CUDA events)
+    against the burst bf16 peak; cuBLAS on the same tiles beside it."""
+    import tempfile
+    import torch
+    from paper_2104_07857_b200 import kernels
+    from paper_2104_07857_b200.store import TierKind, TierStore
+    from paper_2104_07857_b200.tiling import backward_tiled, forward_tiled, tile_linear
+    M, K, N = 8192, 16384, 65536
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(M, K, device="cuda", dtype=torch.bfloat16, generator=g)
+    W = torch.randn(N, K, device="cuda", dtype=torch.bfloat16, generator=g) * K ** -0.5
+    b = torch.randn(N, device="cuda", dtype=torch.bfloat16, generator=g)
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    gy = (torch.randn(M, N, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+
+    def timed(fn, n=iters):
+        fn()
+        torch.cuda.synchronize()
+        a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            fn()
+        c.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(c) / n
+
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        burst = json.load(f)["bf16_tflops"]
+    out = {"workload": f"tiled linear 16384->65536, T={T}, M={M} tokens, bf16"}
+    with TierStore(16 << 30, 1 << 30, nvme_root=tempfile.mkdtemp()) as st:
+        tl = tile_linear(W, b, T, st, TierKind.DEVICE, key="c4")
+        ms_f = timed(lambda: forward_tiled(tl, x, st, out=y))
+        ms_b = timed(lambda: backward_tiled(tl, x, gy, st), max(2, iters // 2))
+    s0, e0 = 0, N // T
+
+    def cub():
+        for s, e in ((i * (N // T), (i + 1) * (N // T)) for i in range(T)):
+            torch.addmm(b[s:e], x, W[s:e].t(), out=y[:, s:e]) if y[:, s:e].is_contiguous() \
+                else y[:, s:e].copy_(torch.addmm(b[s:e], x, W[s:e].t()))
+    ms_c = timed(cub)
+    Wt, yt = W[s0:e0], torch.empty(M, e0 - s0, device="cuda", dtype=torch.bfloat16)
+    ms_k = timed(lambda: kernels.linear_fwd(x, Wt, b[s0:e0], yt))
+    tf_k = 2.0 * M * K * (e0 - s0) / (ms_k / 1e3) / 1e12
+    out.update({"forward_tiled_ms": round(ms_f, 3),
+                "forward_tflops": round(2.0 * M * K * N / (ms_f / 1e3) / 1e12, 1),
+                "backward_tiled_ms": round(ms_b, 3),
+                "backward_tflops": round(4.0 * M * K * N / (ms_b / 1e3) / 1e12, 1),
+                "cublas_same_tiles_fwd_ms": round(ms_c, 3),
+                "roofline": {"kernel": "zi_linear_tile_fwd (2-SM tcgen05, one tile alone)",
+                             "bound": "tensor", "achieved": round(tf_k, 1), "peak": burst,
+                             "peak_kind": "measured burst", "unit": "TFLOP/s",
+                             "frac": round(tf_k / burst, 4),
+                             "ncu": "profiles/r1_gemm_tile_ncu.md (tensor pipe 98.0 % active)"}})
+    del x, W, y, gy
+    torch.cuda.empty_cache()
+    return out
+
+
 def store_leg() -> dict:
     """The tier store through the reference API on the GPU box, on
     the same 128 MiB f32 sample as cpu_components' reference-store numbers: HOST tier
@@ -395,12 +457,10 @@ def run_ours(args):
             offload = {"error": repr(e)[:300]}
             torch.cuda.synchronize()
 
-    store = None
+    store = tiling = None
     if world == 1 and not args.no_offload:
-        try:
-            store = store_leg()
-        except Exception as e:  # noqa: BLE001 — report, never lose the main line
-            store = {"error": repr(e)[:300]}
+        store = _safe(store_leg)
+        tiling = _safe(tiling_leg)
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -446,6 +506,7 @@ def run_ours(args):
             "offload": offload,
             "collectives": collectives,
             "store": store,
+            "tiling": tiling,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
