@@ -226,9 +226,9 @@ class GPTZeroEngine:
         # pass, timed once per process on this engine's shapes (gemm_select.py).
         # "auto" (default, or ZI_GEMM_SELECT) tunes; "zi" / "cublas" force every site.
         # One process per GPU (DistComm) defaults to cuBLAS: with two ranks time-sharing
-        # one GPU (the only multi-process setup testable here) the tcgen05 GEMMs hit
-        # sporadic launch failures that cuBLAS does not, and the tuned
-        # choice is worth ~0.2 ms per step at N=1.
+        # one GPU (the only multi-process setup testable here) a rank holding a
+        # persistent tcgen05 GEMM can starve its peer past the zi_barrier watchdog
+        # (DESIGN.md §8), and the tuned choice is worth ~0.2 ms per step at N=1.
         default = "auto" if self.comm.is_local else "cublas"
         mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", default)
         if mode not in ("auto", "zi", "cublas"):
