@@ -17,10 +17,7 @@ build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/bulk.cuh include/zinf.h
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
-oracle:
-	$(MAKE) -C oracle
-
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean oracle
+.PHONY: all clean
