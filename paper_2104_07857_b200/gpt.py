@@ -1188,7 +1188,9 @@ class GPTZeroEngine:
         self._reduce_update(E, 0, consts)
         if self.nvme:
             self.streamer.drain()         # every bucket's states are back on NVMe
-        cur.wait_stream(self.opt_stream)  # the step ends when the last bucket is updated
+        if self.overlap_opt or self.offload:   # (an unused side stream must not be joined
+            cur.wait_stream(self.opt_stream)  # under capture) the step ends when the last
+                                              # bucket is updated
         if (self.offload and not self.defer_writeback) or self.nvme or self.act_ckpt == "host":
             cur.wait_stream(self.d2h_stream)  # ... and host transfers landed
             cur.wait_stream(self.h2d_stream)
