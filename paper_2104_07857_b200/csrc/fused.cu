@@ -392,16 +392,16 @@ gelu_fwd_kernel(const uint16_t* __restrict__ u, uint16_t* __restrict__ y, size_t
 }
 
 // Column reductions (bias grads, GELU-bwd + bias grad) over rows streamed
-// through a CRW_STAGES-deep bulk-copy ring. CTA (column block, row chunk): C
+// through an NSTG-deep bulk-copy ring. CTA (column block, row chunk): C
 // columns (8 per thread, C/8 threads), rows [r0, r1) in stages of R rows; one
 // bulk copy per row and input. Each thread accumulates its 8 columns over the
 // chunk in row order and writes one partial row part[chunk][N]; the fold kernel
 // then sums the chunks in order: deterministic for a fixed grid.
 //   MODE 0: out = sum_rows a                               (bias grad)
 //   MODE 1: du = gelu_tanh'(u) * a -> d; out = sum_rows du (GELU bwd + fc1 bias grad)
-constexpr int CRW_STAGES = 4, CRW_MAX_COLS = 4096;
+constexpr int CRW_MAX_COLS = 4096;
 
-template <int MODE>
+template <int MODE, int NSTG>
 __global__ void __launch_bounds__(CRW_MAX_COLS / 8)
 colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
               uint16_t* __restrict__ d, float* __restrict__ part, int T, int N, int C, int R,
@@ -409,20 +409,20 @@ colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
   constexpr int NIN = MODE == 1 ? 2 : 1;
   extern __shared__ __align__(128) uint16_t ring[];   // [stage][input][R][C]
   const int SE = R * C;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)CRW_STAGES * NIN * SE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)NSTG * NIN * SE);
   const int c0 = blockIdx.x * C, W = min(C, N - c0);
   const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
   const int nst = r1 > r0 ? (r1 - r0 + R - 1) / R : 0;
   const int t = threadIdx.x;
   const bool colok = t * 8 < W;
   if (t == 0) {
-    for (int s = 0; s < CRW_STAGES; ++s) bulk::mbar_init(&full[s], 1);
+    for (int s = 0; s < NSTG; ++s) bulk::mbar_init(&full[s], 1);
     bulk::fence_init();
   }
   __syncthreads();
   auto issue = [&](int i) {                          // thread 0: rows of stage i
     if (i >= nst) return;
-    const int s = i % CRW_STAGES, rb = r0 + i * R, rows = min(R, r1 - rb);
+    const int s = i % NSTG, rb = r0 + i * R, rows = min(R, r1 - rb);
     const uint32_t bytes = (uint32_t)W * 2;
     bulk::mbar_expect_tx(&full[s], NIN * rows * bytes);
     uint16_t* st = ring + (size_t)s * NIN * SE;
@@ -433,13 +433,13 @@ colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
     }
   };
   if (t == 0)
-    for (int i = 0; i < CRW_STAGES; ++i) issue(i);
+    for (int i = 0; i < NSTG; ++i) issue(i);
   float acc[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.f;
   for (int i = 0; i < nst; ++i) {
-    const int s = i % CRW_STAGES, rb = r0 + i * R, rows = min(R, r1 - rb);
-    bulk::mbar_wait(&full[s], (i / CRW_STAGES) & 1);
+    const int s = i % NSTG, rb = r0 + i * R, rows = min(R, r1 - rb);
+    bulk::mbar_wait(&full[s], (i / NSTG) & 1);
     if (colok) {
       const uint16_t* st = ring + (size_t)s * NIN * SE + t * 8;
       for (int j = 0; j < rows; ++j) {
@@ -458,7 +458,7 @@ colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
       }
     }
     __syncthreads();                                 // stage s read by everyone: refill
-    if (t == 0) issue(i + CRW_STAGES);
+    if (t == 0) issue(i + NSTG);
   }
   if (colok) {
 #pragma unroll
@@ -651,11 +651,13 @@ static int launch_colred(int mode, const void* a, const void* u, void* d, void* 
   const int nin = mode == 1 ? 2 : 1;
   int R = 16384 / (C * 2);
   R = R < 1 ? 1 : (R > 8 ? 8 : R);
-  const size_t smem = (size_t)CRW_STAGES * nin * R * C * 2 + 64;
+  // ring depth: the bulk copies in flight per SM set the bandwidth (~3 us of HBM latency
+  // under load x 44 GB/s per SM needs >= 130 KB in flight), so fill ~190 KB per SM
+  const size_t stage_bytes = (size_t)nin * R * C * 2;
   int per_sm = 2;   // enough bytes in flight per SM; more CTAs only add partial rows
-  const int by_smem = (int)(200000 / smem);
-  if (per_sm > by_smem) per_sm = by_smem;
-  if (per_sm < 1) per_sm = 1;
+  if (4 * stage_bytes * per_sm > 200000) per_sm = 1;
+  const int nstg = 8 * stage_bytes * per_sm <= 197000 ? 8 : (6 * stage_bytes * per_sm <= 197000 ? 6 : 4);
+  const size_t smem = (size_t)nstg * stage_bytes + 64;
   int chunks = (sm_count() * per_sm + cblocks - 1) / cblocks;
   const int max_chunks = (T + R - 1) / R;
   if (chunks > max_chunks) chunks = max_chunks;
@@ -665,19 +667,25 @@ static int launch_colred(int mode, const void* a, const void* u, void* d, void* 
   ZI_CHECK_ARG(work_elems >= 1024 + (size_t)chunks * N, "%s: work needs %zu floats", name,
                1024 + (size_t)chunks * N);
   float* part = work + 1024;
-  static bool attr[2] = {false, false};
-  if (!attr[mode]) {
-    ZI_CUDA(cudaFuncSetAttribute(mode ? colrow_kernel<1> : colrow_kernel<0>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
-            "cudaFuncSetAttribute(colrow)");
-    attr[mode] = true;
+  static bool attr = false;
+  if (!attr) {
+    for (auto k : {colrow_kernel<0, 4>, colrow_kernel<0, 6>, colrow_kernel<0, 8>,
+                   colrow_kernel<1, 4>, colrow_kernel<1, 6>, colrow_kernel<1, 8>})
+      ZI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024),
+              "cudaFuncSetAttribute(colrow)");
+    attr = true;
   }
   dim3 grid(cblocks, chunks);
   const uint16_t* A = static_cast<const uint16_t*>(a);
   const uint16_t* U = static_cast<const uint16_t*>(u);
   uint16_t* D = static_cast<uint16_t*>(d);
-  if (mode == 0) colrow_kernel<0><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per);
-  else colrow_kernel<1><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per);
+#define ZI_COLROW(MODE, NS) colrow_kernel<MODE, NS><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per)
+  if (mode == 0) {
+    if (nstg == 8) ZI_COLROW(0, 8); else if (nstg == 6) ZI_COLROW(0, 6); else ZI_COLROW(0, 4);
+  } else {
+    if (nstg == 8) ZI_COLROW(1, 8); else if (nstg == 6) ZI_COLROW(1, 6); else ZI_COLROW(1, 4);
+  }
+#undef ZI_COLROW
   int st = zi::launch_status(name);
   if (st) return st;
   ln_fold_kernel<<<dim3((N + 31) / 32, 1), 32 * FOLD_SUB, 0, s>>>(part, chunks, N, out, nullptr,
