@@ -162,7 +162,7 @@ class GPTZeroEngine:
                  compute_dtype: torch.dtype | None = None,
                  placement: Placement | None = None,
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
-                 prefetch: bool = True, copy_engine_gather: bool = False,
+                 prefetch: bool = True, copy_engine_gather: bool | None = None,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
@@ -195,6 +195,11 @@ class GPTZeroEngine:
             raise ValueError("act_ckpt must be None, 'device' or 'host'")
         self.act_ckpt = act_ckpt
         self.prefetch = prefetch
+        # One process per GPU: peer shards are pulled by the copy engines, so the
+        # gathers use no SMs and overlap the (all-SM) GEMMs of the op before them
+        # (SURVEY §7 hard parts); in-process ranks gather with the SM kernel.
+        if copy_engine_gather is None:
+            copy_engine_gather = not self.comm.is_local and self.N > 1
         self.copy_engine_gather = copy_engine_gather
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.t = 0
