@@ -676,6 +676,7 @@ def offload_leg(cfg, args) -> dict:
     out["config5_equiv"] = _safe(offload_equiv_leg, args, batch=32, params_host=True)
     if not args.no_nvme:
         out["nvme_optimizer"] = _safe(nvme_leg, cfg, args, bs, steps)
+        out["nvme_optimizer_direct"] = _safe(nvme_leg, cfg, args, bs, 2, direct=True)
     return out
 
 
@@ -768,7 +769,35 @@ def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
             "loss_hbm": res["hbm"]["loss"], "loss_offload": res["offload"]["loss"]}
 
 
-def nvme_leg(cfg, args, bs, steps) -> dict:
+def disk_peak(root: str, nbytes: int = 2 << 30) -> dict:
+    """O_DIRECT write then read of one file through the native engine (8 threads,
+    8 MiB pieces): the disk's own sequential bandwidth, the NVMe legs' denominator."""
+    import os as _os
+    from paper_2104_07857_b200.aio import AioEngine
+    from paper_2104_07857_b200.store import _PinnedBuffer
+    buf = _PinnedBuffer(256 << 20)
+    path = _os.path.join(root, "zinf_disk_peak.bin")
+    eng = AioEngine(8)
+    try:
+        fds = eng.open(path, write=True, create=True)
+        res = {}
+        for name, write in (("write_gbs", True), ("read_gbs", False)):
+            t = time.perf_counter()
+            ids = [eng.submit(fds, write, buf.ptr, o, o + (256 << 20))
+                   for o in range(0, nbytes, 256 << 20)]
+            for i in ids:
+                eng.wait(i)
+            res[name] = round(nbytes / (time.perf_counter() - t) / 1e9, 2)
+        AioEngine.close_file(fds)
+    finally:
+        eng.close()
+        buf.free()
+        if _os.path.exists(path):
+            _os.unlink(path)
+    return res
+
+
+def nvme_leg(cfg, args, bs, steps, direct: bool = False) -> dict:
     """The 1.3B step with fp32 master/m/v as .shard files in the NVMe tier (PAPER §6.2):
     per bucket the streamer runs nc-read -> H2D -> zi_rs_adam_dc -> D2H -> nc-write in
     chunks. Files go through the OS page cache (the shard header is 20 B, so payloads
@@ -782,7 +811,8 @@ def nvme_leg(cfg, args, bs, steps) -> dict:
     root = tempfile.mkdtemp(prefix="zinf_nvme_", dir=args.nvme_dir)
     try:
         eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, nvme_root=root,
-                               placement=eg.Placement(TierKind.DEVICE, TierKind.NVME))
+                               placement=eg.Placement(TierKind.DEVICE, TierKind.NVME),
+                               nvme_direct=direct)
         eng.step([bs[0]])
         torch.cuda.synchronize()
         b0 = eng.streamer.bytes
@@ -792,13 +822,21 @@ def nvme_leg(cfg, args, bs, steps) -> dict:
         loss.item()
         ms = (time.perf_counter() - t) * 1e3 / steps
         moved = (eng.streamer.bytes - b0) / steps
+        how = ("native engine: O_DIRECT whole blocks, C worker threads" if direct else
+               "Python store workers through the OS page cache")
         out = {"workload": "GPT-1.3B ZeRO-3 step, fp32 optimizer state (15.8 GB) in NVMe-tier "
-                           ".shard files", "nvme_root": args.nvme_dir or tempfile.gettempdir(),
+                           f".shard files ({how})",
+               "nvme_root": args.nvme_dir or tempfile.gettempdir(),
                "ms_per_step": round(ms, 1),
                "tflops": round(eg.model_flops_per_step(cfg) / (ms / 1e3) / 1e12, 2),
                "nvme_bytes_per_step": int(moved),
                "nvme_gbs": round(moved / (ms / 1e3) / 1e9, 2),
                "timing": "host wall clock around step() (the step ends with a host drain)"}
+        if direct:
+            peak = disk_peak(root)
+            out["disk_peak"] = peak
+            both = 1.0 / (0.5 / peak["read_gbs"] + 0.5 / peak["write_gbs"])
+            out["frac_of_disk_serial_rw"] = round(out["nvme_gbs"] / both, 3)
         eng.close()
         del eng
     finally:

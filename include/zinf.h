@@ -10,7 +10,7 @@
  *     thread-local message. Status codes map to the reference exception tree
  *     (store.py:54-71): ZI_ECAPACITY -> CapacityExceeded, ZI_ENOTFOUND ->
  *     KeyNotFound, ZI_EINVAL -> ValueError, ZI_EEXHAUSTED -> PoolExhausted,
- *     ZI_ECUDA/ZI_ENCCL -> StoreError.
+ *     ZI_EIO -> OSError, ZI_ECUDA/ZI_ENCCL -> StoreError.
  *   - All device work is asynchronous on the caller's `stream`
  *     (a cudaStream_t passed as void*). Callers own every buffer; the
  *     library owns nothing but its error string.
@@ -35,7 +35,8 @@ typedef enum {
   ZI_ENOTFOUND = 3,
   ZI_ECUDA = 4,
   ZI_ENCCL = 5,
-  ZI_EEXHAUSTED = 6
+  ZI_EEXHAUSTED = 6,
+  ZI_EIO = 7
 } zi_status;
 
 enum { ZI_HALF_FP16 = 0, ZI_HALF_BF16 = 1 };
@@ -192,6 +193,22 @@ int zi_pool_stats(void* pool, int* free_count, uint64_t* waits);
  * D2H = grad / optimizer-state offload. Pinned host memory for full speed. */
 int zi_h2d_async(void* dst, const void* src, size_t bytes, void* stream, void* event);
 int zi_d2h_async(void* dst, const void* src, size_t bytes, void* stream, void* event);
+
+/* ---- native file I/O for the NVMe tier (store.py:442-560, PAPER §6.2) ---------
+ * A worker pool moving byte ranges of a file between disk and pinned host memory.
+ * zi_aio_open opens the file twice: fds[0] O_DIRECT, fds[1] buffered. zi_aio_submit
+ * queues file bytes [b0, b1) <-> buf + (b0 % 4096) ... (buf 4 KiB-aligned): whole 4 KiB
+ * blocks go O_DIRECT in <= 8 MiB pieces across the workers, partial edge blocks through
+ * the buffered descriptor; zi_aio_wait blocks until that request finished (ZI_EIO on an
+ * I/O error or a short read). */
+int zi_aio_create(int threads, void** eng);
+int zi_aio_destroy(void* eng);
+int zi_aio_open(const char* path, int write, int create, int* fds);
+int zi_aio_close(const int* fds);
+int zi_aio_truncate(const int* fds, size_t size);
+int zi_aio_submit(void* eng, const int* fds, int write, void* buf, size_t b0, size_t b1,
+                  uint64_t* id);
+int zi_aio_wait(void* eng, uint64_t id);
 
 /* ---- CUDA IPC (peer buffers for the P2P collectives) ---------------------
  * Buffers that peers map are plain cudaMalloc allocations (zi_device_alloc)

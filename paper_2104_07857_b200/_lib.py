@@ -14,7 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libzinf.so")
 
-ZI_OK, ZI_EINVAL, ZI_ECAPACITY, ZI_ENOTFOUND, ZI_ECUDA, ZI_ENCCL, ZI_EEXHAUSTED = range(7)
+ZI_OK, ZI_EINVAL, ZI_ECAPACITY, ZI_ENOTFOUND, ZI_ECUDA, ZI_ENCCL, ZI_EEXHAUSTED, ZI_EIO = range(8)
 HALF_FP16, HALF_BF16 = 0, 1
 DT_F32, DT_F16, DT_F64, DT_BF16 = 0, 1, 2, 3
 
@@ -86,6 +86,14 @@ SIGNATURES = {
                            c_int, c_int, c_void_p],
     "zi_linear_tile_bwd": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
                            c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p],
+    "zi_aio_create": [c_int, ctypes.POINTER(c_void_p)],
+    "zi_aio_destroy": [c_void_p],
+    "zi_aio_open": [ctypes.c_char_p, c_int, c_int, ctypes.POINTER(c_int)],
+    "zi_aio_close": [ctypes.POINTER(c_int)],
+    "zi_aio_truncate": [ctypes.POINTER(c_int), c_size_t],
+    "zi_aio_submit": [c_void_p, ctypes.POINTER(c_int), c_int, c_void_p, c_size_t, c_size_t,
+                      ctypes.POINTER(c_uint64)],
+    "zi_aio_wait": [c_void_p, c_uint64],
     "zi_device_alloc": [c_size_t, ctypes.POINTER(c_void_p)],
     "zi_device_free": [c_void_p],
     "zi_ipc_get_handle": [c_void_p, ctypes.c_char_p],
@@ -139,6 +147,8 @@ def check(status: int, what: str) -> None:
     from .store import CapacityExceeded, KeyNotFound, PoolExhausted  # late: no cycle at load
     if status == ZI_EEXHAUSTED:
         raise PoolExhausted(msg)
+    if status == ZI_EIO:
+        raise OSError(msg)
     if status == ZI_ECAPACITY:
         raise CapacityExceeded(msg)
     if status == ZI_ENOTFOUND:

@@ -67,7 +67,8 @@ int zi_pool_create(size_t buffer_bytes, int buffer_count, int blocking, int pinn
         return st;
       }
     } else {
-      p->bufs[i] = std::malloc(buffer_bytes);
+      // page-aligned (O_DIRECT file I/O into pool buffers needs 4 KiB alignment)
+      p->bufs[i] = std::aligned_alloc(4096, (buffer_bytes + 4095) / 4096 * 4096);
       if (!p->bufs[i]) {
         zi::set_error("zi_pool_create: malloc of %zu bytes failed", buffer_bytes);
         zi::free_buffers(p);

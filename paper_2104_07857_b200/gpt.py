@@ -166,7 +166,7 @@ class GPTZeroEngine:
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
-                 offload_slots: int | None = None):
+                 offload_slots: int | None = None, nvme_direct: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -184,6 +184,7 @@ class GPTZeroEngine:
         if self.nvme and (self.placement.params is not TierKind.DEVICE or not self.comm.is_local):
             raise NotImplementedError("NVMe optimizer states: params in HBM, simulated ranks")
         self.nvme_root = nvme_root
+        self.nvme_direct = nvme_direct   # NVMe states through the native O_DIRECT engine
         self.lr, self.betas, self.eps = lr, betas, eps
         self.offload_chunk = offload_chunk
         # staging ring depth (slots of offload_chunk fp32 p/m/v): 24 (4.6 GB at 16 M) with
@@ -308,7 +309,7 @@ class GPTZeroEngine:
             from .store import TierStore
             root = self.nvme_root or tempfile.mkdtemp(prefix="zinf-nvme-")
             self.store = TierStore(0, 0, nvme_root=root, workers=8)
-            self.streamer = NvmeOptimizerStreamer(self, self.store)
+            self.streamer = NvmeOptimizerStreamer(self, self.store, direct=self.nvme_direct)
             self.p32 = self.m = self.v = None
             return
         self.p32 = mk(torch.float32, ho)

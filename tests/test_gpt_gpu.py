@@ -210,14 +210,16 @@ def test_offload_matches_hbm(params_host, slots):
     assert b.offload_bytes > 0
 
 
-def test_nvme_optimizer_states_match_hbm(tmp_path):
+@pytest.mark.parametrize("direct", [False, True])
+def test_nvme_optimizer_states_match_hbm(tmp_path, direct):
     """Optimizer states in NVMe .shard files streamed nc -> cg -> RS+Adam -> D2H -> nc in
-    small chunks: the same training result as keeping them in HBM."""
+    small chunks (through the page cache, or the native O_DIRECT engine): the same
+    training result as keeping them in HBM."""
     from paper_2104_07857_b200.gpt import Placement
     from paper_2104_07857_b200.store import SHARD_MAGIC, TierKind
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3)
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, nvme_root=str(tmp_path),
-                         placement=Placement(TierKind.DEVICE, TierKind.NVME))
+                         placement=Placement(TierKind.DEVICE, TierKind.NVME), nvme_direct=direct)
     b.streamer.chunk = 30_000   # several chunks per bucket
     for step in range(3):
         bs = batches_for(SMALL, 2, step)
