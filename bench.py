@@ -676,7 +676,7 @@ def offload_leg(cfg, args) -> dict:
     out["config5_equiv"] = _safe(offload_equiv_leg, args, batch=32, params_host=True)
     if not args.no_nvme:
         out["nvme_optimizer"] = _safe(nvme_leg, cfg, args, bs, steps)
-        out["nvme_optimizer_direct"] = _safe(nvme_leg, cfg, args, bs, 2, direct=True)
+        out["nvme_optimizer_direct"] = _safe(nvme_leg, cfg, args, bs, 1, direct=True)
     return out
 
 
