@@ -1259,6 +1259,8 @@ class GPTZeroEngine:
     def gathered(self, key: str) -> torch.Tensor:
         """Full half bucket (all ranks local) — for tests."""
         b = self.by_key[key]
+        if self.offload:
+            self.flush()        # host params: the deferred bf16 write-back has landed
         out = torch.empty(b.shard * self.N, dtype=self.half, device=self.dev)
         shards = [self._shard_view(self.p16, li, b).to(self.dev) for li in range(len(self.ranks))]
         kernels.allgather(shards, b.shard, out, b.numel)
