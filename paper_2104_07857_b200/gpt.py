@@ -1230,6 +1230,8 @@ class GPTZeroEngine:
             # warm cuBLAS / cuDNN plans and the allocator with two eager steps on a
             # snapshot of the model state, then restore it: every call of
             # step_graphed is exactly one training step
+            self.flush()                 # no deferred write-back in flight under the snapshot
+            torch.cuda.synchronize()
             state = [self.p16, self.p32, self.m, self.v, self.adam.step, self.adam.consts]
             snap = [s.clone() for s in state]
             for _ in range(2):
