@@ -1073,8 +1073,12 @@ class GPTZeroEngine:
             self.comm.device_barrier()  # peers' previous-step Adam writes are done
             self.launches += 1
         if self.offload:
-            if not self.defer_writeback:
-                self.h2d_stream.wait_stream(self.d2h_stream)  # last step's host writes landed
+            # the cg lane follows this step's start (under capture: joins the graph)
+            self.h2d_stream.wait_stream(cur)
+            if not self.defer_writeback and not torch.cuda.is_current_stream_capturing():
+                # last step's host writes landed (a graph replay follows the previous
+                # replay, which joined every lane, in stream order)
+                self.h2d_stream.wait_stream(self.d2h_stream)
             self._obase += len(self._ochunks)
             self._oh2d = {}
         self._spans = []
@@ -1084,7 +1088,10 @@ class GPTZeroEngine:
         self.gfree.clear()
         self.events.clear()
         if torch.cuda.is_current_stream_capturing():
-            self.p16_ready.clear()    # host-side synchronized before capture; no external waits
+            # host-side synchronized before capture: drop events recorded outside it
+            self.p16_ready.clear()
+            if self.offload:
+                self.ev_d2h = [None] * len(self.ev_d2h)
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
         self._nvme_wait = {}
