@@ -128,6 +128,16 @@ int zi_cast_f32_to_half(const float* src, void* dst, size_t n, int half_kind,
 int zi_cast_half_to_f32(const void* src, float* dst, size_t n, int half_kind,
                         void* stream);
 
+/* C[m,n] = sum_{k=0..K-1} A[m,k] B[k,n] (+ bias[n]) in fp32 or fp64 (dtype ZI_DT_F32 /
+ * ZI_DT_F64), one sequential fma chain per output: a fixed summation order, independent
+ * of library heuristics. Strides in elements (A: sam, sak; B: sbk, sbn; C: scm, scn), so
+ * transposed views cost nothing. bias may be NULL. The SPEC harness's linears
+ * ("fixed order everywhere") run on it so that AC-9's
+ * digests are bit-identical across world sizes and placements. */
+int zi_matmul_fixed(const void* A, int64_t sam, int64_t sak, const void* B, int64_t sbk,
+                    int64_t sbn, const void* bias, void* C, int64_t scm, int64_t scn, int M,
+                    int N, int K, int dtype, void* stream);
+
 /* ---- fused block kernels of the GPT step (bf16 activations, fp32 math) ----
  * Row-wise ops take T rows of H (H in {128, 256, 512, 1024, 2048}); column
  * reductions are deterministic (fixed-order fold of per-CTA partials in the

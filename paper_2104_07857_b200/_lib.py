@@ -54,6 +54,9 @@ SIGNATURES = {
     "zi_fill": [c_void_p, c_void_p, c_size_t, c_float, c_int, c_void_p],
     "zi_cast_f32_to_half": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],
     "zi_cast_half_to_f32": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],
+    "zi_matmul_fixed": [c_void_p, ctypes.c_int64, ctypes.c_int64, c_void_p, ctypes.c_int64,
+                        ctypes.c_int64, c_void_p, c_void_p, ctypes.c_int64, ctypes.c_int64, c_int,
+                        c_int, c_int, c_int, c_void_p],
     "zi_ln_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                   c_int, c_int, c_float, c_void_p],
     "zi_ln_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

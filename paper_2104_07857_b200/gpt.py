@@ -166,7 +166,8 @@ class GPTZeroEngine:
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
                  overlap_opt: bool = True, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
-                 offload_slots: int | None = None, nvme_direct: bool = False):
+                 offload_slots: int | None = None, nvme_direct: bool = False,
+                 fwd_state_prefetch_every: int = 2):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -191,6 +192,9 @@ class GPTZeroEngine:
         # params in HBM; 12 with params on the host, whose own H2D the ring's prefetch
         # would otherwise crowd out during the forward (measured: bench config legs)
         self.offload_slots = offload_slots
+        # params on the host: one optimizer-state chunk H2D per this many forward
+        # blocks, queued behind their parameter fetches (0: all after the forward)
+        self.fwd_state_prefetch_every = fwd_state_prefetch_every
         self.overlap_opt = overlap_opt
         if act_ckpt not in (None, "device", "host"):
             raise ValueError("act_ckpt must be None, 'device' or 'host'")
@@ -895,14 +899,14 @@ class GPTZeroEngine:
             self._ostate_h2d(q)
         self._phase = ph
 
-    def _ostate_h2d(self, q: int) -> None:
+    def _ostate_h2d(self, q: int, stream=None) -> None:
         """Issue the H2D of this step's optimizer-state chunk q into its staging slot
-        (the cg lane), behind the D2H that last drained the slot."""
+        (the cg lane, or ``stream``), behind the D2H that last drained the slot."""
         if q >= len(self._ochunks) or q in self._oh2d:
             return
         b, li, s, n = self._ochunks[q]
         k = (self._obase + q) % len(self.stage)
-        h2d = self.h2d_stream
+        h2d = stream if stream is not None else self.h2d_stream
         with torch.cuda.stream(h2d):
             if self.ev_d2h[k] is not None:
                 h2d.wait_event(self.ev_d2h[k])     # staging slot drained
@@ -1112,12 +1116,22 @@ class GPTZeroEngine:
         xs = [self._embed_fwd(PE, batches[li][0]) for li in range(nloc)]
         self._tspan(E.op, "compute", c0, self._tmark(cur))
         caches = [[None] * len(blocks) for _ in range(nloc)]
+        ev_every, fq = self.fwd_state_prefetch_every, 0
         for i, b in enumerate(blocks):
             slot = i % 2
             full = self._full(b, slot)
             if i + 1 < len(blocks):
                 gs.wait_stream(cur)  # slot (i+1)%2 was last read by compute of block i-1
                 self._fetch(blocks[i + 1], (i + 1) % 2, gs)
+                if (self.offload and host_params and ev_every and i % ev_every == ev_every - 1
+                        and fq < len(self.stage) - 1):   # slots this step has not claimed
+                    # the H2D lane has slack while the forward computes: queue one
+                    # optimizer-state chunk behind this fetch, in the fetch's own FIFO
+                    # (so it never delays the next fetch by more than its own length)
+                    self._phase = "backward"
+                    self._ostate_h2d(fq, stream=gs)
+                    self._phase = "forward"
+                    fq += 1
             else:
                 gs.wait_stream(cur)
                 self._phase = "backward"     # the head is the first backward op
@@ -1154,9 +1168,8 @@ class GPTZeroEngine:
         self._reduce_update(FB, fslot, consts)
         # ---- backward through the blocks, re-gathering each one
         nb = len(blocks)
-        if nb:
-            gs.wait_stream(cur)
-            self._fetch(blocks[-1], (nb - 1) % 2, gs)  # slot of FB is free after its update? no: use parity
+        # blocks[-1] is still in slot (nb-1)%2 from the forward (the head used the other
+        # slot), so the backward starts on it without a second fetch
         for j in range(nb - 1, -1, -1):
             b = blocks[j]
             slot = j % 2

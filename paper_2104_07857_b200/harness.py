@@ -242,7 +242,7 @@ def train_step(model: PartitionedModel, batch, hyper: AdamHyper, store: TierStor
         fetched = {k: _gather_widen(model, k) for k in sorted(model.fetch_sets[i])}
         W, b = _layer_weights(model, i, fetched)
         for g in range(G):
-            z = torch.addmm(b, acts[g][-1], W.t())
+            z = kernels.matmul_fixed(acts[g][-1], W.t(), bias=b)
             zs[g].append(z)
             acts[g].append(_act_fwd(spec.layers[i].act, z))
         del fetched, W, b  # release
@@ -267,9 +267,9 @@ def train_step(model: PartitionedModel, batch, hyper: AdamHyper, store: TierStor
         W, _ = _layer_weights(model, i, fetched)
         for g in range(G):
             dz = _act_bwd(L.act, zs[g][i], grads_out[g])
-            dW = dz.t() @ acts[g][i]
+            dW = kernels.matmul_fixed(dz.t(), acts[g][i])
             db = dz.sum(0)
-            grads_out[g] = dz @ W
+            grads_out[g] = kernels.matmul_fixed(dz, W)
             for key, s, e in own_buckets(spec)[i]:
                 flat = torch.cat([dW[s:e].reshape(-1), db[s:e]])
                 acc[(key, g)] = flat if (key, g) not in acc else acc[(key, g)] + flat
@@ -334,7 +334,7 @@ def synthetic_batch(spec: ModelSpec, batch: int, device):
     kernels.init_uniform(x, None, _key(spec.seed, 1000), 0, float(2.0 ** -24))
     kernels.init_uniform(A, None, _key(spec.seed, 1001), 0, float(2.0 ** -24))
     x = x.view(batch, d_in)
-    return x, x @ A.view(d_out, d_in).t()
+    return x, kernels.matmul_fixed(x, A.view(d_out, d_in).t())
 
 
 def digest(model: PartitionedModel) -> str:

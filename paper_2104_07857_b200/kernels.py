@@ -176,6 +176,32 @@ def cast_half_to_f32(src, dst, stream=None) -> None:
               half_kind(src.dtype), _stream(stream))
 
 
+def matmul_fixed(a: torch.Tensor, b: torch.Tensor, bias: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a @ b (+ bias) for 2-D f32/f64 CUDA views of any strides, summed over k in order
+    on one thread per output (zi_matmul_fixed): bit-reproducible, unlike cuBLAS."""
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[0]:
+        raise ValueError("matmul_fixed: shapes must be (M,K) @ (K,N)")
+    if a.dtype not in (torch.float32, torch.float64) or b.dtype != a.dtype:
+        raise ValueError("matmul_fixed: f32 or f64 operands of one dtype")
+    M, K = a.shape
+    N = b.shape[1]
+    if out is None:
+        out = torch.empty(M, N, dtype=a.dtype, device=a.device)
+    if out.shape != (M, N) or out.dtype != a.dtype:
+        raise ValueError("matmul_fixed: out shape/dtype mismatch")
+    if bias is not None and (bias.dtype != a.dtype or bias.numel() != N or not bias.is_contiguous()):
+        raise ValueError("matmul_fixed: bias must be a contiguous (N,) vector of the dtype")
+    dt = _lib.DT_F32 if a.dtype == torch.float32 else _lib.DT_F64
+    for t, nm in ((a, "a"), (b, "b"), (out, "out")):
+        if not t.is_cuda:
+            raise ValueError(f"matmul_fixed: {nm} must be a CUDA tensor")
+    _lib.call("zi_matmul_fixed", a.data_ptr(), a.stride(0), a.stride(1), b.data_ptr(),
+              b.stride(0), b.stride(1), _dev(bias, "bias") if bias is not None else None,
+              out.data_ptr(), out.stride(0), out.stride(1), M, N, K, dt, _stream(stream))
+    return out
+
+
 def _operand(t: torch.Tensor, name: str):
     """(pointer, mn_major, ld) of a 2-D bf16 view seen as (rows, k).
 

@@ -1,4 +1,5 @@
 make -j8 >/dev/null 2>&1
-timeout 600 python -m pytest tests/test_gpt_gpu.py tests/test_fused_gpu.py -q -x 2>&1 | tail -2
-for f in auto cublas; do ZI_GEMM_SELECT=$f timeout 600 python bench.py --no-cpu --no-offload > gpurun_out/bf$f.json 2>/dev/null; python -c "
-import json;d=json.loads(open('gpurun_out/bf$f.json').read().strip().splitlines()[-1]);print('gemm_select=$f', d['value'], d['ms_per_step'], d['e2e']['value'], d['clocks'])"; done
+timeout 300 python scripts/diag_ac9.py 2>&1 | tail -6
+CUBLAS_WORKSPACE_CONFIG=:4096:8 timeout 300 python scripts/diag_ac9.py 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_kernels_gpu.py tests/test_harness_gpu.py tests/test_gpt_gpu.py tests/test_cli.py -m gpu -q 2>&1 | tail -4
+timeout 900 python scripts/ab_config5.py 0:12 3:12 2:12 3:16 4:12 2>&1 | grep -v Warn | tail -8

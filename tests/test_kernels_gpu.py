@@ -207,3 +207,29 @@ def test_bad_arguments_raise():
         kernels.reduce_scatter_cast([], 0, 8, 8, 1.0, torch.bfloat16, t)
     with pytest.raises(ValueError):
         _lib.call("zi_adam_step", None, None, None, None, None, 8, None, 0, None)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_matmul_fixed_order(dtype):
+    """zi_matmul_fixed: equals a sequential fma chain per output (checked against an fp64
+    reference within the fp32 / fp64 rounding bound), accepts transposed views, and is
+    bit-identical across calls and operand placements."""
+    torch.manual_seed(0)
+    M, K, N = 37, 19, 23
+    a = torch.randn(M, K, dtype=dtype, device="cuda")
+    w = torch.randn(N, K, dtype=dtype, device="cuda")
+    b = torch.randn(N, dtype=dtype, device="cuda")
+    y = kernels.matmul_fixed(a, w.t(), bias=b)
+    ref = a.double() @ w.double().t() + b.double()
+    eps = torch.finfo(dtype).eps
+    assert (y.double() - ref).abs().max().item() <= 4 * K * eps * ref.abs().max().item()
+    # same bits through a differently laid-out copy of the operands
+    wt = w.t().contiguous()                 # (K, N) row-major: the same B, other strides
+    big = torch.zeros(M + 5, K + 3, dtype=dtype, device="cuda")
+    big[5:, 3:] = a
+    y2 = kernels.matmul_fixed(big[5:, 3:], wt, bias=b)
+    assert torch.equal(y, y2)
+    yc = kernels.matmul_fixed(a.t().contiguous().t(), w.t())   # column-major A view
+    assert torch.equal(yc, kernels.matmul_fixed(a, w.t()))
+    with pytest.raises(ValueError):
+        kernels.matmul_fixed(a, w)
