@@ -229,6 +229,36 @@ int zi_ipc_get_handle(void* dptr, unsigned char handle[64]);
 int zi_ipc_open(const unsigned char handle[64], void** dptr);
 int zi_ipc_close(void* dptr);
 
+/* ---- communicator context (SURVEY.md §8(b) zi_ctx_create / zi_ctx_destroy) -
+ * One per data-parallel rank: rank, world, device, and "windows" = the same-shaped
+ * buffer on every rank (parameter arena, gradient ring, barrier flags), IPC-mapped
+ * into this process once. Handles and byte offsets are exchanged out of band
+ * (torch.distributed in comm.DistComm): handles = world x 64 bytes from
+ * zi_ipc_get_handle of each rank's allocation, offsets = world byte offsets of the
+ * window inside it (our own entries are ignored; `local` is our pointer). The
+ * collectives below are the SPEC ops over a window, rank order = fold order.
+ * The NCCL communicator is torch.distributed's (plumbing); the data path is
+ * P2P loads/stores and copy-engine DMA over NVLink. Replaces the reference's
+ * in-process rank loop. Thread-safe per context. */
+typedef struct zi_ctx zi_ctx;
+int zi_ctx_create(int rank, int world, int device, zi_ctx** out);
+int zi_ctx_destroy(zi_ctx* ctx);
+int zi_ctx_info(const zi_ctx* ctx, int* rank, int* world, int* device);
+int zi_ctx_add_window(zi_ctx* ctx, void* local, const unsigned char* handles,
+                      const uint64_t* offsets, int* win);
+int zi_ctx_window_ptrs(zi_ctx* ctx, int win, void** ptrs);
+/* SPEC allgather: full[r*shard + i] = window_r[offset + i]. */
+int zi_ctx_allgather(zi_ctx* ctx, int win, size_t offset_bytes, size_t shard_elems, int dtype,
+                     void* full, size_t full_elems, int use_copy_engine, void* stream);
+/* SPEC reduce_scatter + cast: our shard (rank * shard_elems ..)
+ * of the rank-order fp32 fold of every rank's half bucket at window + offset,
+ * times scale; elements >= contrib_len read 0. Bit-exact to the oracle. */
+int zi_ctx_reduce_scatter_cast(zi_ctx* ctx, int win, size_t offset_bytes, size_t contrib_len,
+                               size_t shard_elems, float scale, int half_kind, float* shard_out,
+                               void* stream);
+/* zi_barrier over a window of `world` uint32 flags, with the epoch kept per window. */
+int zi_ctx_barrier(zi_ctx* ctx, int flags_win, void* stream);
+
 /* ---- memory-centric tiling ------------------------------
  * One tile of a tiled linear on the 5th-gen tensor cores (tcgen05 + TMEM,
  * TMA-fed), bf16 in, fp32 accumulate, bf16 out:

@@ -102,6 +102,17 @@ SIGNATURES = {
     "zi_ipc_get_handle": [c_void_p, ctypes.c_char_p],
     "zi_ipc_open": [ctypes.c_char_p, ctypes.POINTER(c_void_p)],
     "zi_ipc_close": [c_void_p],
+    "zi_ctx_create": [c_int, c_int, c_int, ctypes.POINTER(c_void_p)],
+    "zi_ctx_destroy": [c_void_p],
+    "zi_ctx_info": [c_void_p, ctypes.POINTER(c_int), ctypes.POINTER(c_int), ctypes.POINTER(c_int)],
+    "zi_ctx_add_window": [c_void_p, c_void_p, ctypes.c_char_p, ctypes.POINTER(c_uint64),
+                          ctypes.POINTER(c_int)],
+    "zi_ctx_window_ptrs": [c_void_p, c_int, ctypes.POINTER(c_void_p)],
+    "zi_ctx_allgather": [c_void_p, c_int, c_size_t, c_size_t, c_int, c_void_p, c_size_t, c_int,
+                         c_void_p],
+    "zi_ctx_reduce_scatter_cast": [c_void_p, c_int, c_size_t, c_size_t, c_size_t, c_float, c_int,
+                                   c_void_p, c_void_p],
+    "zi_ctx_barrier": [c_void_p, c_int, c_void_p],
     "zi_linear_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                       c_int, c_void_p],
     "zi_gemm": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,

@@ -8,10 +8,11 @@ Two implementations of one small interface:
   data path: every collective goes through the same libzinf kernels with
   the N shard / gradient buffers as local device pointers.
 * ``DistComm()`` — one process per GPU over ``torch.distributed``. Peer
-  buffers are exchanged once as CUDA-IPC handles, so the reduce-scatter and
-  the gather read peer HBM directly over NVLink 5 / NVSwitch inside libzinf
-  kernels (or copy engines); ``zi_barrier`` orders producers and consumers
-  across GPUs. With the gloo backend and no GPU the host-side plumbing
+  buffers are exchanged once as CUDA-IPC handles and mapped by the native
+  communicator context (``zi_ctx``: rank, world, device, windows), so the
+  reduce-scatter and the gather read peer HBM directly over NVLink 5 /
+  NVSwitch inside libzinf kernels (or copy engines); ``zi_ctx_barrier``
+  orders producers and consumers across GPUs. With the gloo backend and no GPU the host-side plumbing
   (rank layout, handle exchange, object collectives) runs on CPU for tests.
 """
 
@@ -97,9 +98,21 @@ class DistComm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.backend = dist.get_backend(group)
-        self._chan: dict = {}   # barrier channel -> [flags tensor, peer flag pointers, epoch]
-        self._opened: dict[bytes, int] = {}
+        self._chan: dict = {}   # barrier channel -> (flags tensor, its zi_ctx window)
         self._owned: dict[int, int] = {}   # base pointer -> bytes of our shareable buffers
+        self._ctx = None        # native zi_ctx (created on first peer-memory use: needs CUDA)
+        self.windows: dict[int, int] = {}  # local pointer -> zi_ctx window id
+
+    @property
+    def ctx(self) -> int:
+        """The native communicator context (zi_ctx_create): rank, world, device and
+        the IPC-mapped windows; the P2P collectives and barriers run through it."""
+        if self._ctx is None:
+            c = ctypes.c_void_p()
+            _lib.call("zi_ctx_create", self.rank, self.world, torch.cuda.current_device(),
+                      ctypes.byref(c))
+            self._ctx = c.value
+        return self._ctx
 
     def ranks(self):
         return [self.rank]
@@ -142,19 +155,43 @@ class DistComm:
         h = (ctypes.c_char * 64)()
         _lib.call("zi_ipc_get_handle", base, h)
         infos = self.all_gather_object((bytes(h), ptr - base))
-        ptrs = []
-        for r, (hb, off) in enumerate(infos):
-            if r == self.rank:
-                ptrs.append(ptr)
-                continue
-            pbase = self._opened.get(hb)
-            if pbase is None:  # one mapping per peer allocation
-                buf = (ctypes.c_char * 64).from_buffer_copy(hb)
-                p = ctypes.c_void_p()
-                _lib.call("zi_ipc_open", buf, ctypes.byref(p))
-                pbase = self._opened[hb] = p.value
-            ptrs.append(pbase + off)
-        return ptrs
+        handles = b"".join(hb for hb, _ in infos)
+        offs = (ctypes.c_uint64 * self.world)(*[off for _, off in infos])
+        win = ctypes.c_int()
+        # zi_ctx maps each peer allocation once (lazy peer access over NVLink)
+        _lib.call("zi_ctx_add_window", self.ctx, ptr, handles, offs, ctypes.byref(win))
+        arr = (ctypes.c_void_p * self.world)()
+        _lib.call("zi_ctx_window_ptrs", self.ctx, win.value, arr)
+        self.windows[ptr] = win.value
+        return [int(a) for a in arr]
+
+    def window(self, t: torch.Tensor) -> int:
+        """zi_ctx window id of a buffer passed to ``share``."""
+        return self.windows[t.data_ptr()]
+
+    def allgather_window(self, t: torch.Tensor, shard_elems: int, full: torch.Tensor,
+                         offset_elems: int = 0, use_copy_engine: bool = False,
+                         stream=None) -> None:
+        """SPEC allgather over a shared window (zi_ctx_allgather): full = concat over
+        ranks of window_r[offset : offset + shard], truncated to full.numel()."""
+        dt = {torch.float32: _lib.DT_F32, torch.float64: _lib.DT_F64,
+              torch.float16: _lib.DT_F16, torch.bfloat16: _lib.DT_BF16}[t.dtype]
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _lib.call("zi_ctx_allgather", self.ctx, self.window(t), offset_elems * t.element_size(),
+                  shard_elems, dt, full.data_ptr(), full.numel(), int(use_copy_engine),
+                  s.cuda_stream)
+
+    def reduce_scatter_window(self, t: torch.Tensor, shard_elems: int, out: torch.Tensor,
+                              scale: float, contrib_len: int | None = None,
+                              offset_elems: int = 0, stream=None) -> None:
+        """SPEC reduce_scatter + cast over a shared half window (zi_ctx_reduce_scatter_cast):
+        out (fp32, our shard) = scale * rank-order fold of every rank's bucket."""
+        from .kernels import half_kind
+        s = stream if stream is not None else torch.cuda.current_stream()
+        n = t.numel() - offset_elems if contrib_len is None else contrib_len
+        _lib.call("zi_ctx_reduce_scatter_cast", self.ctx, self.window(t),
+                  offset_elems * t.element_size(), n, shard_elems, scale, half_kind(t.dtype),
+                  out.data_ptr(), s.cuda_stream)
 
     def device_barrier(self, stream=None, channel: int = 0) -> None:
         """zi_barrier over IPC flag words (orders P2P reads with peer writers).
@@ -168,12 +205,10 @@ class DistComm:
             return
         if channel not in self._chan:   # collective on first use of the channel
             flags = self.alloc((self.world,), torch.int32)
-            self._chan[channel] = [flags, self.share(flags), 0]
-        ch = self._chan[channel]
-        ch[2] += 1
+            self.share(flags)
+            self._chan[channel] = (flags, self.window(flags))
         s = stream if stream is not None else torch.cuda.current_stream()
-        _lib.call("zi_barrier", _lib.ptr_array(ch[1]), self.world, self.rank, ch[2],
-                  s.cuda_stream)
+        _lib.call("zi_ctx_barrier", self.ctx, self._chan[channel][1], s.cuda_stream)
 
     def barrier(self, stream=None) -> None:
         if self.backend == "nccl":
@@ -182,6 +217,9 @@ class DistComm:
             dist.barrier(group=self.group)
 
     def close(self) -> None:
-        for p in self._opened.values():
-            _lib.call("zi_ipc_close", p)
-        self._opened.clear()
+        """zi_ctx_destroy: unmaps every peer window (peers must be done reading ours)."""
+        if self._ctx is not None:
+            _lib.call("zi_ctx_destroy", self._ctx)
+            self._ctx = None
+            self.windows.clear()
+            self._chan.clear()

@@ -534,7 +534,13 @@ class GPTZeroEngine:
                 # IPC-shared HBM staging slot, then gg = P2P gather of every rank's slot.
                 # The gather-channel barrier before the gg makes all ranks' cg visible; the
                 # next fetch's barrier keeps a slot from being refilled while peers read it.
-                k = 0 if b.key == "embed" else 1 + slot
+                # the two ring stages alternate per fetch (not per slot: the backward
+                # skips the re-fetch of the last block, so slots do not alternate there)
+                if b.key == "embed":
+                    k = 0
+                else:
+                    self._pstage_n = getattr(self, "_pstage_n", 0) + 1
+                    k = 1 + self._pstage_n % 2
                 stage = self.pstage[k]
                 stage[:b.shard].copy_(self._shard_view(self.p16, 0, b), non_blocking=True)
                 self.comm.device_barrier(stream, channel=1)

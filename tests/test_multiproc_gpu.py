@@ -92,3 +92,84 @@ def test_two_processes_match_local_comm(placement):
             np.testing.assert_allclose(arr, want, rtol=0, atol=5e-5, err_msg=key)
     mean_dist = [(res[0][0][s] + res[1][0][s]) / 2 for s in range(2)]
     np.testing.assert_allclose(mean_dist, ref_losses, rtol=1e-5)
+
+
+def _ctx_rank_main(rank, world, port, q):
+    """zi_ctx collectives through DistComm windows: one rank per process."""
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import numerics as nx
+        from paper_2104_07857_b200.comm import DistComm
+        comm = DistComm()
+        n = 10_007                                   # ragged: last shard zero padded
+        L = -(-n // world)
+        off = 24                                     # window at an offset inside its allocation
+        rng = np.random.default_rng(100 + rank)
+        g_bits = nx.f32_to_half_bits(rng.standard_normal(n).astype(np.float32), nx.HALF_BF16)
+        buf = comm.alloc((off + n,), torch.bfloat16)
+        grads = buf[off:]
+        grads.copy_(torch.from_numpy(g_bits.view(np.int16).copy()).view(torch.bfloat16))
+        pbuf = comm.alloc((L,), torch.float32)
+        pbuf.copy_(torch.arange(rank * L, rank * L + L, dtype=torch.float32) * 0.5)
+        comm.share(grads)
+        comm.share(pbuf)
+        comm.device_barrier()                        # peers' windows are written
+        out = torch.empty(L, dtype=torch.float32, device="cuda")
+        comm.reduce_scatter_window(grads, L, out, scale=1.0 / world)
+        full = torch.empty(n, dtype=torch.float32, device="cuda")
+        comm.allgather_window(pbuf, L, full)
+        full_ce = torch.empty(n, dtype=torch.float32, device="cuda")
+        comm.allgather_window(pbuf, L, full_ce, use_copy_engine=True)
+        comm.device_barrier()                        # peers are done reading our windows
+        torch.cuda.synchronize()
+        info = [ctypes_info(comm)]
+        res = (out.cpu().numpy(), full.cpu().numpy(), full_ce.cpu().numpy(), g_bits, info)
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok", res))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+def ctypes_info(comm):
+    import ctypes
+    from paper_2104_07857_b200 import _lib
+    r, w, d = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.call("zi_ctx_info", comm.ctx, ctypes.byref(r), ctypes.byref(w), ctypes.byref(d))
+    return r.value, w.value, d.value
+
+
+def test_ctx_collectives_two_processes():
+    """zi_ctx_reduce_scatter_cast / zi_ctx_allgather across 2 processes:
+    RS bit-exact against the oracle's rank-order fold, gathers bit-exact (SM kernel and
+    copy engines), windows at byte offsets inside their allocations."""
+    from oracle import numerics as nx
+    from oracle.partition import reduce_scatter_cast
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_ctx_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, st, b = q.get(timeout=300)
+        assert st == "ok", b
+        res[r] = b
+    for p in procs:
+        p.join(timeout=60)
+    n, L = 10_007, 5004
+    contribs = [nx.half_bits_to_f32(res[r][3], nx.HALF_BF16) for r in range(world)]
+    want = reduce_scatter_cast(contribs, world, 1.0 / world)
+    pfull = (np.arange(world * L, dtype=np.float32) * 0.5)[:n]
+    for r in range(world):
+        out, full, full_ce, _, info = res[r]
+        assert info[0] == (r, world, 0)
+        assert np.array_equal(out.view(np.uint32), want[r].view(np.uint32))
+        assert np.array_equal(full, pfull) and np.array_equal(full_ce, pfull)
