@@ -135,6 +135,7 @@ class DistComm:
     def alloc(self, shape, dtype: torch.dtype) -> torch.Tensor:
         """A zeroed CUDA buffer peers can map: its own cudaMalloc (zi_device_alloc),
         so the IPC handle names exactly this buffer."""
+        _ = self.ctx            # zi_ctx_create pins libzinf's device to this rank's GPU
         t = _ipc_tensor(shape, dtype)
         self._owned[t.data_ptr()] = t.untyped_storage().nbytes()
         return t

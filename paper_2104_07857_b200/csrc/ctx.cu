@@ -70,6 +70,9 @@ int zi_ctx_create(int rank, int world, int device, zi_ctx** out) {
   int ndev = 0;
   ZI_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
   ZI_CHECK_ARG(device < ndev, "zi_ctx_create: device %d of %d", device, ndev);
+  // libzinf links its own (static) CUDA runtime: make its current device on this thread
+  // the rank's GPU, so zi_device_alloc / IPC mappings / launches agree with the caller's
+  ZI_CUDA(cudaSetDevice(device), "cudaSetDevice");
   zi_ctx* c = new zi_ctx;
   c->rank = rank;
   c->world = world;

@@ -164,7 +164,7 @@ class GPTZeroEngine:
                  lr: float = 1e-4, betas=(0.9, 0.999), eps: float = 1e-8,
                  prefetch: bool = True, copy_engine_gather: bool | None = None,
                  trace: bool = False, offload_chunk: int = 16 << 20, fused: bool = True,
-                 overlap_opt: bool = True, act_ckpt: str | None = None,
+                 overlap_opt: bool | None = None, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
                  offload_slots: int | None = None, nvme_direct: bool = False,
                  fwd_state_prefetch_every: int = 2):
@@ -195,6 +195,15 @@ class GPTZeroEngine:
         # params on the host: one optimizer-state chunk H2D per this many forward
         # blocks, queued behind their parameter fetches (0: all after the forward)
         self.fwd_state_prefetch_every = fwd_state_prefetch_every
+        # RS + Adam on a side stream, overlapped with the next bucket's backward GEMMs:
+        # pays with peers (the RS reads them over NVLink) or host transfers in flight;
+        # at N=1 in HBM it measured equal to running them in order (69.4-69.7 ms,
+        # scripts/ab_overlap.py), and in order the HBM-bound kernel has the GPU to itself
+        if overlap_opt is None:
+            env = os.environ.get("ZI_OVERLAP_OPT")
+            overlap_opt = (env == "1") if env in ("0", "1") else (
+                self.N > 1 or self.placement.optim is not TierKind.DEVICE
+                or self.placement.params is not TierKind.DEVICE)
         self.overlap_opt = overlap_opt
         if act_ckpt not in (None, "device", "host"):
             raise ValueError("act_ckpt must be None, 'device' or 'host'")
