@@ -536,6 +536,125 @@ softmax_ce_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ tgt
     L[i] = tobf((__expf(bf(L[i]) - lse) - (i == t ? 1.f : 0.f)) * scale);
 }
 
+// Persistent, row-staged variant (V % 8 == 0, two rows fit in shared memory): one CTA
+// per SM streams its rows through a 2-deep ring of whole bf16 rows filled by one bulk
+// copy each, so row r+1 lands while row r is worked on, and the logits are read from
+// HBM once (the CTA-per-row kernel reads them twice with one 16-byte load per thread
+// in flight). The row work is issue-bound, so it is kept to ~8 instructions per
+// logit: max on packed bf16 pairs (exact), then e = 2^(l*log2e - max*log2e) (one
+// FFMA + one MUFU) summed in fp32 and parked as fp16 over the row in shared memory,
+// then dlogits = e * (scale / sum) with the target's -scale applied once by the
+// thread that owns it. lse = max + log(sum) from the fp32 sum, as in the CTA-per-row
+// kernel (same loss; dlogits differ by the fp16 parking of e: relative 2^-11, under
+// the bf16 output rounding).
+constexpr int CE_NT = 1024;
+__device__ __forceinline__ float ce_block_reduce(float v, float* red, bool is_max) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, u) : v + u;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = red[0];
+#pragma unroll
+  for (int k = 1; k < CE_NT / 32; ++k) r = is_max ? fmaxf(r, red[k]) : r + red[k];
+  return r;   // red is rewritten only after the caller's next __syncthreads
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__global__ void __launch_bounds__(CE_NT, 1)
+softmax_ce_ring_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ tgt,
+                       float* __restrict__ loss_rows, int T, int V, int Vpad, float scale) {
+  extern __shared__ __align__(128) uint16_t rowbuf[];     // [2][Vpad] bf16 + 2 mbarriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowbuf + 2 * (size_t)Vpad);
+  __shared__ float red_m[CE_NT / 32], red_s[CE_NT / 32];
+  constexpr float LOG2E = 1.4426950408889634f;
+  const int V8 = V / 8;
+  const uint32_t bytes = (uint32_t)V * 2;
+  if (threadIdx.x == 0) {
+    bulk::mbar_init(&full[0], 1);
+    bulk::mbar_init(&full[1], 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int it) {                      // thread 0: row of iteration it
+    const size_t row = (size_t)blockIdx.x + (size_t)it * gridDim.x;
+    if (row >= (size_t)T) return;
+    const int b = it & 1;
+    bulk::mbar_expect_tx(&full[b], bytes);
+    bulk::g2s(rowbuf + b * (size_t)Vpad, logits + row * V, bytes, &full[b]);
+  };
+  if (threadIdx.x == 0) {
+    issue(0);
+    issue(1);
+  }
+  for (int it = 0;; ++it) {
+    const size_t row = (size_t)blockIdx.x + (size_t)it * gridDim.x;
+    if (row >= (size_t)T) break;
+    const int b = it & 1;
+    const int t = (int)tgt[row];
+    bulk::mbar_wait(&full[b], (it >> 1) & 1);
+    uint16_t* R = rowbuf + b * (size_t)Vpad;
+    uint4* S = reinterpret_cast<uint4*>(R);
+    const float lt = threadIdx.x == 0 ? bf(R[t]) : 0.f;   // read before the barrier in the
+                                                           // max reduce: e overwrites R below
+    __nv_bfloat162 mx = __float2bfloat162_rn(-INFINITY);
+    for (int i = threadIdx.x; i < V8; i += CE_NT) {
+      const uint4 w = S[i];
+      mx = __hmax2(mx, __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.x),
+                               *reinterpret_cast<const __nv_bfloat162*>(&w.y)));
+      mx = __hmax2(mx, __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&w.z),
+                               *reinterpret_cast<const __nv_bfloat162*>(&w.w)));
+    }
+    const float m = ce_block_reduce(fmaxf(__low2float(mx), __high2float(mx)), red_m, true);
+    const float ml = m * LOG2E;
+    float sum = 0.f;
+    for (int i = threadIdx.x; i < V8; i += CE_NT) {
+      float f[8];
+      ld_row<8>(reinterpret_cast<const uint16_t*>(S + i), f);
+      uint32_t h[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float e0 = ex2_approx(fmaf(f[2 * j], LOG2E, -ml));
+        const float e1 = ex2_approx(fmaf(f[2 * j + 1], LOG2E, -ml));
+        sum += e0;
+        sum += e1;
+        const __half2 hv = __floats2half2_rn(e0, e1);
+        h[j] = *reinterpret_cast<const uint32_t*>(&hv);
+      }
+      S[i] = make_uint4(h[0], h[1], h[2], h[3]);  // e parked as fp16 in place (own chunk)
+    }
+    sum = ce_block_reduce(sum, red_s, false);
+    if (threadIdx.x == 0) loss_rows[row] = m + __logf(sum) - lt;
+    const float c = scale / sum;
+    uint16_t* L = logits + row * V;
+    for (int i = threadIdx.x; i < V8; i += CE_NT) {
+      const uint4 w = S[i];
+      const uint32_t h[4] = {w.x, w.y, w.z, w.w};
+      float f[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 e = __half22float2(*reinterpret_cast<const __half2*>(&h[j]));
+        f[2 * j] = e.x * c;
+        f[2 * j + 1] = e.y * c;
+      }
+      if (i == (t >> 3)) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] -= (j == (t & 7)) ? scale : 0.f;
+      }
+      st_row<8>(L + 8 * i, f);
+    }
+    __syncthreads();                              // row buffer b and red_* fully read
+    if (threadIdx.x == 0) issue(it + 2);
+  }
+}
+
 __global__ void sum_kernel(const float* __restrict__ v, int n, float scale, float* __restrict__ out) {
   // single block, fixed-order tree: deterministic
   __shared__ float sm[1024];
@@ -756,7 +875,21 @@ int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float*
                   float scale, void* stream) {
   ZI_CHECK_ARG(logits && targets && loss_rows && loss && T > 0 && V > 0, "zi_softmax_ce: bad args");
   cudaStream_t s = (cudaStream_t)stream;
-  softmax_ce_kernel<<<T, 512, 0, s>>>((uint16_t*)logits, targets, loss_rows, V, scale);
+  const int Vpad = (V + 63) / 64 * 64;                    // 128-byte aligned row slots
+  const size_t ring_smem = 2 * (size_t)Vpad * 2 + 16;
+  if (V % 8 == 0 && zi::aligned(logits, 16) && ring_smem <= 220 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      ZI_CUDA(cudaFuncSetAttribute(softmax_ce_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   220 * 1024), "cudaFuncSetAttribute(softmax_ce)");
+      attr = true;
+    }
+    const int grid = T < sm_count() ? T : sm_count();
+    softmax_ce_ring_kernel<<<grid, CE_NT, ring_smem, s>>>((uint16_t*)logits, targets, loss_rows, T,
+                                                           V, Vpad, scale);
+  } else {
+    softmax_ce_kernel<<<T, 512, 0, s>>>((uint16_t*)logits, targets, loss_rows, V, scale);
+  }
   int st = zi::launch_status("zi_softmax_ce");
   if (st) return st;
   sum_kernel<<<1, 1024, 0, s>>>(loss_rows, T, 1.0f / T, loss);

@@ -121,7 +121,7 @@ def test_bias_grad(T, N, gelu):
     close(db, ref, atol=1e-3 * T ** 0.5)
 
 
-@pytest.mark.parametrize("T,V", [(8, 512), (1024, 50304), (33, 1000)])
+@pytest.mark.parametrize("T,V", [(8, 512), (1024, 50304), (33, 1000), (300, 50304), (5, 1001)])
 def test_softmax_ce(T, V):
     g = torch.Generator(device="cuda").manual_seed(V)
     logits = (3 * torch.randn(T, V, device="cuda", generator=g)).bfloat16()
