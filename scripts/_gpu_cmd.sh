@@ -1,9 +1,5 @@
-L=paper_2104_07857_b200/libzinf.so
-cp $L /tmp/new.so
-for rep in 1 2; do
-cp build_ab/libzinf_old.so $L; echo old; timeout 300 python scripts/bench_fused.py 2>&1 | grep -i "softmax"
-cp /tmp/new.so $L; echo new; timeout 300 python scripts/bench_fused.py 2>&1 | grep -i "softmax"
-done
-timeout 600 python -m pytest tests/test_fused_gpu.py tests/test_gpt_gpu.py -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py --no-cpu --no-offload > gpurun_out/b.json 2>/dev/null; python -c "
-import json;d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]);print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['clocks'])"
+make -j8 >/dev/null 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests $?; tail -2 gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench_s3b.json 2> gpurun_out/bench_s3b.err; echo bench $?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_s3b.csv python scripts/profile_step.py --graph > /dev/null 2>&1; echo ncu $?
