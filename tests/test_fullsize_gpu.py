@@ -9,6 +9,9 @@ shard only:
   world 8 and ragged world 3; the fused RS + Adam of one rank's shard against the numpy
   oracle on that shard (bit-exact); Adam chunk invariance at the offload chunk size;
 * config 2 step: optimizer states offloaded to pinned host vs in HBM after one step;
+* configs 3 and 5 (10B / 70B): one layer bucket (0.2 G / 0.8 G elements) — gather round
+  trip at world 8 and ragged world 3, and the fused RS + Adam over 8 full 70B-layer
+  gradient buckets (12.9 GB) checked against the oracle on windows of the shard;
 * config 4 (tiling 16384 -> 65536, M = 8192): the tiled forward at T = 4, 8, 16 against
   the untiled tcgen05 GEMM (every output element is the same K-reduction, so the tile
   count must not change a bit), and the tiled backward against cuBLAS.
@@ -180,3 +183,63 @@ def test_config4_tiled_backward_matches_cublas(config4, tmp_path):
         rW = g[:, s:e].t().float() @ x.float()
         assert ((dW[t].float() - rW).norm() / rW.norm()) < 4e-3, t
         torch.testing.assert_close(db[t].float(), g[:, s:e].float().sum(0), rtol=1e-2, atol=1e-2)
+
+
+# BASELINE configs 3 and 5: one transformer layer's bucket (SURVEY.md §8 size sheet)
+LAYER_10B = 12 * 4096 * 4096 + 13 * 4096            # 201,379,840
+LAYER_70B = 12 * 8192 * 8192 + 13 * 8192            # 805,412,864
+
+
+@pytest.mark.parametrize("n,world", [(LAYER_70B, 8), (LAYER_10B, 8), (LAYER_70B, 3)])
+def test_config5_layer_gather_roundtrip(n, world):
+    """The 70B (config 5) and 10B (config 3) layer buckets, 1.6 GB / 0.4 GB of bf16:
+    partition + gather is the identity (SM kernel and copy engines), size_t offsets."""
+    full = torch.randint(-32768, 32767, (n,), dtype=torch.int16, device="cuda")
+    L = -(-n // world)
+    shards = [torch.zeros(L, dtype=torch.int16, device="cuda") for _ in range(world)]
+    for r in range(world):
+        lo, hi = r * L, min(n, (r + 1) * L)
+        shards[r][:hi - lo] = full[lo:hi]
+    out = torch.empty(L * world, dtype=torch.int16, device="cuda")
+    for ce in (False, True):
+        out.fill_(-1)
+        kernels.allgather(shards, L, out, n, use_copy_engine=ce)
+        assert torch.equal(out[:n], full)
+        assert (out[n:] == -1).all()
+    del full, shards, out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("world,rank", [(8, 5), (3, 2)])
+def test_config5_layer_rs_adam_windows_match_oracle(world, rank):
+    """zi_rs_adam over `world` full 70B-layer bf16 gradient buckets (805 M elements each,
+    12.9 GB at world 8): the fused RS + Adam is elementwise in the shard, so the oracle
+    on three 1 M-element windows of this rank's shard (head, middle, and the tail that
+    runs into the zero pad at world 3) must match the kernel's full-shard launch bit
+    for bit."""
+    n = LAYER_70B
+    L = -(-n // world)
+    gen = torch.Generator(device="cuda").manual_seed(world * 100 + rank)
+    dc = [(torch.randn(n, device="cuda", generator=gen) * 1e-2).bfloat16() for _ in range(world)]
+    tp = torch.rand(L, device="cuda", generator=gen) * 0.1 - 0.05
+    tm = torch.randn(L, device="cuda", generator=gen) * 1e-3
+    tv = (torch.randn(L, device="cuda", generator=gen) * 1e-5).abs()
+    w = 1 << 20
+    starts = [0, L // 2 - w // 2, L - w]
+    before = [[t[s:s + w].cpu().numpy().copy() for t in (tp, tm, tv)] for s in starts]
+    win_c = [[_bits16(d[rank * L + s:min(n, rank * L + s + w)]) for d in dc] for s in starts]
+    th = torch.empty(L, dtype=torch.bfloat16, device="cuda")
+    tg = torch.empty(L, dtype=torch.float32, device="cuda")
+    kernels.rs_adam(dc, rank * L, L, n, 1.0 / world, tp, tm, tv, th,
+                    _lib.adam_consts(1e-4, 0.9, 0.999, 1e-8, 7), g_out=tg)
+    torch.cuda.synchronize()
+    c = AdamConsts.make(1e-4, 0.9, 0.999, 1e-8, 7)
+    for s, (p, m, v), cw in zip(starts, before, win_c):
+        P, M, V, H, G = rs_adam(p, m, v, cw, 0, world, 1.0 / world, c, nx.HALF_BF16)
+        for got, want in ((tg, G), (tp, P), (tm, M), (tv, V)):
+            assert np.array_equal(got[s:s + w].cpu().numpy().view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(_bits16(th[s:s + w]), H)
+    if rank * L + L > n:                      # the pad of the last shard folds zeros
+        assert (tg[n - rank * L:] == 0).all()
+    del dc
+    torch.cuda.empty_cache()
