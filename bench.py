@@ -373,8 +373,8 @@ def run_ours(args):
         rec.append((tm, None, n * (2 * ncontrib + 12 + 14), torch.cuda.is_current_stream_capturing()))
 
     K.rs_adam_dc = timed_rs_adam
-    if world > 1:
-        args.no_graph = True   # multi-process: eager steps (barrier kernels + IPC peers)
+    # multi-process too: the zi_ctx barriers take their epochs from device counters, so
+    # the captured step (P2P gathers, barriers, RS + Adam over peer buckets) replays
     step = eng.step if args.no_graph else eng.step_graphed
     for w in range(args.warmup):
         step([dev_batches[w % len(dev_batches)]])

@@ -113,6 +113,9 @@ int zi_allgather(const void* const* shards, int world, size_t shard_elems,
  * `world` uint32), then spins until its own array holds >= epoch in every
  * slot. Orders the P2P reduce-scatter / gather with the peers' producers. */
 int zi_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream);
+/* Same barrier with the epoch taken from (and advanced in) a device counter: graph-safe. */
+int zi_barrier_dev(uint32_t* const* flags, int world, int rank, uint32_t* epoch_ctr,
+                   void* stream);
 
 /* ---- init / casts ---------------------------------------------------------
  * Counter-RNG uniform init (oracle/numerics.py:uniform_init):
@@ -256,7 +259,8 @@ int zi_ctx_allgather(zi_ctx* ctx, int win, size_t offset_bytes, size_t shard_ele
 int zi_ctx_reduce_scatter_cast(zi_ctx* ctx, int win, size_t offset_bytes, size_t contrib_len,
                                size_t shard_elems, float scale, int half_kind, float* shard_out,
                                void* stream);
-/* zi_barrier over a window of `world` uint32 flags, with the epoch kept per window. */
+/* zi_barrier_dev over a window of `world` uint32 flags; the epoch is a device counter per
+ * window, so the barrier may be captured in a CUDA graph and replayed. */
 int zi_ctx_barrier(zi_ctx* ctx, int flags_win, void* stream);
 
 /* ---- memory-centric tiling ------------------------------

@@ -50,6 +50,7 @@ SIGNATURES = {
     "zi_allgather": [ctypes.POINTER(c_void_p), c_int, c_size_t, c_size_t, c_void_p, c_size_t,
                      c_int, c_void_p],
     "zi_barrier": [ctypes.POINTER(c_void_p), c_int, c_int, c_uint32, c_void_p],
+    "zi_barrier_dev": [ctypes.POINTER(c_void_p), c_int, c_int, c_void_p, c_void_p],
     "zi_init_uniform": [c_void_p, c_void_p, c_size_t, c_uint64, c_uint64, c_float, c_int, c_void_p],
     "zi_fill": [c_void_p, c_void_p, c_size_t, c_float, c_int, c_void_p],
     "zi_cast_f32_to_half": [c_void_p, c_void_p, c_size_t, c_int, c_void_p],

@@ -68,7 +68,18 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-__global__ void barrier_kernel(FlagTable f, int world, int rank, uint32_t epoch) {
+// epoch_ctr != nullptr: the epoch is this channel's device counter + 1 (incremented
+// here, in stream order), so a barrier captured in a CUDA graph gets a fresh epoch on
+// every replay, identical on every rank (each rank runs the same barrier sequence).
+__global__ void barrier_kernel(FlagTable f, int world, int rank, uint32_t epoch,
+                               uint32_t* epoch_ctr) {
+  if (epoch_ctr != nullptr) {
+    __shared__ uint32_t e;
+    if (threadIdx.x == 0) e = *epoch_ctr + 1;
+    __syncthreads();
+    epoch = e;
+    if (threadIdx.x == 0) *epoch_ctr = e;
+  }
   const int k = threadIdx.x;
   if (k < world) {
     __threadfence_system();
@@ -143,8 +154,23 @@ int zi_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void
     ZI_CHECK_ARG(flags[k] != nullptr, "zi_barrier: flags[%d] is NULL", k);
     f.ptr[k] = flags[k];
   }
-  zi::barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, rank, epoch);
+  zi::barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, rank, epoch, nullptr);
   return zi::launch_status("zi_barrier");
+}
+
+int zi_barrier_dev(uint32_t* const* flags, int world, int rank, uint32_t* epoch_ctr,
+                   void* stream) {
+  ZI_CHECK_ARG(flags != nullptr && epoch_ctr != nullptr, "zi_barrier_dev: NULL argument");
+  ZI_CHECK_ARG(world >= 1 && world <= zi::kMaxWorld && rank >= 0 && rank < world,
+               "zi_barrier_dev: bad world/rank %d/%d", world, rank);
+  if (world == 1) return ZI_OK;
+  zi::FlagTable f{};
+  for (int k = 0; k < world; ++k) {
+    ZI_CHECK_ARG(flags[k] != nullptr, "zi_barrier_dev: flags[%d] is NULL", k);
+    f.ptr[k] = flags[k];
+  }
+  zi::barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, rank, 0u, epoch_ctr);
+  return zi::launch_status("zi_barrier_dev");
 }
 
 }  // extern "C"

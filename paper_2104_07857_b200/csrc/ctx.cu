@@ -9,8 +9,10 @@
 //     any launcher) and handed to zi_ctx_add_window, which maps every peer
 //     allocation once (cudaIpcMemLazyEnablePeerAccess: direct NVLink 5 loads and
 //     stores between GPUs) and keeps the per-rank pointer table;
-//   * barrier epochs: one counter per flag window, so zi_ctx_barrier needs no
-//     caller-side state and barriers on different streams use different windows.
+//   * barrier epochs: one device-side counter per flag window, advanced by the barrier
+//     kernel itself, so zi_ctx_barrier needs no caller-side state, a barrier captured in
+//     a CUDA graph stays correct on every replay, and barriers on different streams use
+//     different windows.
 // The data-path entry points are the SPEC collectives over a window:
 //   zi_ctx_allgather           = SPEC allgather
 //   zi_ctx_reduce_scatter_cast = SPEC reduce_scatter with the half->fp32 cast and
@@ -28,8 +30,9 @@ struct zi_ctx {
   std::mutex mu;
   struct Window {
     std::vector<uint8_t*> ptr;   // [world] base of this window on each rank (ours is local)
-    uint32_t epoch = 0;          // barrier epoch when used as a flag window
   };
+  static constexpr int kMaxWindows = 1024;
+  uint32_t* epochs = nullptr;    // device: barrier epoch counter per window (graph-safe)
   std::vector<Window> windows;
   struct Mapping {
     unsigned char handle[64];
@@ -73,7 +76,11 @@ int zi_ctx_create(int rank, int world, int device, zi_ctx** out) {
   // libzinf links its own (static) CUDA runtime: make its current device on this thread
   // the rank's GPU, so zi_device_alloc / IPC mappings / launches agree with the caller's
   ZI_CUDA(cudaSetDevice(device), "cudaSetDevice");
+  uint32_t* ep = nullptr;
+  ZI_CUDA(cudaMalloc(&ep, zi_ctx::kMaxWindows * sizeof(uint32_t)), "cudaMalloc(epochs)");
+  ZI_CUDA(cudaMemset(ep, 0, zi_ctx::kMaxWindows * sizeof(uint32_t)), "cudaMemset(epochs)");
   zi_ctx* c = new zi_ctx;
+  c->epochs = ep;
   c->rank = rank;
   c->world = world;
   c->device = device;
@@ -92,6 +99,7 @@ int zi_ctx_destroy(zi_ctx* c) {
     }
     c->mapped.clear();
   }
+  if (c->epochs) cudaFree(c->epochs);
   delete c;
   return st;
 }
@@ -107,6 +115,7 @@ int zi_ctx_info(const zi_ctx* c, int* rank, int* world, int* device) {
 int zi_ctx_add_window(zi_ctx* c, void* local, const unsigned char* handles,
                       const uint64_t* offsets, int* win) {
   ZI_CHECK_ARG(c && local && win, "zi_ctx_add_window: NULL argument");
+  ZI_CHECK_ARG((int)c->windows.size() < zi_ctx::kMaxWindows, "zi_ctx_add_window: too many windows");
   ZI_CHECK_ARG(c->world == 1 || (handles && offsets), "zi_ctx_add_window: NULL handles/offsets");
   std::lock_guard<std::mutex> g(c->mu);
   zi_ctx::Window w;
@@ -176,16 +185,16 @@ int zi_ctx_reduce_scatter_cast(zi_ctx* c, int win, size_t offset_bytes, size_t c
 int zi_ctx_barrier(zi_ctx* c, int flags_win, void* stream) {
   ZI_CHECK_ARG(c != nullptr, "zi_ctx_barrier: NULL ctx");
   std::vector<uint32_t*> f(c->world);
-  uint32_t epoch;
   {
     std::lock_guard<std::mutex> g(c->mu);
     ZI_CHECK_ARG(flags_win >= 0 && flags_win < (int)c->windows.size(),
                  "zi_ctx_barrier: bad window %d", flags_win);
     auto& w = c->windows[flags_win];
     for (int r = 0; r < c->world; ++r) f[r] = reinterpret_cast<uint32_t*>(w.ptr[r]);
-    epoch = ++w.epoch;
   }
-  return zi_barrier(f.data(), c->world, c->rank, epoch, stream);
+  // the epoch lives on the device (one counter per window): CUDA-graph replays of a
+  // captured barrier advance it like eager calls do
+  return zi_barrier_dev(f.data(), c->world, c->rank, c->epochs + flags_win, stream);
 }
 
 }  // extern "C"

@@ -1,2 +1,2 @@
 make -j8 >/dev/null 2>&1
-timeout 900 python -m pytest tests/test_fullsize_gpu.py -m gpu -q -k "config5" --durations=5 2>&1 | tail -12
+ZINF_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --steps 3 --warmup 3 --no-cpu --no-offload 2>&1 | grep -v Warning | tail -1 > gpurun_out/bench_4rank_graph.json; echo rc $?; cut -c1-600 gpurun_out/bench_4rank_graph.json

@@ -34,7 +34,7 @@ def _placement(name):
     return {"hbm": Placement(D, D), "params_host": Placement(H, D), "all_host": Placement(H, H)}[name]
 
 
-def _rank_main(rank, world, port, q, placement="hbm"):
+def _rank_main(rank, world, port, q, placement="hbm", graph=False):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -47,8 +47,9 @@ def _rank_main(rank, world, port, q, placement="hbm"):
         eng = eg.GPTZeroEngine(c, comm, lr=1e-3, placement=_placement(placement),
                                offload_chunk=20_000)
         losses = []
+        run = eng.step_graphed if graph else eng.step
         for step in range(2):
-            losses.append(eng.step([eg.synthetic_tokens(c, 7, rank, step)]).item())
+            losses.append(run([eg.synthetic_tokens(c, 7, rank, step)]).item())
         torch.cuda.synchronize()
         out = {k: eng.shard(k, 0)["p32"].cpu().numpy() for k in eng.by_key}
         dist.barrier()
@@ -60,15 +61,19 @@ def _rank_main(rank, world, port, q, placement="hbm"):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("placement", ["hbm", "params_host", "all_host"])
-def test_two_processes_match_local_comm(placement):
+@pytest.mark.parametrize("placement,graph", [("hbm", False), ("params_host", False),
+                                             ("all_host", False), ("hbm", True),
+                                             ("params_host", True)])
+def test_two_processes_match_local_comm(placement, graph):
+    """graph=True: each rank captures its step (P2P gathers, barriers with device-side
+    epochs, RS + Adam over peer buckets) in a CUDA graph and replays it."""
     from paper_2104_07857_b200 import gpt as eg
     from paper_2104_07857_b200.comm import LocalComm
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, placement))
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, placement, graph))
              for r in range(world)]
     for p in procs:
         p.start()
