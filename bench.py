@@ -717,9 +717,15 @@ def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
     steps = max(2, min(args.steps, 3))
     res = {}
     H, D = TierKind.HOST, TierKind.DEVICE
+    # params on the host: the reuse cache config 5 can afford. Per GPU at config 5 (70B,
+    # N=8, 4 x 1024 tokens) ~99 GB of activations and ~10 GB of rings leave ~70 GB of
+    # the 180 GB for ~40 of the 87 gathered 1.61 GB layers (46 %); the same share of the
+    # 1.3B model's 24 blocks is 11.
+    cache = int(round(0.46 * cfg.nl)) if params_host else 0
     for name, pl in (("hbm", eg.Placement(D, D)),
                      ("offload", eg.Placement(H if params_host else D, H))):
-        eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, placement=pl)
+        eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, placement=pl,
+                               param_cache=cache if name == "offload" else 0)
         for w in range(2):
             eng.step([bs[w % 2]])
         torch.cuda.synchronize()
@@ -760,6 +766,7 @@ def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
             "ms_per_step_offload": round(res["offload"]["ms"], 2),
             "tflops_offload": round(fl / (res["offload"]["ms"] / 1e3) / 1e12, 1),
             "host_bytes_per_step": int(moved),
+            "param_reuse_cache_blocks": cache,
             "transfer_ms_at_duplex_peak": round(t_xfer, 2),
             "exposed_ms": round(exposed, 2),
             "hidden_fraction": round(max(0.0, 1.0 - exposed / t_xfer), 4) if t_xfer > 0 else None,

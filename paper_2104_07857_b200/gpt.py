@@ -167,7 +167,7 @@ class GPTZeroEngine:
                  overlap_opt: bool | None = None, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
                  offload_slots: int | None = None, nvme_direct: bool = False,
-                 fwd_state_prefetch_every: int = 2):
+                 fwd_state_prefetch_every: int = 2, param_cache: int = 0):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -195,6 +195,11 @@ class GPTZeroEngine:
         # params on the host: one optimizer-state chunk H2D per this many forward
         # blocks, queued behind their parameter fetches (0: all after the forward)
         self.fwd_state_prefetch_every = fwd_state_prefetch_every
+        # reuse distance (ZeRO-3's max_reuse_distance): the forward's last `param_cache`
+        # blocks stay gathered in their own HBM slots, and the backward, which starts with
+        # them, does not fetch them again (with params on the host: that many fewer
+        # parameter H2Ds per step; with peers: fewer NVLink gathers)
+        self.param_cache = max(0, int(param_cache))
         # RS + Adam on a side stream, overlapped with the next bucket's backward GEMMs:
         # pays with peers (the RS reads them over NVLink) or host transfers in flight;
         # at N=1 in HBM it measured equal to running them in order (69.4-69.7 ms,
@@ -369,11 +374,15 @@ class GPTZeroEngine:
         e = self.by_key["embed"]
         # gathered-parameter slots: a 2-slot ring for blocks/final + a resident embed slot
         self.zero_copy = self.N == 1 and self.placement.params is TierKind.DEVICE and self.cdt == self.half
-        if not self.zero_copy:
-            self.slots = [torch.empty(maxn, dtype=self.half, device=self.dev) for _ in range(2)]
+        nb = len(self.buckets) - 2
+        self.K = min(self.param_cache, max(0, nb - 1)) if not self.zero_copy else 0
+        if not self.zero_copy:   # 2-slot ring + K reuse-cache slots
+            self.slots = [torch.empty(maxn, dtype=self.half, device=self.dev)
+                          for _ in range(2 + self.K)]
             self.embed_slot = torch.empty(e.shard * self.N, dtype=self.half, device=self.dev)
         if self.cdt != self.half:
-            self.wide_slots = [torch.empty(maxn, dtype=self.cdt, device=self.dev) for _ in range(2)]
+            self.wide_slots = [torch.empty(maxn, dtype=self.cdt, device=self.dev)
+                               for _ in range(2 + getattr(self, "K", 0))]
             self.wide_embed = torch.empty(e.shard * self.N, dtype=self.cdt, device=self.dev)
         self.slot_ready = [None, None]
         # gradient contribution buckets: per local rank, 2-slot ring + embed slot
@@ -571,6 +580,16 @@ class GPTZeroEngine:
             ev = torch.cuda.Event()
             ev.record(stream)
         self.events[(b.key, slot)] = ev
+
+    def _pslot(self, i: int, nb: int) -> int:
+        """Gathered-parameter slot of block i (i == nb: the head bucket): the last K
+        blocks own reuse-cache slots 2.., the others alternate in the 2-slot ring; the
+        head takes the ring slot the block before it (or the first cached block) would
+        have used, which never holds a block the backward still needs."""
+        K = self.K
+        if K and i < nb and i >= nb - K:
+            return 2 + i - (nb - K)
+        return (nb - K) % 2 if (K and i == nb) else i % 2
 
     def _full(self, b: Bucket, slot: int) -> torch.Tensor:
         """The gathered (compute-dtype) flat bucket, after waiting for its fetch."""
@@ -1132,12 +1151,12 @@ class GPTZeroEngine:
         self._tspan(E.op, "compute", c0, self._tmark(cur))
         caches = [[None] * len(blocks) for _ in range(nloc)]
         ev_every, fq = self.fwd_state_prefetch_every, 0
+        nb = len(blocks)
         for i, b in enumerate(blocks):
-            slot = i % 2
-            full = self._full(b, slot)
+            full = self._full(b, self._pslot(i, nb))
             if i + 1 < len(blocks):
-                gs.wait_stream(cur)  # slot (i+1)%2 was last read by compute of block i-1
-                self._fetch(blocks[i + 1], (i + 1) % 2, gs)
+                gs.wait_stream(cur)  # ring slot (i+1)%2 was last read by compute of block i-1
+                self._fetch(blocks[i + 1], self._pslot(i + 1, nb), gs)
                 if (self.offload and host_params and ev_every and i % ev_every == ev_every - 1
                         and fq < len(self.stage) - 1):   # slots this step has not claimed
                     # the H2D lane has slack while the forward computes: queue one
@@ -1150,7 +1169,7 @@ class GPTZeroEngine:
             else:
                 gs.wait_stream(cur)
                 self._phase = "backward"     # the head is the first backward op
-                self._fetch(FB, (i + 1) % 2, gs)
+                self._fetch(FB, self._pslot(nb, nb), gs)
                 if self.offload and host_params:
                     # with params on the host the forward's H2D lane carries their fetches;
                     # the state prefetch starts behind the last of them
@@ -1164,11 +1183,11 @@ class GPTZeroEngine:
                 if self.act_ckpt is not None:   # keep only the block input (checkpoint)
                     caches[li][i] = self._ckpt_save(li, i, x_in)
             self._tspan(b.op, "compute", c0, self._tmark(cur))
-        fslot = len(blocks) % 2
+        fslot = len(blocks) % 2                 # the head's gradient slot
         self._phase = "backward"
         if not blocks:
             self._fetch(FB, 0, gs)
-        PF = self._params(FB, self._full(FB, fslot))
+        PF = self._params(FB, self._full(FB, self._pslot(nb, nb) if blocks else 0))
         # ---- head (forward + backward fused; its bucket reduces first)
         losses = []
         GF = []
@@ -1182,16 +1201,15 @@ class GPTZeroEngine:
         self._tspan(FB.op, "compute", c0, self._tmark(cur))
         self._reduce_update(FB, fslot, consts)
         # ---- backward through the blocks, re-gathering each one
-        nb = len(blocks)
-        # blocks[-1] is still in slot (nb-1)%2 from the forward (the head used the other
-        # slot), so the backward starts on it without a second fetch
+        # blocks[-1] is still in its slot from the forward (the head used another), and
+        # so are the reuse-cached blocks: the backward fetches only blocks[: nb - 1 - K]
         for j in range(nb - 1, -1, -1):
             b = blocks[j]
-            slot = j % 2
-            full = self._full(b, slot)
-            if j - 1 >= 0:
+            slot = j % 2                           # gradient slot
+            full = self._full(b, self._pslot(j, nb))
+            if j - 1 >= 0 and j - 1 < nb - 1 - self.K:
                 gs.wait_stream(cur)
-                self._fetch(blocks[j - 1], (j - 1) % 2, gs)
+                self._fetch(blocks[j - 1], self._pslot(j - 1, nb), gs)
             P = self._params(b, full)
             self._wait_gslot(slot)
             if self.act_ckpt == "host" and j - 1 >= 0:

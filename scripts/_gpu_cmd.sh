@@ -1,2 +1,4 @@
 make -j8 >/dev/null 2>&1
-ZINF_BENCH_SAME_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 4 --steps 3 --warmup 3 --no-cpu --no-offload 2>&1 | grep -v Warning | tail -1 > gpurun_out/bench_4rank_graph.json; echo rc $?; cut -c1-600 gpurun_out/bench_4rank_graph.json
+timeout 900 python -m pytest tests/test_gpt_gpu.py tests/test_multiproc_gpu.py -m gpu -q 2>&1 | tail -3
+for i in 1 2; do timeout 600 python scripts/offload_equiv.py --batch 32 --params-host 2>/dev/null | tail -1 | python -c "
+import json,sys;d=json.loads(sys.stdin.read());print({k:d[k] for k in ('ms_per_step_hbm','ms_per_step_offload','hidden_fraction','host_bytes_per_step','transfer_ms_at_duplex_peak','param_reuse_cache_blocks')})"; done

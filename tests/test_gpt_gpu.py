@@ -294,3 +294,33 @@ def test_offload_graphed_matches_eager(params_host):
         for r in range(2):
             sa, sb = a.shard(key, r), b.shard(key, r)
             torch.testing.assert_close(sa["p32"].cpu(), sb["p32"].cpu(), rtol=0, atol=5e-5)
+
+
+@pytest.mark.parametrize("K,params_host,graph", [(1, False, False), (2, True, False),
+                                                 (99, True, False), (2, True, True)])
+def test_param_reuse_cache_matches(K, params_host, graph):
+    """param_cache=K keeps the forward's last K blocks gathered for the backward: same
+    training as K=0 (K=99 clamps to every block but the first), and K fewer parameter
+    fetches per step (host bytes with params on the host)."""
+    from paper_2104_07857_b200.gpt import Placement
+    from paper_2104_07857_b200.store import TierKind
+    pl = Placement(params=TierKind.HOST if params_host else TierKind.DEVICE,
+                   optim=TierKind.HOST if params_host else TierKind.DEVICE)
+    cfg = eg.GPTConfig(nl=5, hd=128, heads=2, seq=64, vocab=256, batch=2)
+    kw = dict(lr=1e-3, placement=pl, offload_chunk=10_007, gemm_select="cublas")
+    a = eg.GPTZeroEngine(cfg, LocalComm(2), **kw)
+    b = eg.GPTZeroEngine(cfg, LocalComm(2), param_cache=K, **kw)
+    assert b.K == min(K, cfg.nl - 1) and len(b.slots) == 2 + b.K
+    for step in range(3):
+        bs = batches_for(cfg, 2, step)
+        la = a.step(bs).item()
+        lb = (b.step_graphed if graph else b.step)(bs).item()
+        assert abs(la - lb) <= 1e-5 * abs(la), (step, la, lb)
+    torch.cuda.synchronize()
+    for key in a.by_key:
+        for r in range(2):
+            torch.testing.assert_close(a.shard(key, r)["p32"].cpu(), b.shard(key, r)["p32"].cpu(),
+                                       rtol=0, atol=5e-5)
+    if params_host and not graph:
+        blk = a.buckets[1].shard * 2 * 2                 # one block's bf16 shards, 2 ranks
+        assert a.fetch_bytes - b.fetch_bytes == 3 * b.K * blk

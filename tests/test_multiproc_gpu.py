@@ -34,7 +34,7 @@ def _placement(name):
     return {"hbm": Placement(D, D), "params_host": Placement(H, D), "all_host": Placement(H, H)}[name]
 
 
-def _rank_main(rank, world, port, q, placement="hbm", graph=False):
+def _rank_main(rank, world, port, q, placement="hbm", graph=False, cache=0):
     try:
         import torch.distributed as dist
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -45,7 +45,7 @@ def _rank_main(rank, world, port, q, placement="hbm", graph=False):
         c = eg.GPTConfig(nl=2, hd=128, heads=2, seq=64, vocab=256, batch=2)
         comm = DistComm()
         eng = eg.GPTZeroEngine(c, comm, lr=1e-3, placement=_placement(placement),
-                               offload_chunk=20_000)
+                               offload_chunk=20_000, param_cache=cache)
         losses = []
         run = eng.step_graphed if graph else eng.step
         for step in range(2):
@@ -61,10 +61,11 @@ def _rank_main(rank, world, port, q, placement="hbm", graph=False):
         q.put((rank, "error", traceback.format_exc()))
 
 
-@pytest.mark.parametrize("placement,graph", [("hbm", False), ("params_host", False),
-                                             ("all_host", False), ("hbm", True),
-                                             ("params_host", True)])
-def test_two_processes_match_local_comm(placement, graph):
+@pytest.mark.parametrize("placement,graph,cache", [("hbm", False, 0), ("params_host", False, 0),
+                                                   ("all_host", False, 0), ("hbm", True, 0),
+                                                   ("params_host", True, 0),
+                                                   ("params_host", False, 1)])
+def test_two_processes_match_local_comm(placement, graph, cache):
     """graph=True: each rank captures its step (P2P gathers, barriers with device-side
     epochs, RS + Adam over peer buckets) in a CUDA graph and replays it."""
     from paper_2104_07857_b200 import gpt as eg
@@ -73,7 +74,7 @@ def test_two_processes_match_local_comm(placement, graph):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, placement, graph))
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, placement, graph, cache))
              for r in range(world)]
     for p in procs:
         p.start()
