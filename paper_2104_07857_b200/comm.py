@@ -79,6 +79,9 @@ class LocalComm:
     def barrier(self, stream=None) -> None:  # all ranks share one stream order
         return None
 
+    def host_barrier(self) -> None:
+        return None
+
     def allreduce_max(self, x: float) -> float:
         return x
 
@@ -210,6 +213,10 @@ class DistComm:
             self._chan[channel] = (flags, self.window(flags))
         s = stream if stream is not None else torch.cuda.current_stream()
         _lib.call("zi_ctx_barrier", self.ctx, self._chan[channel][1], s.cuda_stream)
+
+    def host_barrier(self) -> None:
+        """Every rank's host reached this point (torch.distributed barrier)."""
+        dist.barrier(group=self.group)
 
     def barrier(self, stream=None) -> None:
         if self.backend == "nccl":

@@ -1290,11 +1290,16 @@ class GPTZeroEngine:
             for _ in range(2):
                 self.step(self._static)
             torch.cuda.synchronize()
+            multi = not self.comm.is_local and self.N > 1
+            if multi:   # peers finished reading our buffers before we restore them ...
+                self.comm.host_barrier()
             for s, c in zip(state, snap):
                 s.copy_(c)
             del snap
             self.t -= 2
             torch.cuda.synchronize()
+            if multi:   # ... and every rank restored before anyone replays (P2P reads)
+                self.comm.host_barrier()
             g = torch.cuda.CUDAGraph()
             l0, t0 = self.launches, self.t
             with torch.cuda.graph(g):
