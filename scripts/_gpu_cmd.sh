@@ -1,3 +1,5 @@
 make -j8 >/dev/null 2>&1
-for i in 1 2; do timeout 900 python -m pytest tests/test_multiproc_gpu.py -m gpu -q 2>&1 | tail -1; done
-timeout 900 python -m pytest tests/test_gpt_gpu.py -m gpu -q 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests $?; tail -1 gpurun_out/gpu_tests.log
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench $?
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2>&1; echo ref $?; tail -c 300 gpurun_out/bench_ref.json
