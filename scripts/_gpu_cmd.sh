@@ -1,5 +1,8 @@
 make -j8 >/dev/null 2>&1
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests $?; tail -1 gpurun_out/gpu_tests.log
-timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err; echo bench $?
-timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2>&1; echo ref $?; tail -c 300 gpurun_out/bench_ref.json
+L=paper_2104_07857_b200/libzinf.so
+cp $L /tmp/new.so
+echo EW8; timeout 300 python scripts/bench_gemm_adam.py 2>&1 | tail -1
+cp build_ab/lib_ew16.so $L
+timeout 600 python -m pytest tests/test_gemm_gpu.py -m gpu -q -k gemm_adam 2>&1 | tail -1
+echo EW16; timeout 300 python scripts/bench_gemm_adam.py 2>&1 | tail -5
+cp /tmp/new.so $L
