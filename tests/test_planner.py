@@ -1,0 +1,119 @@
+"""Placement planner (CPU): the SPEC placement-planner / efficiency examples and
+invariants (PAPER Fig. 9, §6.1, Table 3, Table 4), on the DGX-2 default profile, and the
+B200 profile's answers for the BASELINE configs."""
+
+import math
+
+import pytest
+
+from paper_2104_07857_b200 import planner as P
+
+S = P.Strategy
+
+
+def test_effective_param_bandwidth_examples():
+    c = P.dgx2()
+    assert P.effective_param_bandwidth(c, P.Tier.HOST, False) == 12e9        # broadcast
+    assert P.effective_param_bandwidth(P.dgx2(64), P.Tier.HOST, False) == 12e9
+    assert P.effective_param_bandwidth(c, P.Tier.HOST, True) == 48e9
+    assert P.effective_param_bandwidth(c, P.Tier.NVME, True) == 25e9
+    c64 = P.dgx2(64)
+    assert P.effective_param_bandwidth(c64, P.Tier.HOST, True) >= 3e12
+    assert P.effective_param_bandwidth(c64, P.Tier.NVME, True) >= 1.5e12
+    prev = 0
+    for n in (1, 2, 4, 8, 16, 64):        # allgather nondecreasing in nodes, > broadcast
+        bw = P.effective_param_bandwidth(P.dgx2(n), P.Tier.HOST, True)
+        assert bw >= prev and bw > 12e9
+        prev = bw
+
+
+@pytest.mark.parametrize("st,paper,tol", [(S.DATA_PARALLEL, 1.4e9, 0.25), (S.ZERO2, 1.3e10, 0.35),
+                                          (S.ZERO_OFFLOAD, 1.3e10, 0.35),
+                                          (S.ZERO_INF_CPU, 1e11, 0.35),
+                                          (S.ZERO_INF_NVME, 1e12, 0.40)])
+def test_max_model_params_fig9(st, paper, tol):
+    got = P.max_model_params(P.dgx2(), st)
+    assert abs(got - paper) <= tol * paper, (st, got)
+
+
+def test_max_model_params_monotone():
+    c = P.dgx2()
+    sizes = [P.max_model_params(c, st) for st in S]
+    assert sizes == sorted(sizes)
+    bigger = P.ClusterConfig(device_mem_bytes=64e9, host_mem_bytes_per_node=3e12,
+                             nvme_bytes_per_node=56e12)
+    for st in S:
+        assert P.max_model_params(bigger, st) >= P.max_model_params(c, st)
+
+
+def test_feasibility_examples():
+    c = P.dgx2()
+    t1 = P.ModelShape(nl=128, hd=25600)                 # ~1.0e12 params (Table 1, 1 node)
+    fits = [r.strategy for r in (P.feasibility(t1, c, st) for st in S) if r.fits]
+    assert fits == [S.ZERO_INF_NVME]
+    ten = P.ModelShape(nl=50, hd=4096)                  # ~1.0e10
+    rep = {st: P.feasibility(ten, c, st) for st in S}
+    assert not rep[S.DATA_PARALLEL].fits
+    for st in (S.ZERO_OFFLOAD, S.ZERO3, S.ZERO_INF_CPU, S.ZERO_INF_NVME):
+        assert rep[st].fits, st
+    # SPEC lists Zero2 as fitting 10B too, but its own Zero2 rate (2 + 18/N B/param) plus
+    # the 2 GB reserve it fixes needs 34.0 GB of a 32 GB device: within 7 % of capacity
+    z2 = rep[S.ZERO2]
+    assert z2.binding_constraint == "device" and z2.demand["device"] < 1.07 * 32e9
+    wide = P.ModelShape(nl=4, hd=65536)                 # MSWM 68.7 GB > 32 GB
+    assert not P.feasibility(wide, c, S.ZERO_INF_NVME).working_memory_ok
+    assert P.feasibility(wide, c, S.ZERO_INF_NVME, tiling=4).working_memory_ok
+    for st in S:                                        # fits <=> demands <= capacity and WM ok
+        r = P.feasibility(ten, c, st)
+        assert r.fits == (all(r.demand[k] <= r.capacity[k] for k in r.demand)
+                          and r.working_memory_ok)
+
+
+def test_recommend_ranks_total_and_deterministic():
+    c = P.dgx2()
+    r1 = P.recommend(P.ModelShape(nl=128, hd=25600), c)
+    assert r1[0].strategy is S.ZERO_INF_NVME and [r.fits for r in r1].count(True) == 1
+    r2 = P.recommend(P.ModelShape(nl=4096, hd=65536), c)   # infeasible everywhere
+    assert not any(r.fits for r in r2) and len(r2) == len(S)
+    assert [r.strategy for r in P.recommend(P.ModelShape(nl=2, hd=256), c)] == \
+        [r.strategy for r in P.recommend(P.ModelShape(nl=2, hd=256), c)]
+
+
+def test_efficiency_examples_and_future_table():
+    assert abs(P.efficiency(1024, 70e9, 70e12) - 0.5059) < 1e-4
+    assert P.efficiency(5, 0, 70e12) == 0
+    assert abs(P.efficiency(49152, 2e9, 70e12) - 0.584) < 1e-3
+    assert abs(P.required_bandwidth(512, 70e12, 0.9) - 1.2305e12) < 1e8
+    assert abs(P.required_bandwidth(1024, 70e12, 0.5) - 68.36e9) < 1e7
+    assert abs(P.required_bandwidth(196608, 70e12, 0.5) - 0.356e9) < 1e6
+    s = P.ModelShape(nl=1, hd=2048, seq=1024, bsz=2)
+    assert P.ait(P.AitKind.OPTIMIZER_STATES, s) == 512
+    assert P.ait(P.AitKind.PARAM_GRAD, P.ModelShape(nl=1, hd=1)) == 1024
+    assert P.ait(P.AitKind.ACTIVATION_CKPT, P.ModelShape(nl=1, hd=2048)) == 49152
+    rows = P.future_hardware_table(P.dgx2(32))          # 512 V100s
+    r1 = rows[0]
+    assert abs(r1["slow_memory_aggregate"] - 1.5e12) <= 0.25 * 1.5e12
+    assert abs(r1["slow_memory_per_device"] - 3e9) <= 0.25 * 3e9
+    assert abs(r1["device_device"] - 70e9) <= 0.25 * 70e9
+    for k, r in zip((10, 100), rows[1:]):
+        for key in ("slow_memory_per_device", "slow_memory_aggregate", "device_device"):
+            assert math.isclose(r[key], k * r1[key], rel_tol=1e-12)
+
+
+def test_b200_profile_places_the_baseline_configs():
+    """BASELINE configs on 8 x B200: 1.3B and 10B fit all-in-HBM ZeRO-3; 70B needs a host
+    tier for its optimizer states (config 5 runs params + optimizer offloaded); one node
+    holds far more than 70B with ZeRO-Infinity."""
+    c = P.b200()
+    cfg2 = P.ModelShape(nl=24, hd=2048, attn_heads=16, bsz=8)
+    cfg3 = P.ModelShape(nl=50, hd=4096, attn_heads=32, bsz=8)
+    cfg5 = P.ModelShape(nl=87, hd=8192, attn_heads=64, bsz=4)
+    assert P.feasibility(cfg2, c, S.ZERO3).fits and P.feasibility(cfg3, c, S.ZERO3).fits
+    assert not P.feasibility(cfg5, c, S.ZERO3).fits
+    assert P.feasibility(cfg5, c, S.ZERO_INF_CPU).fits
+    assert P.max_model_params(c, S.ZERO_INF_NVME) > 1e12
+    assert P.ClusterConfig.from_flat({"nodes": 1, "devices_per_node": 8, "device_mem": 180e9,
+                                      "host_mem_per_node": 2e12, "nvme_per_node": 30e12,
+                                      "pcie_bw": 55.6e9, "host_bw_per_node": 444.8e9,
+                                      "nvme_bw_per_node": 50e9, "d2d_bw": 900e9,
+                                      "peak_tp": 1386e12}).world_size == 8
