@@ -184,12 +184,46 @@ def cmd_train(argv=None) -> int:
     return EXIT_OK
 
 
+def cmd_plan(argv=None) -> int:
+    """Rank the placement strategies for a model on a cluster profile (planner.py)."""
+    from . import planner as P
+    ap = argparse.ArgumentParser(prog="zinf plan")
+    ap.add_argument("--profile", choices=["dgx2", "b200"], default="b200")
+    ap.add_argument("--nodes", type=int, default=1)
+    ap.add_argument("--nl", type=int, required=True)
+    ap.add_argument("--hd", type=int, required=True)
+    ap.add_argument("--heads", type=int, default=32)
+    ap.add_argument("--seq", type=int, default=1024)
+    ap.add_argument("--bsz", type=float, default=1.0)
+    ap.add_argument("--ci", type=int, default=1)
+    ap.add_argument("--tiling", type=int, default=1)
+    try:
+        a = ap.parse_args(argv)
+        shape = P.ModelShape(a.nl, a.hd, a.heads, a.seq, a.bsz, a.ci)
+        cluster = (P.b200 if a.profile == "b200" else P.dgx2)(a.nodes)
+    except SystemExit as e:
+        return EXIT_USAGE if e.code else EXIT_OK
+    except ValueError as e:
+        print(f"config error: {e}", file=sys.stderr)
+        return EXIT_USAGE
+    print(f"model {shape.params:.4g} params on {cluster.name} x {cluster.nodes} node(s), "
+          f"{cluster.world_size} devices")
+    print("strategy,fits,binding,device_GB,host_GB_per_node,nvme_GB_per_node,pred_eff")
+    for r in P.recommend(shape, cluster, a.tiling):
+        d = r.demand
+        print(f"{r.strategy.value},{int(r.fits)},{r.binding_constraint},{d['device'] / 1e9:.2f},"
+              f"{d['host'] / 1e9:.2f},{d['nvme'] / 1e9:.2f},{r.predicted_efficiency:.4f}")
+    return EXIT_OK
+
+
 def main(argv=None) -> int:
     argv = list(sys.argv[1:] if argv is None else argv)
+    if argv and argv[0] == "plan":
+        return cmd_plan(argv[1:])
     if not argv or argv[0] != "train":
-        print("usage: python -m paper_2104_07857_b200.cli train --model CFG [options]\n"
-              "(plan / sweep / simulate are analytic SPEC modules outside this build's hot path)",
-              file=sys.stderr)
+        print("usage: python -m paper_2104_07857_b200.cli {train --model CFG | plan --nl N --hd H}"
+              " [options]\n(sweep / simulate are analytic SPEC modules outside this build's hot"
+              " path)", file=sys.stderr)
         return EXIT_USAGE
     return cmd_train(argv[1:])
 

@@ -117,3 +117,10 @@ def test_b200_profile_places_the_baseline_configs():
                                       "pcie_bw": 55.6e9, "host_bw_per_node": 444.8e9,
                                       "nvme_bw_per_node": 50e9, "d2d_bw": 900e9,
                                       "peak_tp": 1386e12}).world_size == 8
+
+
+def test_cli_plan(capsys):
+    from paper_2104_07857_b200 import cli
+    assert cli.main(["plan", "--profile", "dgx2", "--nl", "128", "--hd", "25600"]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[1].startswith("strategy,fits") and out[2].startswith("ZeroInfNvme,1,")
