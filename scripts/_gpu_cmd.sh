@@ -1,3 +1,3 @@
 make -j8 >/dev/null 2>&1
-timeout 600 python -m pytest tests/test_gemm_gpu.py -m gpu -q -k gemm_adam 2>&1 | tail -2
-timeout 300 python scripts/bench_gemm_adam.py 2>&1 | tail -5
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests $?; tail -1 gpurun_out/gpu_tests.log
