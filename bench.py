@@ -436,8 +436,14 @@ def run_ours(args):
         e2e_ms = comm.allreduce_max(e2e_ms)
     e2e_tflops = flops * world / (e2e_ms / args.steps / 1e3) / 1e12
 
-    # ---------------- collectives over NVLink (N > 1): bus GB/s of the step's AG / RS
+    # ---------------- collectives over NVLink (N > 1): bus GB/s of the step's AG / RS;
+    # at N=1 the same kernels over 8 simulated ranks' buffers in this GPU's HBM
     collectives = None
+    if world == 1:
+        try:
+            collectives = local_collective_kernels(eng)
+        except Exception as e:  # noqa: BLE001 — report, never lose the main line
+            collectives = {"error": repr(e)[:300]}
     if world > 1:
         try:
             collectives = collective_leg(eng, comm)
@@ -513,6 +519,54 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def local_collective_kernels(eng, ranks: int = 8, iters: int = 10) -> dict:
+    """N=1: the step's gather and reduce-scatter kernels over `ranks` simulated ranks' buffers
+    of one 1.3B block bucket in this GPU's HBM (shards / gradient buckets at distinct
+    addresses, as the IPC-mapped peers would be). Not NVLink numbers: HBM GB/s of the
+    kernels themselves (gather: shard bytes read + full bytes written; RS: every rank's
+    bf16 bucket read over our shard + the fp32 shard written), against the copy peak."""
+    import torch
+    from paper_2104_07857_b200 import kernels as K
+    b = eng.by_key["h0"]
+    n = b.numel
+    L = -(-n // ranks)
+    shards = [torch.randint(-3000, 3000, (L,), dtype=torch.int16, device="cuda").view(torch.bfloat16)
+              for _ in range(ranks)]
+    full = torch.empty(L * ranks, dtype=torch.bfloat16, device="cuda")
+    grads = [torch.randn(n, device="cuda").bfloat16() for _ in range(ranks)]
+    out = torch.empty(L, dtype=torch.float32, device="cuda")
+    hbm, _, _ = _peaks()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / iters
+
+    res = {"what": f"{ranks} simulated ranks in one GPU's HBM (not NVLink): kernel GB/s",
+           "bucket_elems": n}
+    ag_bytes = 2 * 2 * n
+    for name, ce in (("allgather_sm", False), ("allgather_ce", True)):
+        ms = timed(lambda: K.allgather(shards, L, full, n, use_copy_engine=ce))
+        res[f"{name}_ms"] = round(ms, 4)
+        res[f"{name}_gbs"] = round(ag_bytes / (ms / 1e3) / 1e9, 1)
+    rs_bytes = ranks * 2 * L + 4 * L
+    # one rank's shard of the rank-order fold (each rank runs this for its own shard)
+    ms = timed(lambda: K.reduce_scatter_cast(grads, 3 * L, L, n, 1.0 / ranks, torch.bfloat16, out))
+    res["reduce_scatter_ms"] = round(ms, 4)
+    res["reduce_scatter_gbs"] = round(rs_bytes / (ms / 1e3) / 1e9, 1)
+    res["reduce_scatter_frac_of_hbm_peak"] = round(rs_bytes / (ms / 1e3) / 1e9 / hbm, 4)
+    res["allgather_sm_frac_of_hbm_peak"] = round(res["allgather_sm_gbs"] / hbm, 4)
+    del shards, full, grads, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def collective_leg(eng, comm, iters: int = 10) -> dict:
