@@ -1,3 +1,3 @@
 make -j8 >/dev/null 2>&1
-timeout 600 python bench.py --no-cpu --no-offload > gpurun_out/b.json 2>gpurun_out/b.err; python -c "
-import json;d=json.loads(open('gpurun_out/b.json').read().strip().splitlines()[-1]);print(d['value'], d['collectives'])"; tail -2 gpurun_out/b.err
+timeout 900 python bench.py > gpurun_out/bench_final2.json 2> gpurun_out/bench_final2.err; echo bench $?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_final.csv python scripts/profile_step.py --graph > /dev/null 2>&1; echo ncu $?
