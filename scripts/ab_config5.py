@@ -19,7 +19,8 @@ H = TierKind.HOST
 for v in (sys.argv[1:] or ["0:12", "3:12", "2:12", "3:16"]):
     k, ns = (int(x) for x in v.split(":"))
     eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, placement=eg.Placement(H, H),
-                           offload_slots=ns, fwd_state_prefetch_every=k)
+                           offload_slots=ns, fwd_state_prefetch_every=k,
+                           param_cache=int(os.environ.get("CACHE", 0)))
     for w in range(2):
         eng.step([bs[w % 2]])
     torch.cuda.synchronize()
