@@ -1,2 +1,2 @@
 make -j8 >/dev/null 2>&1
-CACHE=11 timeout 1200 python scripts/ab_config5.py 2:12 2:16 1:16 2:20 2:12 2>&1 | grep -v Warn | tail -6
+ZINF_BENCH_SAME_GPU=1 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 8 --steps 3 --warmup 3 --no-cpu --no-offload 2>&1 | grep -v Warning | grep "^{" | tail -1 > gpurun_out/bench_8rank_graph.json; echo rc $?; cut -c1-400 gpurun_out/bench_8rank_graph.json
