@@ -262,6 +262,13 @@ int zi_ctx_reduce_scatter_cast(zi_ctx* ctx, int win, size_t offset_bytes, size_t
 /* zi_barrier_dev over a window of `world` uint32 flags; the epoch is a device counter per
  * window, so the barrier may be captured in a CUDA graph and replayed. */
 int zi_ctx_barrier(zi_ctx* ctx, int flags_win, void* stream);
+/* Barrier with no SM held, over a flag window of 2*world uint32 (two slot sets). Arrive =
+ * cuStreamWriteValue32(1) into our slot of set `parity` in every peer's array (fenced
+ * after this stream's earlier writes); wait = cuStreamWaitValue32(== 1) on every peer's
+ * slot of our set in the stream front end, then reset it to 0. Consecutive barriers on
+ * one window alternate parity; comm.DistComm keeps that order, padding a captured CUDA
+ * graph to an even barrier count per window. */
+int zi_ctx_barrier_value(zi_ctx* ctx, int flags_win, int parity, void* stream);
 
 /* ---- memory-centric tiling ------------------------------
  * One tile of a tiled linear on the 5th-gen tensor cores (tcgen05 + TMEM,

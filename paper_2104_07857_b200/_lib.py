@@ -114,6 +114,7 @@ SIGNATURES = {
     "zi_ctx_reduce_scatter_cast": [c_void_p, c_int, c_size_t, c_size_t, c_size_t, c_float, c_int,
                                    c_void_p, c_void_p],
     "zi_ctx_barrier": [c_void_p, c_int, c_void_p],
+    "zi_ctx_barrier_value": [c_void_p, c_int, c_int, c_void_p],
     "zi_linear_fwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int,
                       c_int, c_void_p],
     "zi_gemm": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,

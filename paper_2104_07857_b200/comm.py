@@ -56,6 +56,9 @@ def _ipc_tensor(shape, dtype: torch.dtype) -> torch.Tensor:
     buf = _DeviceBuffer(nbytes)
     t = torch.as_tensor(buf, device="cuda")[:nbytes].view(dtype).view(*shape)
     t.zero_()
+    # zeroed before the IPC handle is published: a peer's first write (a barrier
+    # arrival) must never be erased by this zero_ landing late on our stream
+    torch.cuda.current_stream().synchronize()
     return t
 
 
@@ -105,6 +108,14 @@ class DistComm:
         self._owned: dict[int, int] = {}   # base pointer -> bytes of our shareable buffers
         self._ctx = None        # native zi_ctx (created on first peer-memory use: needs CUDA)
         self.windows: dict[int, int] = {}  # local pointer -> zi_ctx window id
+        self._staging: dict = {}  # (name, elems, dtype) -> (shared buffer, peer pointers)
+        # barrier flavour: "memop" (stream write / wait-value, no SM held; default) or
+        # "kernel" (zi_barrier spin kernel with a device-side epoch)
+        self.barrier_kind = os.environ.get("ZI_BARRIER", "memop")
+        if self.barrier_kind not in ("memop", "kernel"):
+            raise ValueError("ZI_BARRIER must be 'memop' or 'kernel'")
+        self._bar_count: dict[int, int] = {}   # channel -> barriers issued (value parity)
+        self._capture_mark: dict[int, int] | None = None
 
     @property
     def ctx(self) -> int:
@@ -197,6 +208,37 @@ class DistComm:
                   offset_elems * t.element_size(), n, shard_elems, scale, half_kind(t.dtype),
                   out.data_ptr(), s.cuda_stream)
 
+    def staging(self, name: str, elems: int, dtype: torch.dtype) -> tuple[torch.Tensor, list[int]]:
+        """A persistent shared window of ``elems`` (allocated and IPC-mapped once per name).
+
+        Collective on first use. The SPEC collectives over tier-store shards
+        (partition.allgather / reduce_scatter with a DistComm) copy the local
+        shard in, so one window per PartitionedTensor serves every call and
+        the zi_ctx window table does not grow per call.
+        """
+        k = (name, int(elems), dtype)
+        if k not in self._staging:
+            t = self.alloc((max(1, int(elems)),), dtype)
+            self._staging[k] = (t, self.share(t))
+        return self._staging[k]
+
+    def open_channels(self, channels=(0, 1, 2)) -> None:
+        """Create barrier channels eagerly (collective), then a host barrier, so no
+        channel's flag window is created lazily in the middle of a step on a
+        stream that is not ordered after its zeroing."""
+        if self.world == 1:
+            return
+        for ch in channels:
+            self._channel(ch)
+        self.host_barrier()
+
+    def _channel(self, channel: int):
+        if channel not in self._chan:   # collective on first use of the channel
+            flags = self.alloc((2 * self.world,), torch.int32)   # two slot sets
+            self.share(flags)
+            self._chan[channel] = (flags, self.window(flags))
+        return self._chan[channel]
+
     def device_barrier(self, stream=None, channel: int = 0) -> None:
         """zi_barrier over IPC flag words (orders P2P reads with peer writers).
 
@@ -207,12 +249,29 @@ class DistComm:
         """
         if self.world == 1:
             return
-        if channel not in self._chan:   # collective on first use of the channel
-            flags = self.alloc((self.world,), torch.int32)
-            self.share(flags)
-            self._chan[channel] = (flags, self.window(flags))
+        win = self._channel(channel)[1]
         s = stream if stream is not None else torch.cuda.current_stream()
-        _lib.call("zi_ctx_barrier", self.ctx, self._chan[channel][1], s.cuda_stream)
+        if self.barrier_kind == "kernel":
+            _lib.call("zi_ctx_barrier", self.ctx, win, s.cuda_stream)
+            return
+        n = self._bar_count.get(channel, 0)
+        self._bar_count[channel] = n + 1
+        _lib.call("zi_ctx_barrier_value", self.ctx, win, n % 2, s.cuda_stream)
+
+    def begin_capture(self) -> None:
+        """Mark the barrier counts before a CUDA-graph capture (see end_capture)."""
+        self._capture_mark = dict(self._bar_count)
+
+    def end_capture(self, stream=None) -> None:
+        """Before the capture ends: pad every channel whose captured barrier count is
+        odd with one more barrier, so each replay leaves the slot-set parity where it
+        found it and replays / eager calls keep alternating (zi_ctx_barrier_value)."""
+        mark, self._capture_mark = self._capture_mark or {}, None
+        if self.barrier_kind != "memop":
+            return
+        for ch, n in sorted(self._bar_count.items()):
+            if (n - mark.get(ch, 0)) % 2:
+                self.device_barrier(stream, channel=ch)
 
     def host_barrier(self) -> None:
         """Every rank's host reached this point (torch.distributed barrier)."""
@@ -231,3 +290,4 @@ class DistComm:
             self._ctx = None
             self.windows.clear()
             self._chan.clear()
+            self._staging.clear()

@@ -19,6 +19,9 @@
 //                                1/N scale, folded in rank order
 // Every call is asynchronous on the caller's stream; the context is guarded by a
 // mutex, so one context may be shared by the threads of a rank.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -59,6 +62,33 @@ int open_mapping(zi_ctx* c, const unsigned char* h, void** base) {
   c->mapped.push_back(m);
   *base = p;
   return ZI_OK;
+}
+
+// Stream memory operations (driver API, resolved once through the runtime's entry-point
+// query so libzinf needs no -lcuda): the barrier's writes and waits execute in the
+// stream's front end, so a waiting rank holds no SM (it cannot starve the persistent
+// tcgen05 GEMMs, or a peer context time-sharing the GPU).
+PFN_cuStreamWriteValue32_v11070 g_write32 = nullptr;
+PFN_cuStreamWaitValue32_v11070 g_wait32 = nullptr;
+
+int load_memops() {
+  static std::once_flag once;
+  static int st = ZI_OK;
+  std::call_once(once, [] {
+    void* w = nullptr;
+    void* t = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !t) {
+      st = ZI_ECUDA;
+      return;
+    }
+    g_write32 = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(w);
+    g_wait32 = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(t);
+  });
+  if (st != ZI_OK) zi::set_error("cuStreamWriteValue32 / cuStreamWaitValue32 unavailable");
+  return st;
 }
 
 }  // namespace
@@ -195,6 +225,47 @@ int zi_ctx_barrier(zi_ctx* c, int flags_win, void* stream) {
   // the epoch lives on the device (one counter per window): CUDA-graph replays of a
   // captured barrier advance it like eager calls do
   return zi_barrier_dev(f.data(), c->world, c->rank, c->epochs + flags_win, stream);
+}
+
+int zi_ctx_barrier_value(zi_ctx* c, int flags_win, int parity, void* stream) {
+  ZI_CHECK_ARG(c != nullptr, "zi_ctx_barrier_value: NULL ctx");
+  ZI_CHECK_ARG(parity == 0 || parity == 1, "zi_ctx_barrier_value: parity must be 0 or 1");
+  const int st = load_memops();
+  if (st != ZI_OK) return st;
+  std::vector<uint8_t*> f(c->world);
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    ZI_CHECK_ARG(flags_win >= 0 && flags_win < (int)c->windows.size(),
+                 "zi_ctx_barrier_value: bad window %d", flags_win);
+    for (int r = 0; r < c->world; ++r) f[r] = c->windows[flags_win].ptr[r];
+  }
+  CUstream s = reinterpret_cast<CUstream>(stream);
+  const size_t set = (size_t)parity * c->world * 4;   // this barrier's slot set
+  auto fail = [](const char* what, CUresult e) {
+    zi::set_error("%s failed (%d)", what, (int)e);
+    return ZI_ECUDA;
+  };
+  // arrive: 1 into our slot of every peer's set (the default write is preceded by a
+  // memory fence: this stream's earlier writes are visible to the peer first) ...
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    const CUresult e = g_write32(s, reinterpret_cast<CUdeviceptr>(f[r] + set + 4 * (size_t)c->rank),
+                                 1u, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (e != CUDA_SUCCESS) return fail("cuStreamWriteValue32", e);
+  }
+  // ... wait for every peer's arrival in our set, then reset it. A peer can run at most
+  // one barrier ahead (it needs our arrival to pass this one), and that barrier uses the
+  // other set; it writes this set again only after our next arrival, which is fenced
+  // behind these resets.
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    const CUdeviceptr slot = reinterpret_cast<CUdeviceptr>(f[c->rank] + set + 4 * (size_t)r);
+    CUresult e = g_wait32(s, slot, 1u, CU_STREAM_WAIT_VALUE_EQ);
+    if (e != CUDA_SUCCESS) return fail("cuStreamWaitValue32", e);
+    e = g_write32(s, slot, 0u, CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (e != CUDA_SUCCESS) return fail("cuStreamWriteValue32", e);
+  }
+  return ZI_OK;
 }
 
 }  // extern "C"

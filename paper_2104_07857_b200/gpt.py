@@ -236,6 +236,10 @@ class GPTZeroEngine:
         self.p16_stream = torch.cuda.Stream(self.dev)   # host params: bf16 write-back lane
         self.p16_ready = {}                              # bucket -> its bf16 write-back landed
         self._alloc_work()
+        if not self.comm.is_local and self.N > 1:
+            # every barrier channel the step uses (0: step start, 1: cg staging, 2: the
+            # optimizer stream) exists and is zeroed on every rank before the first step
+            self.comm.open_channels((0, 1, 2))
         self.launches = 0  # libzinf kernel launches issued by step()
         self.adam = kernels.DeviceAdamState(lr, betas, eps, device=self.dev)
         self._graph = None
@@ -1302,8 +1306,12 @@ class GPTZeroEngine:
                 self.comm.host_barrier()
             g = torch.cuda.CUDAGraph()
             l0, t0 = self.launches, self.t
+            if multi:
+                self.comm.begin_capture()
             with torch.cuda.graph(g):
                 self._static_loss = self.step(self._static)
+                if multi:   # every side stream joined cur: pad the barrier parity there
+                    self.comm.end_capture()
             self._graph = g
             self._launches_per_replay = self.launches - l0
             self.launches, self.t = l0, t0      # capture executes nothing

@@ -235,26 +235,41 @@ def train_step(model: PartitionedModel, batch, hyper: AdamHyper, store: TierStor
     rows = B // G
     norm = float(B * t.shape[1])
     nl = len(spec.layers)
+    dist_mode = model.comm is not None and not model.comm.is_local and N > 1
+    # data parallel: with one process per rank, rank r computes the G/N groups
+    # [r*G/N, (r+1)*G/N); the reduce-scatter folds every rank's groups rank-major,
+    # which is group order, so the result is the simulated model's bit for bit
+    groups = range(model.comm.rank * (G // N), (model.comm.rank + 1) * (G // N)) \
+        if dist_mode else range(G)
     # ---- forward: fetch -> compute -> release, per layer
-    acts = [[x[g * rows:(g + 1) * rows].float()] for g in range(G)]
-    zs = [[] for _ in range(G)]
+    acts = {g: [x[g * rows:(g + 1) * rows].float()] for g in groups}
+    zs = {g: [] for g in groups}
     for i in range(nl):
         fetched = {k: _gather_widen(model, k) for k in sorted(model.fetch_sets[i])}
         W, b = _layer_weights(model, i, fetched)
-        for g in range(G):
+        for g in groups:
             z = kernels.matmul_fixed(acts[g][-1], W.t(), bias=b)
             zs[g].append(z)
             acts[g].append(_act_fwd(spec.layers[i].act, z))
         del fetched, W, b  # release
     losses = []
-    grads_out = []
-    for g in range(G):
+    grads_out = {}
+    for g in groups:
         d = acts[g][-1] - t[g * rows:(g + 1) * rows].float()
         losses.append((d * d).sum() / norm)
-        grads_out.append(2.0 * d / norm)
-    loss = losses[0]
-    for l in losses[1:]:
-        loss = loss + l
+        grads_out[g] = 2.0 * d / norm
+    if dist_mode:   # every group's loss, folded in group order in fp32 as below
+        import numpy as np
+        vals = [v for part in model.comm.all_gather_object([float(l.item()) for l in losses])
+                for v in part]
+        acc32 = np.float32(vals[0])
+        for v in vals[1:]:
+            acc32 = np.float32(acc32 + np.float32(v))
+        loss = torch.tensor(float(acc32))
+    else:
+        loss = losses[0]
+        for l in losses[1:]:
+            loss = loss + l
     # ---- backward: re-gather, per-group grads, reduce + offload when a bucket completes
     last_use = {}
     for i in range(nl):
@@ -265,7 +280,7 @@ def train_step(model: PartitionedModel, batch, hyper: AdamHyper, store: TierStor
         L = spec.layers[i]
         fetched = {k: _gather_widen(model, k) for k in sorted(model.fetch_sets[i])}
         W, _ = _layer_weights(model, i, fetched)
-        for g in range(G):
+        for g in groups:
             dz = _act_bwd(L.act, zs[g][i], grads_out[g])
             dW = kernels.matmul_fixed(dz.t(), acts[g][i])
             db = dz.sum(0)
@@ -276,7 +291,7 @@ def train_step(model: PartitionedModel, batch, hyper: AdamHyper, store: TierStor
         del fetched, W
         for key, _, _ in own_buckets(spec)[i]:
             if last_use[key] == i:
-                _reduce_offload(model, key, [acc.pop((key, g)) for g in range(G)], store)
+                _reduce_offload(model, key, [acc.pop((key, g)) for g in groups], store)
     chunked_adam_step(model, hyper, chunk_elems, store)
     return float(loss.item())
 
@@ -289,8 +304,12 @@ def _reduce_offload(model: PartitionedModel, key: str, group_grads, store: TierS
         h = torch.empty(gg.numel(), dtype=model.half, device=gg.device)
         kernels.cast_f32_to_half(gg.contiguous(), h)
         contribs.append(h)
-    ranks = range(model.world) if (model.comm is None or model.comm.is_local) else [model.comm.rank]
-    shards = reduce_scatter(contribs, pt.world_size, ranks=ranks)
+    local = model.comm is None or model.comm.is_local
+    ranks = range(model.world) if local else [model.comm.rank]
+    # simulated ranks: every group is local; DistComm: this rank's groups, folded with
+    # the peers' over NVLink (partition.reduce_scatter's shared window)
+    shards = reduce_scatter(contribs, pt.world_size, comm=None if local else model.comm,
+                            ranks=ranks)
     tickets = [store.write(f"{key}.g32/rank{r}", s, model.placement.grad_tier)
                for r, s in zip(ranks, shards)]
     store.flush(tickets)
@@ -352,11 +371,14 @@ def digest(model: PartitionedModel) -> str:
 
 def run_training(spec: ModelSpec, world: int, placement: HarnessPlacement | None, steps: int,
                  seed: int | None, store: TierStore, batch: int = 16, lr: float = 1e-2,
-                 half: torch.dtype = torch.float16, chunk_elems: int = 1 << 20):
-    """returns (digest, loss history)."""
+                 half: torch.dtype = torch.float16, chunk_elems: int = 1 << 20, comm=None):
+    """returns (digest, loss history).
+
+    With a DistComm (one process per rank) each process passes its own store;
+    the digest is identical on every rank and to the simulated run's."""
     if seed is not None:
         spec = ModelSpec(spec.layers, spec.tied_pairs, seed)
-    model = init_partitioned(spec, world, store, placement, half)
+    model = init_partitioned(spec, world, store, placement, half, comm=comm)
     x, t = synthetic_batch(spec, batch, store.device)
     hyper = AdamHyper(lr=lr)
     losses = [train_step(model, (x, t), hyper, store, chunk_elems) for _ in range(steps)]

@@ -33,6 +33,8 @@ from .store import TierKind, TierStore, _as_tensor
 _DT = {torch.float32: _lib.DT_F32, torch.float16: _lib.DT_F16, torch.float64: _lib.DT_F64,
        torch.bfloat16: _lib.DT_BF16}
 _auto_key = itertools.count()
+# barrier channel of the SPEC collectives over a DistComm (the GPT engine uses 0-2)
+PARTITION_CHANNEL = 3
 
 
 def shard_len(full_len: int, world_size: int) -> int:
@@ -136,17 +138,23 @@ def allgather(pt: PartitionedTensor, store: TierStore, comm=None, out: torch.Ten
                           use_copy_engine=use_copy_engine or pt.tier is not TierKind.DEVICE)
         return out
     mine = _device_shard(pt, store, comm.rank)
-    if not mine.is_cuda:
-        mine = mine.to(store.device, non_blocking=True)
     if method == "nccl":
+        if not mine.is_cuda:
+            mine = mine.to(store.device, non_blocking=True)
         padded = torch.empty(L * pt.world_size, dtype=pt.dtype, device=store.device)
         dist.all_gather_into_tensor(padded, mine, group=comm.group)
         out[: pt.full_len].copy_(padded[: pt.full_len])
         return out
-    ptrs = comm.share(mine)
-    comm.device_barrier()
-    kernels.allgather(ptrs, L, out, pt.full_len, use_copy_engine=use_copy_engine)
-    comm.device_barrier()
+    if method != "p2p":
+        raise ValueError("method must be 'p2p' or 'nccl'")
+    # one persistent shared window per PartitionedTensor: our shard is staged into it
+    # (an H2D for host / NVMe tiers: the cg step), then every rank's window is read
+    # over NVLink (the gg step) by the SM gather kernel or the copy engines
+    stage, _ = comm.staging(f"ag:{pt.key}", L, pt.dtype)
+    comm.device_barrier(channel=PARTITION_CHANNEL)   # peers finished reading the last gather
+    stage.copy_(mine, non_blocking=True)
+    comm.device_barrier(channel=PARTITION_CHANNEL)   # every rank's shard is staged
+    comm.allgather_window(stage, L, out[: pt.full_len], use_copy_engine=use_copy_engine)
     return out
 
 
@@ -154,8 +162,13 @@ def reduce_scatter(contribs, world_size: int, comm=None, scale: float = 1.0,
                    ranks=None) -> list[torch.Tensor]:
     """shard r of the elementwise sum, folded in rank order.
 
-    ``contribs``: full-length CUDA tensors in fold order (one per rank in the
-    simulated model). Half inputs produce fp32 shards (the cast of
+    ``contribs``: full-length CUDA tensors in fold order. In the simulated
+    model (no comm / LocalComm) they are every rank's contributions. With a
+    DistComm they are this process's own contributions (one per rank in
+    standard DP, or k per rank when a rank holds k fixed gradient groups):
+    they are staged into a shared window and every rank's entries are read
+    over NVLink, folded rank-major (rank 0's first, ... ) — the same order
+    the simulated model uses. Half inputs produce fp32 shards (the cast of
     SPEC.md:782 fused in); f32 / f64 inputs keep their dtype. Returns the
     shards of ``ranks`` (default: every local rank).
     """
@@ -168,19 +181,57 @@ def reduce_scatter(contribs, world_size: int, comm=None, scale: float = 1.0,
     L = shard_len(n, world_size)
     out_dt = torch.float64 if ref.dtype == torch.float64 else torch.float32
     rs = list(ranks) if ranks is not None else list(_ranks(world_size, comm))
+    ptrs = [c if isinstance(c, int) else c.data_ptr() for c in contribs]
+    dist_mode = comm is not None and not comm.is_local and comm.world > 1
+    if dist_mode:
+        if comm.world != world_size:
+            raise ValueError("world_size disagrees with the communicator")
+        k = len(contribs)
+        stage, peer = comm.staging(f"rs:{n}:{k}", k * n, ref.dtype)
+        comm.device_barrier(channel=PARTITION_CHANNEL)   # peers finished the last fold
+        for j, c in enumerate(contribs):
+            stage[j * n:(j + 1) * n].copy_(c, non_blocking=True)
+        comm.device_barrier(channel=PARTITION_CHANNEL)   # every rank's contributions staged
+        es = ref.element_size()
+        ptrs = [p + j * n * es for p in peer for j in range(k)]
+        rs = [comm.rank]
     outs = []
-    arr = _lib.ptr_array([c if isinstance(c, int) else c.data_ptr() for c in contribs])
+    arr = _lib.ptr_array(ptrs)
     stream = torch.cuda.current_stream().cuda_stream
     for r in rs:
         o = torch.empty(L, dtype=out_dt, device=ref.device)
-        _lib.call("zi_reduce_scatter", arr, len(contribs), r * L, L, n, _DT[ref.dtype], scale,
+        _lib.call("zi_reduce_scatter", arr, len(ptrs), r * L, L, n, _DT[ref.dtype], scale,
                   o.data_ptr(), stream)
         outs.append(o)
     return outs
 
 
-def broadcast_fetch(key: str, tier: TierKind, store: TierStore) -> tuple[torch.Tensor, int]:
-    """whole tensor from one owner key; all bytes on one path."""
-    data = store.read(key, tier).wait()
-    t = data if data.is_cuda else data.to(store.device, non_blocking=True)
-    return t, t.numel() * t.element_size()
+def broadcast_fetch(key: str, tier: TierKind, store: TierStore, comm=None, owner: int = 0,
+                    numel: int | None = None, dtype: torch.dtype | None = None
+                    ) -> tuple[torch.Tensor, int]:
+    """whole tensor from one owner key; all bytes on one path.
+
+    Simulated ranks (no comm / LocalComm): the owner's store read, as the SPEC.
+    With a DistComm the tensor lives only in ``owner``'s store: the owner
+    stages it into a shared window and every rank pulls the whole tensor from
+    that one GPU (copy engines) — the owner-broadcast baseline the
+    bandwidth-centric all-gather replaces. Non-owners pass
+    ``numel`` / ``dtype``. Returns (tensor, bytes charged to the owner's path).
+    """
+    if comm is None or comm.is_local or comm.world == 1:
+        data = store.read(key, tier).wait()
+        t = data if data.is_cuda else data.to(store.device, non_blocking=True)
+        return t, t.numel() * t.element_size()
+    if comm.rank == owner:
+        data = store.read(key, tier).wait()
+        numel, dtype = data.numel(), data.dtype
+    elif numel is None or dtype is None:
+        raise ValueError("non-owner ranks pass numel and dtype")
+    stage, peer = comm.staging(f"bc:{key}", numel, dtype)
+    comm.device_barrier(channel=PARTITION_CHANNEL)   # peers finished the last fetch
+    if comm.rank == owner:
+        stage[:numel].copy_(data, non_blocking=True)
+    comm.device_barrier(channel=PARTITION_CHANNEL)   # the owner's copy is staged
+    out = torch.empty(numel, dtype=dtype, device=store.device)
+    kernels.allgather([peer[owner]], numel, out, numel, use_copy_engine=True)
+    return out, numel * out.element_size() * (comm.world - 1)
