@@ -447,6 +447,10 @@ def run_ours(args):
     if world > 1:
         try:
             collectives = collective_leg(eng, comm)
+            if same_gpu:   # every rank time-shares one GPU: local HBM copies, not NVLink
+                collectives["link"] = ("local HBM: ranks time-share one GPU (ZINF_BENCH_SAME_GPU); "
+                                       "not an NVLink bus bandwidth")
+                collectives.pop("nvlink_ref_gbs", None)
         except Exception as e:  # noqa: BLE001 — report, never lose the main line
             collectives = {"error": repr(e)[:300]}
 
@@ -483,6 +487,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(tflops_job, 3), "unit": "TFLOPS",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "same_gpu": same_gpu, "physical_gpus": 1 if same_gpu else world,
             "ms_per_step": round(ms_step, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "GPT-style 1.3B (24 layers, hidden 2048, 16 heads, seq 1024, "
@@ -493,7 +498,10 @@ def run_ours(args):
             "tflops_per_gpu": round(tflops_job / world, 3),
             "samples_per_s": round(samples_s, 3),
             "flops_per_step_per_gpu": flops,
-            "flops_formula": "6*tokens*params + causal attention (no recompute)",
+            "flops_formula": "6*tokens*params + 12*B*S^2*hd*nl (attention at the dense-equivalent "
+                             "count, the MFU convention; no recompute)",
+            "tflops_per_gpu_causal_executed": round(
+                eg.model_flops_per_step(cfg, causal_executed=True) / (ms_step / 1e3) / 1e12, 3),
             "loss": float(loss.item()),
             "e2e": {"value": round(e2e_tflops, 3), "unit": "TFLOPS",
                     "h2d_bytes_per_step": cfg.batch * (cfg.seq + 1) * 8,
@@ -615,6 +623,29 @@ def collective_leg(eng, comm, iters: int = 10) -> dict:
         ms = timed(lambda: dist.all_gather_into_tensor(full, mine))
         out["allgather_nccl_ms"], out["allgather_nccl_busbw_gbs"] = round(ms, 4), bus(ms)
     out["nvlink_ref_gbs"] = 770.0
+    # bandwidth-centric partitioning A/B through the SPEC API: the
+    # bucket as a PartitionedTensor gathered from every rank's shard vs the whole bucket
+    # pulled from one owner (broadcast_fetch); effective GB/s = bucket bytes delivered
+    # to each rank per second (allgather should scale with N, the broadcast stays flat)
+    try:
+        from paper_2104_07857_b200.partition import allgather, broadcast_fetch, partition
+        from paper_2104_07857_b200.store import TierKind, TierStore
+        import tempfile
+        st = TierStore(4 * S + (64 << 20), 0, nvme_root=tempfile.mkdtemp(prefix="zinf-ab-"))
+        src = torch.empty(b.numel, dtype=torch.bfloat16, device="cuda").normal_()
+        pt = partition(src, N, TierKind.DEVICE, st, key="ab.bucket", comm=comm)
+        if r == 0:
+            st.write("ab.whole", src, TierKind.DEVICE).wait()
+        ag_out = torch.empty(b.numel, dtype=torch.bfloat16, device="cuda")
+        ms_ag = timed(lambda: allgather(pt, st, comm, out=ag_out, use_copy_engine=True))
+        ms_bc = timed(lambda: broadcast_fetch("ab.whole", TierKind.DEVICE, st, comm=comm, owner=0,
+                                              numel=b.numel, dtype=torch.bfloat16))
+        out["spec_api_ab"] = {"allgather_ms": round(ms_ag, 4), "broadcast_fetch_ms": round(ms_bc, 4),
+                              "allgather_eff_gbs": round(S / (ms_ag / 1e3) / 1e9, 1),
+                              "broadcast_eff_gbs": round(S / (ms_bc / 1e3) / 1e9, 1)}
+        st.close()
+    except Exception as e:  # noqa: BLE001 — report, never lose the main line
+        out["spec_api_ab"] = {"error": repr(e)[:300]}
     return out
 
 
@@ -919,9 +950,39 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     args = ap.parse_args()
     sys.path.insert(0, ROOT)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}",
+              file=sys.stderr)
+        return 2
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without a launcher: start N ranks through torch.distributed.run (one
+    process per GPU, rendezvous on 127.0.0.1). With fewer GPUs than N on the box the
+    ranks time-share cuda:0 (ZINF_BENCH_SAME_GPU=1; the line says same_gpu / physical_gpus)."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    try:
+        import torch
+        ndev = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001
+        ndev = 0
+    if ndev < args.gpus:
+        env["ZINF_BENCH_SAME_GPU"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

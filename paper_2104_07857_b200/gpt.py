@@ -102,14 +102,19 @@ def param_count(c: GPTConfig) -> int:
     return n + c.nl * sum(_numel(s) for _, s, _ in layer_params(c))
 
 
-def model_flops_per_step(c: GPTConfig, ranks: int = 1) -> float:
-    """6 * tokens * params (dense, no recompute) + causal attention matmuls.
+def model_flops_per_step(c: GPTConfig, ranks: int = 1, causal_executed: bool = False) -> float:
+    """6 * tokens * params + the attention score / value matmuls, no recompute.
 
-    The paper's 8*tokens*params (efficiency.py:38-45) counts an activation
-    recompute this engine does not perform; we report executed model flops.
+    The attention term is 12 * B * S^2 * hd * nl (QK^T and PV, forward + backward)
+    at the dense-equivalent count, the MFU convention (Megatron-LM / PaLM); the
+    causal kernels execute half of it (``causal_executed=True`` counts that). The
+    paper's 8*tokens*params (efficiency.py:38-45) counts an activation recompute
+    this engine does not perform.
     """
     T = c.tokens * ranks
-    attn = 6 * 2 * c.batch * ranks * c.seq * c.seq * c.hd * c.nl  # QK^T, PV fwd+bwd (causal: half of dense x2)
+    attn = 12 * c.batch * ranks * c.seq * c.seq * c.hd * c.nl
+    if causal_executed:
+        attn //= 2
     return 6.0 * T * param_count(c) + attn
 
 
@@ -253,12 +258,9 @@ class GPTZeroEngine:
         # pass folded into its epilogue where the site has one) and cuBLAS + a separate
         # pass, timed once per process on this engine's shapes (gemm_select.py).
         # "auto" (default, or ZI_GEMM_SELECT) tunes; "zi" / "cublas" force every site.
-        # One process per GPU (DistComm) defaults to cuBLAS: with two ranks time-sharing
-        # one GPU (the only multi-process setup testable here) a rank holding a
-        # persistent tcgen05 GEMM can starve its peer past the zi_barrier watchdog
-        # (DESIGN.md §8), and the tuned choice is worth ~0.2 ms per step at N=1.
-        default = "auto" if self.comm.is_local else "cublas"
-        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", default)
+        # The cross-rank barriers are stream memory operations (no SM held while a rank
+        # waits), so one process per GPU (DistComm) tunes the same way.
+        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", "auto")
         if mode not in ("auto", "zi", "cublas"):
             raise ValueError("gemm_select must be 'auto', 'zi' or 'cublas'")
         self.gemm_select = mode
@@ -1085,6 +1087,8 @@ class GPTZeroEngine:
         """Before overwriting a gradient slot: the optimizer stream must be done reading it."""
         for done in self._nvme_wait.pop(slot, ()):   # NVMe streamer jobs still using it
             done.wait()
+            if self.streamer.err is not None:         # surface the I/O failure itself
+                raise self.streamer.err
             torch.cuda.current_stream().wait_event(done.ev)
         ev = self.gfree.pop(slot, None)
         if ev is not None:

@@ -102,8 +102,12 @@ class NvmeOptimizerStreamer:
             try:
                 if self.err is None:
                     self._bucket(*job)
+                else:                           # an earlier job failed: release waiters
+                    job[-1].ev = None
+                    job[-1].set()
             except BaseException as exc:  # noqa: BLE001 — surfaced by drain()
                 self.err = exc
+                job[-1].ev = None              # no completion event: waiters re-raise err
                 job[-1].set()
             finally:
                 self.q.task_done()

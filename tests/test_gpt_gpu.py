@@ -1,11 +1,10 @@
 """The partitioned GPT step on the GPU against the CPU oracle (oracle/gpt.py).
 
-Layout and init are bit-exact; gradients / loss within stated tolerances:
-fp32 compute (half params widened, as the SPEC harness computes)
-within 1e-5 on the loss and 1e-2 relative L2 on gradient shards (bucket
-grads are rounded to half before the reduce-scatter, so summation-order
-differences can flip single half ulps); bf16 compute within 2e-2 on the
-loss and 6e-2 on gradients (SURVEY.md §8c tolerance proposal).
+Layout and init are bit-exact. The step (BASELINE config 1 at world 2, 3 steps; a
+1.3B-shape block; ragged worlds) is checked per step on the loss, every gradient
+shard and the Adam update of every master element, with tolerances set at ~5x the
+error measured on B200 (TOL_BF16 / TOL_FP32 below, scripts/parity_probe.py): tight
+enough that a skipped, doubled or misrouted update fails.
 """
 
 import numpy as np
@@ -55,40 +54,84 @@ def test_init_layout_bit_exact(world, half, kind):
         assert np.array_equal(full, want)
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_step_fp32_compute_matches_oracle(world):
-    torch.backends.cuda.matmul.allow_tf32 = False
-    eng = eg.GPTZeroEngine(SMALL, LocalComm(world), half_dtype=torch.float16,
-                           compute_dtype=torch.float32, lr=1e-3)
+def update_errors(eng, prev, st, lr):
+    """Adam update of the GPU step vs the oracle's, per element in units of lr:
+    (fraction of elements off by more than 0.1*lr, relative L2 of the update difference).
+    A skipped or wrong update is off by ~lr on most elements: fraction ~1, rel ~1."""
+    errs, num, den = [], 0.0, 0.0
+    for key in st.p32:
+        for r in range(st.world):
+            p = eng.shard(key, r)["p32"].cpu().numpy().astype(np.float64)
+            dg = p - prev[key][r]
+            do = st.p32[key][r].astype(np.float64) - prev[key][r]
+            errs.append(np.abs(dg - do) / lr)
+            num += float(((dg - do) ** 2).sum())
+            den += float((do ** 2).sum())
+    e = np.concatenate(errs)
+    return float((e > 0.1).mean()), float(np.sqrt(num / den))
+
+
+def run_vs_oracle(cfg, world, steps, lr, tol, half=torch.bfloat16, compute=None, **kw):
+    """``steps`` partitioned steps of the engine and the CPU oracle on the same seeded
+    tokens, checked per step against ``tol`` = (loss rel, grad-shard rel L2,
+    fraction of update elements off by > 0.1 lr, update rel L2)."""
+    kind = nx.HALF_BF16 if half == torch.bfloat16 else nx.HALF_FP16
+    eng = eg.GPTZeroEngine(cfg, LocalComm(world), lr=lr, half_dtype=half, compute_dtype=compute, **kw)
     eng.capture_grads = True
-    st = og.init_partitioned(ocfg(SMALL), world, half_kind=nx.HALF_FP16)
-    for step in range(2):
-        bs = batches_for(SMALL, world, step)
+    st = og.init_partitioned(ocfg(cfg), world, half_kind=kind)
+    for step in range(steps):
+        prev = {k: [s.astype(np.float64) for s in st.p32[k]] for k in st.p32}
+        bs = batches_for(cfg, world, step)
         loss = eng.step(bs).item()
-        oloss, gsh = og.train_step(st, [(t.cpu().numpy(), y.cpu().numpy()) for t, y in bs], lr=1e-3)
-        assert abs(loss - oloss) <= 1e-5 * abs(oloss), (step, loss, oloss)
+        oloss, gsh = og.train_step(st, [(t.cpu().numpy(), y.cpu().numpy()) for t, y in bs], lr=lr)
+        assert abs(loss - oloss) <= tol[0] * abs(oloss), (step, loss, oloss)
         for key in gsh:
             for r in range(world):
-                g = eng.grad_shards[key][r].cpu().numpy()
-                assert rel(g, gsh[key][r]) < 1e-2, (step, key, r, rel(g, gsh[key][r]))
-        for key in st.p32:
-            for r in range(world):
-                p = eng.shard(key, r)["p32"].cpu().numpy()
-                assert np.abs(p - st.p32[key][r]).max() < 3e-3, key
+                e = rel(eng.grad_shards[key][r].cpu().numpy(), gsh[key][r])
+                assert e < tol[1], (step, key, r, e)
+        frac, urel = update_errors(eng, prev, st, lr)
+        assert frac < tol[2] and urel < tol[3], (step, frac, urel)
+    return eng, st
 
 
-def test_step_bf16_matches_oracle():
-    world = 2
-    eng = eg.GPTZeroEngine(SMALL, LocalComm(world), lr=1e-3)
-    eng.capture_grads = True
-    st = og.init_partitioned(ocfg(SMALL), world, half_kind=nx.HALF_BF16)
-    bs = batches_for(SMALL, world)
-    loss = eng.step(bs).item()
-    oloss, gsh = og.train_step(st, [(t.cpu().numpy(), y.cpu().numpy()) for t, y in bs], lr=1e-3)
-    assert abs(loss - oloss) <= 2e-2 * abs(oloss)
-    for key in gsh:
-        for r in range(world):
-            assert rel(eng.grad_shards[key][r].cpu().numpy(), gsh[key][r]) < 6e-2, key
+# Tolerances ~5x the errors measured on B200 (scripts/parity_probe.py; per step, worst of
+# 3): bf16 compute vs the fp32 oracle: loss 4.4e-5, grad shards 1.1e-2, update elements
+# off by > 0.1 lr 1.2 %, update rel L2 0.21. fp32 compute (fp16 params): loss 7.5e-8,
+# grads 1.8e-4, 2.4e-6, 2.1e-3. A skipped or wrong Adam update gives ~1 and ~1.
+TOL_BF16 = (2e-4, 5e-2, 5e-2, 0.5)
+TOL_FP32 = (1e-6, 1e-3, 1e-4, 1e-2)
+
+
+@pytest.mark.parametrize("act_ckpt", [None, "host"])
+def test_config1_bf16_matches_oracle(act_ckpt):
+    """BASELINE config 1 (nl4 / hd256 / 4 heads / seq128 / batch4 / V512), world 2, 3 steps
+    against the CPU oracle; with act_ckpt="host" the block inputs go to pinned host DRAM
+    and the backward recomputes from them (PAPER §5.1.2) — checked against the oracle
+    directly, not against the no-checkpoint engine."""
+    eng, _ = run_vs_oracle(eg.TINY, 2, 3, 1e-3, TOL_BF16, act_ckpt=act_ckpt)
+    if act_ckpt == "host":
+        assert eng.ckpt_bytes > 0
+
+
+def test_config1_fp32_compute_matches_oracle():
+    """fp32 compute (half params widened) against the fp32 oracle: the
+    remaining error is summation order and single-ulp flips of the fp16 gradient
+    contributions."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    run_vs_oracle(eg.TINY, 2, 3, 1e-3, TOL_FP32, half=torch.float16, compute=torch.float32)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_small_worlds_match_oracle(world):
+    """Ragged world sizes (zero-padded shards) on the small config."""
+    run_vs_oracle(SMALL, world, 2, 1e-3, TOL_BF16)
+
+
+def test_1p3b_block_shape_matches_oracle():
+    """One step of a block at the BASELINE 1.3B shape (hd 2048, 16 heads, seq 1024,
+    V 50304, one sequence). Measured: loss 1.6e-5, grads 6.2e-3, 0.25 %, 0.058."""
+    c = eg.GPTConfig(nl=1, hd=2048, heads=16, seq=1024, vocab=50304, batch=1)
+    run_vs_oracle(c, 1, 1, 1e-4, (1e-4, 3e-2, 2e-2, 0.25))
 
 
 @pytest.mark.parametrize("world", [1, 2])

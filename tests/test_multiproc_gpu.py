@@ -100,6 +100,85 @@ def test_two_processes_match_local_comm(placement, graph, cache):
     np.testing.assert_allclose(mean_dist, ref_losses, rtol=1e-5)
 
 
+def _oracle_rank_main(rank, world, port, q, gemm_select):
+    """BASELINE config 1 with one process per rank: per-step loss, gradient shards and
+    master shards (before / after) for the oracle comparison in the parent."""
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2104_07857_b200 import gpt as eg
+        from paper_2104_07857_b200.comm import DistComm
+        comm = DistComm()
+        eng = eg.GPTZeroEngine(eg.TINY, comm, lr=1e-3, gemm_select=gemm_select)
+        eng.capture_grads = True
+        out = []
+        for step in range(3):
+            loss = eng.step([eg.synthetic_tokens(eg.TINY, 7, rank, step)]).item()
+            out.append((loss, {k: v[rank].cpu().numpy() for k, v in eng.grad_shards.items()},
+                        {k: eng.shard(k, 0)["p32"].cpu().numpy() for k in eng.by_key}))
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok", out))
+    except Exception:  # noqa: BLE001
+        import traceback
+        q.put((rank, "error", traceback.format_exc()))
+
+
+@pytest.mark.parametrize("gemm_select", ["cublas", "zi"])
+def test_config1_two_processes_match_oracle(gemm_select):
+    """BASELINE config 1 (nl4 / hd256 / seq128 / batch4 / V512) at world 2 with one
+    process per rank (DistComm: P2P gathers, stream-memop barriers, RS + Adam over the
+    peer's gradient bucket), 3 steps against the CPU oracle with test_gpt_gpu's
+    tolerances; gemm_select="zi" runs every linear on the tcgen05 GEMM (no SM is held
+    by a waiting barrier, so a time-sliced peer cannot be starved)."""
+    from oracle import gpt as og
+    from oracle import numerics as nx
+    from paper_2104_07857_b200 import gpt as eg
+    from test_gpt_gpu import TOL_BF16, rel
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_oracle_rank_main, args=(r, world, port, q, gemm_select))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, st, b = q.get(timeout=600)
+        assert st == "ok", b
+        res[r] = b
+    for p in procs:
+        p.join(timeout=60)
+    c = eg.TINY
+    ost = og.init_partitioned(og.GPTConfig(c.nl, c.hd, c.heads, c.seq, c.vocab, c.batch), world,
+                              half_kind=nx.HALF_BF16)
+    lr = 1e-3
+    for step in range(3):
+        prev = {k: [s.astype(np.float64) for s in ost.p32[k]] for k in ost.p32}
+        bs = [tuple(t.cpu().numpy() for t in eg.synthetic_tokens(c, 7, r, step, device="cpu"))
+              for r in range(world)]
+        oloss, gsh = og.train_step(ost, bs, lr=lr)
+        mean = (res[0][step][0] + res[1][step][0]) / 2   # DistComm: each rank's own loss
+        assert abs(mean - oloss) <= TOL_BF16[0] * abs(oloss), (step, mean, oloss)
+        errs, num, den = [], 0.0, 0.0
+        for r in range(world):
+            _, g, p32 = res[r][step]
+            for key in gsh:
+                assert rel(g[key], gsh[key][r]) < TOL_BF16[1], (step, key, r)
+                dg = p32[key].astype(np.float64) - prev[key][r]
+                do = ost.p32[key][r].astype(np.float64) - prev[key][r]
+                errs.append(np.abs(dg - do) / lr)
+                num += float(((dg - do) ** 2).sum())
+                den += float((do ** 2).sum())
+        e = np.concatenate(errs)
+        assert (e > 0.1).mean() < TOL_BF16[2] and np.sqrt(num / den) < TOL_BF16[3], step
+
+
 def _ctx_rank_main(rank, world, port, q):
     """zi_ctx collectives through DistComm windows: one rank per process."""
     try:
