@@ -321,6 +321,16 @@ int zi_gemm_ex(const void* A, int a_mn_major, int lda, const void* B, int b_mn_m
  * wide-tile GEMM's pipeline (NULL turns it off). Not for production use. */
 int zi_gemm_set_profile(void* buf);
 
+/* ---- causal multi-head attention on tcgen05 (csrc/attn_sm100.cu) -------------
+ * qkv [B*S, 3*H*D] bf16 (head h of q / k / v at columns h*D, H*D + h*D, 2*H*D + h*D),
+ * out / dout [B*S, H*D] bf16, lse / delta fp32 [B*H*S] (lse in the log2 domain of the
+ * scaled scores), dqkv like qkv. D in {64, 128}, S a multiple of 128. The backward
+ * is deterministic: no atomics, every output row summed in a fixed order. */
+int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int head_dim,
+                void* stream);
+int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
+                void* dqkv, int B, int H, int S, int head_dim, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

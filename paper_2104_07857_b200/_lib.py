@@ -120,6 +120,9 @@ SIGNATURES = {
     "zi_gemm": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
                 c_int, c_int, c_int, c_int, c_void_p],
     "zi_gemm_set_profile": [c_void_p],
+    "zi_attn_fwd": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
+    "zi_attn_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                    c_int, c_void_p],
     "zi_gemm_ex": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int,
                    c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p],
 }

@@ -387,3 +387,42 @@ def linear_tile_bwd(x: torch.Tensor, w_t: torch.Tensor, dy_t: torch.Tensor, dw_t
               dx_acc.data_ptr() if dx_acc is not None else None,
               dx_acc.stride(0) if dx_acc is not None else 0,
               db_t.data_ptr() if db_t is not None else None, M, K, N, _stream(stream))
+
+
+def _attn_shapes(qkv: torch.Tensor, batch: int, heads: int):
+    if qkv.dtype != torch.bfloat16 or qkv.dim() != 2 or qkv.shape[1] % (3 * heads):
+        raise ValueError("qkv must be bf16 [B*S, 3*H*D]")
+    if qkv.shape[0] % batch:
+        raise ValueError("qkv rows must be batch * seq")
+    return qkv.shape[0] // batch, qkv.shape[1] // (3 * heads)
+
+
+def attn_fwd(qkv: torch.Tensor, out: torch.Tensor, lse: torch.Tensor, batch: int, heads: int,
+             stream=None) -> None:
+    """zi_attn_fwd: causal attention on tcgen05; out [B*S, H*D] bf16, lse fp32 [B*H*S]
+    (log2 domain of the 1/sqrt(D)-scaled scores, kept for the backward)."""
+    S, D = _attn_shapes(qkv, batch, heads)
+    if out.dtype != torch.bfloat16 or out.shape != (qkv.shape[0], heads * D):
+        raise ValueError("out must be bf16 [B*S, H*D]")
+    if lse.dtype != torch.float32 or lse.numel() != batch * heads * S:
+        raise ValueError("lse must be fp32 with B*H*S elements")
+    _lib.call("zi_attn_fwd", _dev(qkv, "qkv"), _dev(out, "out"), _dev(lse, "lse"), batch, heads,
+              S, D, _stream(stream))
+
+
+def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
+             delta: torch.Tensor, dqkv: torch.Tensor, batch: int, heads: int, stream=None) -> None:
+    """zi_attn_bwd: dqkv of causal attention, deterministic (fixed-order sums, no
+    atomics); delta is an fp32 [B*H*S] workspace (rowsum of dout * out)."""
+    S, D = _attn_shapes(qkv, batch, heads)
+    for t, nm in ((out, "out"), (dout, "dout")):
+        if t.dtype != torch.bfloat16 or t.shape != (qkv.shape[0], heads * D):
+            raise ValueError(f"{nm} must be bf16 [B*S, H*D]")
+    if dqkv.dtype != torch.bfloat16 or dqkv.shape != qkv.shape:
+        raise ValueError("dqkv must be bf16 like qkv")
+    for t, nm in ((lse, "lse"), (delta, "delta")):
+        if t.dtype != torch.float32 or t.numel() != batch * heads * S:
+            raise ValueError(f"{nm} must be fp32 with B*H*S elements")
+    _lib.call("zi_attn_bwd", _dev(qkv, "qkv"), _dev(out, "out"), _dev(dout, "dout"),
+              _dev(lse, "lse"), _dev(delta, "delta"), _dev(dqkv, "dqkv"), batch, heads, S, D,
+              _stream(stream))
