@@ -330,6 +330,9 @@ int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int
                 void* stream);
 int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
                 void* dqkv, int B, int H, int S, int head_dim, void* stream);
+/* Diagnostics: per-CTA globaltimer records of zi_attn_fwd into buf (6 u64 per CTA: sm,
+ * entry, operands in, last MMA issued, softmax done, exit); NULL turns it off. */
+int zi_attn_set_trace(void* buf);
 
 #ifdef __cplusplus
 }

@@ -37,31 +37,33 @@ namespace attn {
 
 using namespace zi::tc;
 
-constexpr int THREADS = 192;
-constexpr int PB = 128 * 128 * 2;            // one 128 x 128 bf16 tile
+constexpr int THREADS = 320;                 // warp 0 TMA, warp 1 MMA, warps 2..9 elementwise
+constexpr int GW = 4;                        // warps per elementwise group (one per lane quadrant)
 constexpr float LOG2E = 1.4426950408889634f;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// 128 rows x D columns of a bf16 matrix (box 64 x 64) -> chunk regions of 16 KiB
-template <int D>
-__device__ __forceinline__ void load_tile(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+// ROWS x D bf16 (box 64 x 64) -> D/64 chunk regions of ROWS*128 bytes (tc.cuh layout)
+template <int D, int ROWS>
+__device__ __forceinline__ void load_rows(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
                                           int col0, int row0) {
 #pragma unroll
   for (int kc = 0; kc < D / 64; ++kc)
 #pragma unroll
-    for (int rh = 0; rh < 2; ++rh)
-      tma_load_2d(dst + kc * 16384 + rh * 8192, map, bar, col0 + kc * 64, row0 + rh * 64);
+    for (int rh = 0; rh < ROWS / 64; ++rh)
+      tma_load_2d(dst + kc * ROWS * 128 + rh * 8192, map, bar, col0 + kc * 64, row0 + rh * 64);
 }
 
-// k-step kk (16 deep) of a 128-row tile read K-major / MN-major (tc.cuh convention)
+// k-step kk (16 deep) of a ROWS-row tile read K-major / MN-major
+template <int ROWS>
 __device__ __forceinline__ uint64_t kdesc(const uint8_t* base, int kk) {
-  return sdesc_sw128(smem_u32(base) + (kk >> 2) * 16384 + (kk & 3) * 32, 16);
+  return sdesc_sw128(smem_u32(base) + (kk >> 2) * ROWS * 128 + (kk & 3) * 32, 16);
 }
+template <int ROWS>
 __device__ __forceinline__ uint64_t mndesc(const uint8_t* base, int kk) {
-  return sdesc_sw128(smem_u32(base) + kk * 2048, 16384);
+  return sdesc_sw128(smem_u32(base) + kk * 2048, ROWS * 128);
 }
 
 // 16-byte piece g (elements 8g .. 8g+7) of row r of a 128-row K-major tile
@@ -71,20 +73,42 @@ __device__ __forceinline__ void st_piece(uint8_t* tile, int r, int g, uint4 v) {
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 
-// D[128 x N] (+)= A B over `ksteps` 16-deep steps; A K-major, B K- or MN-major
-template <bool B_MN>
-__device__ __forceinline__ void mma_tile(uint32_t d, const uint8_t* a, const uint8_t* b,
-                                         int ksteps, uint32_t idesc, bool accumulate) {
-  for (int kk = 0; kk < ksteps; ++kk)
-    umma_bf16(d, kdesc(a, kk), B_MN ? mndesc(b, kk) : kdesc(b, kk), idesc,
-              (accumulate || kk > 0) ? 1u : 0u);
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
-// one row of D fp32 TMEM columns (x scale) -> bf16 global (16-byte stores)
-template <int D>
+// D[128 x N] (+)= A B over KS 16-deep steps: A a 128-row K-major tile, B a BROWS-row tile
+// (K- or MN-major). Descriptors are built once and stepped by constant offsets (the start
+// address field holds bytes >> 4), so each MMA issues with no per-step address math.
+template <int BROWS, bool B_MN, int KS>
+__device__ __forceinline__ void mma_tile(uint32_t d, const uint8_t* a, const uint8_t* b,
+                                         uint32_t idesc, bool accumulate) {
+  const uint64_t da = kdesc<128>(a, 0);
+  const uint64_t db = B_MN ? mndesc<BROWS>(b, 0) : kdesc<BROWS>(b, 0);
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const uint64_t oa = (uint64_t)((kk >> 2) * (128 * 128 >> 4) + (kk & 3) * 2);
+    const uint64_t ob = B_MN ? (uint64_t)(kk * (2048 >> 4))
+                             : (uint64_t)((kk >> 2) * (BROWS * 128 >> 4) + (kk & 3) * 2);
+    umma_bf16(d, da + oa, db + ob, idesc, (accumulate || kk > 0) ? 1u : 0u);
+  }
+}
+
+// one lane of a converged warp (elect.sync): the tcgen05.mma issuer
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p = 0;
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\tselp.u32 %0, 1, 0, e;\n\t}"
+               : "=r"(p));
+  return p != 0;
+}
+
+// one row of NC fp32 TMEM columns (x scale) -> bf16 global (16-byte stores)
+template <int NC>
 __device__ __forceinline__ void store_row(uint32_t taddr, float scale, __nv_bfloat16* dst) {
 #pragma unroll
-  for (int cc = 0; cc < D / 32; ++cc) {
+  for (int cc = 0; cc < NC / 32; ++cc) {
     uint32_t o[32];
     tmem_ld32(taddr + cc * 32, o);
     uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
@@ -110,44 +134,61 @@ __device__ __forceinline__ void tmem_free512(uint32_t tmem) {
                : "memory");
 }
 
+// Every kernel walks its kv (or q) range in 64-column sub-tiles u = 0, 1, 2, ...; sub-tile
+// u belongs to elementwise group g = u & 1 (warps 2..5 / 6..9: lane quadrant = warp & 3),
+// which owns TMEM score slot g and shared tile slot g. The MMA thread issues the score
+// MMAs of sub-tile u before it waits for group (u-1)&1's elementwise result, so the
+// tensor core works on one sub-tile while the other group works on the previous one.
+
 // ============================================================================ forward
+// Two independent online softmaxes: group g folds the kv columns g*64..g*64+63 of every
+// kv tile into its own (m_g, l_g, O_g); the epilogue merges the two.
 template <int D>
 struct Fwd {
-  static constexpr int TB = 128 * D * 2;
-  static constexpr int Q = 0, K = TB, V = 3 * TB, P = 5 * TB, BAR = 5 * TB + PB;
+  static constexpr int QB = 128 * D * 2, HB = 64 * D * 2, NST = 4;   // kv half-tile stages
+  static constexpr int Q = 0, KV = QB, P = QB + NST * 2 * HB, XCH = P + 2 * 16384,
+                       BAR = XCH + 4 * 128 * 4;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
 template <int D>
 __global__ void __launch_bounds__(THREADS, 1)
 fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
-           float* __restrict__ lse, int B, int H, int S, int hd, float sl2) {
+           float* __restrict__ lse, int B, int H, int S, int hd, float sl2,
+           unsigned long long* __restrict__ trace) {
+  // trace (diagnostics, normally null): per CTA {sm, entry, operands in, last MMA issued,
+  // softmax done, exit} in globaltimer ns
+  unsigned long long* tr = trace ? trace + blockIdx.x * 6 : nullptr;
+  if (tr && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[0] = smid;
+    tr[1] = gtimer();
+  }
   using L = Fwd<D>;
-  constexpr int TB = L::TB;
+  constexpr int HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sQ = sm + L::Q, *sK = sm + L::K, *sV = sm + L::V, *sP = sm + L::P;
+  uint8_t *sQ = sm + L::Q, *sKV = sm + L::KV, *sP = sm + L::P;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5,
-           *v_empty = bar + 7, *s_full = bar + 9, *s_free = bar + 11, *p_full = bar + 13,
-           *pv_done = bar + 14;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + NST,
+           *s_full = bar + 1 + 2 * NST, *s_free = s_full + 2, *p_full = s_full + 4,
+           *pv_done = s_full + 6;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int nq = S / 128, BH = B * H;
   const int i = nq - 1 - (int)blockIdx.x / BH;     // long causal rows first
   const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
-  const int nkv = i + 1, row0 = b * S;
+  const int nkv = i + 1, nsub = 2 * nkv, row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1);
-      mbar_init(&s_full[s], 1); mbar_init(&s_free[s], 4);
+    for (int s = 0; s < NST; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1); mbar_init(&s_free[g], GW);
+      mbar_init(&p_full[g], GW); mbar_init(&pv_done[g], 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm);
   }
@@ -155,118 +196,174 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
-  const uint32_t tmem = *tslot;
-  const uint32_t tS0 = tmem, tO = tmem + 256;
+  const uint32_t tmem = *tslot;        // S slot g at g*64; O_g at 256 + g*128
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, TB);
-      load_tile<D>(sQ, &tm, q_full, h * D, row0 + i * 128);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_empty[s], ph ^ 1);
-        mbar_expect_tx(&k_full[s], TB);
-        load_tile<D>(sK + s * TB, &tm, &k_full[s], hd + h * D, row0 + j * 128);
-        mbar_wait(&v_empty[s], ph ^ 1);
-        mbar_expect_tx(&v_full[s], TB);
-        load_tile<D>(sV + s * TB, &tm, &v_full[s], 2 * hd + h * D, row0 + j * 128);
+      mbar_expect_tx(q_full, L::QB);
+      load_rows<D, 128>(sQ, &tm, q_full, h * D, row0 + i * 128);
+      for (int u = 0; u < nsub; ++u) {
+        const int st = u % NST;
+        mbar_wait(&kv_empty[st], ((u / NST) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * HB);
+        const int r = row0 + u * 64;               // kv rows of sub-tile u
+        load_rows<D, 64>(sKV + st * 2 * HB, &tm, &kv_full[st], hd + h * D, r);
+        load_rows<D, 64>(sKV + st * 2 * HB + HB, &tm, &kv_full[st], 2 * hd + h * D, r);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16_f32(128, 128, false, false);
-      constexpr uint32_t id_o = idesc_bf16_f32(128, D, false, true);
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
-      fence_after_sync();
-      mma_tile<false>(tS0, sQ, sK, D / 16, id_s, false);
-      umma_commit(&k_empty[0]);
-      umma_commit(&s_full[0]);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) {                       // S_{j+1} overlaps the softmax of S_j
-          const int n = j + 1, sb = n & 1;
-          if (n >= 2) mbar_wait(&s_free[sb], ((n - 2) >> 1) & 1);
-          mbar_wait(&k_full[sb], (n >> 1) & 1);
-          fence_after_sync();
-          mma_tile<false>(tS0 + sb * 128, sQ, sK + sb * TB, D / 16, id_s, false);
-          umma_commit(&k_empty[sb]);
-          umma_commit(&s_full[sb]);
-        }
-        mbar_wait(p_full, j & 1);
-        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+    // the whole warp waits; one elected lane issues each group of MMAs and commits
+    constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
+    constexpr uint32_t id_o = idesc_bf16_f32(128, D, false, true);
+    mbar_wait(q_full, 0);
+    unsigned long long* ms = (tr && blockIdx.x == 0 && lane == 0)
+                                 ? trace + gridDim.x * 6 + 2 * 64 * 6 : nullptr;
+    for (int u = 0; u <= nsub; ++u) {
+      if (tr && lane == 0 && u == 1) tr[2] = gtimer();
+      if (ms) ms[u * 4 + 0] = clock64();
+      if (u < nsub) {                              // scores of sub-tile u
+        const int st = u % NST, g = u & 1;
+        mbar_wait(&kv_full[st], (u / NST) & 1);
+        if (ms) ms[u * 4 + 1] = clock64();
+        if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
+        if (ms) ms[u * 4 + 2] = clock64();
         fence_after_sync();
-        mma_tile<true>(tO, sP, sV + (j & 1) * TB, 8, id_o, j > 0);
-        umma_commit(&v_empty[j & 1]);
-        umma_commit(pv_done);
+        if (elect_one()) {
+          mma_tile<64, false, D / 16>(tmem + g * 64, sQ, sKV + st * 2 * HB, id_s, false);
+          umma_commit(&s_full[g]);
+        }
+        __syncwarp();
+      }
+      if (u >= 1) {                                // O_g += P V of sub-tile u-1
+        const int v = u - 1, st = v % NST, g = v & 1;
+        mbar_wait(&p_full[g], (v >> 1) & 1);
+        if (ms) ms[u * 4 + 3] = clock64();
+        fence_after_sync();
+        if (elect_one()) {
+          mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sKV + st * 2 * HB + HB,
+                                id_o, v >= 2);
+          umma_commit(&kv_empty[st]);
+          umma_commit(&pv_done[g]);
+        }
+        __syncwarp();
       }
     }
-    __syncwarp();
+    if (tr && lane == 0) tr[3] = gtimer();
   } else {
-    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + g * 64 + lo, tO = tmem + 256 + g * 128 + lo;
+    uint8_t* sPg = sP + g * 16384;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+    unsigned long long* fs = (tr && blockIdx.x == 0 && lane == 0 && (warp == 2 || warp == 6))
+                                 ? trace + gridDim.x * 6 + g * 64 * 6 : nullptr;
+    for (int jj = 0; jj < nkv; ++jj) {
+      if (fs) fs[jj * 6 + 0] = clock64();
+      mbar_wait(&s_full[g], jj & 1);
+      if (fs) fs[jj * 6 + 1] = clock64();
       fence_after_sync();
-      float x[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t t[32];
-        tmem_ld32(tS0 + sb * 128 + lo + c * 32, t);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) x[c * 32 + k] = u2f(t[k]) * sl2;
-      }
+      uint32_t t0[32], t1[32];
+      tmem_ld32_nowait(tS, t0);
+      tmem_ld32_nowait(tS + 32, t1);
+      tmem_wait_ld();
+      if (fs) fs[jj * 6 + 2] = clock64();
       fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[sb]);
-      if (j == i) {                              // diagonal tile: key index > query index
+      if (lane == 0) mbar_arrive(&s_free[g]);
+      float x[64];
 #pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > r) x[c] = -INFINITY;
+      for (int k = 0; k < 32; ++k) {
+        x[k] = u2f(t0[k]);
+        x[32 + k] = u2f(t1[k]);
       }
-      float mx = m;
+      if (jj == i) {                             // diagonal tile: key index > query index
 #pragma unroll
-      for (int c = 0; c < 128; ++c) mx = fmaxf(mx, x[c]);
-      const float alpha = ex2(m - mx);           // 0 on the first tile (m = -inf)
-      uint32_t pk[64];
-      float rs = 0.f;
+        for (int c = 0; c < 64; ++c)
+          if (g * 64 + c > r) x[c] = -INFINITY;
+      }
+      float mx[8];
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float p0 = ex2(x[2 * c] - mx), p1 = ex2(x[2 * c + 1] - mx);
-        rs += p0 + p1;
+      for (int k = 0; k < 8; ++k) mx[k] = x[k];
+#pragma unroll
+      for (int c = 8; c < 64; ++c) mx[c & 7] = fmaxf(mx[c & 7], x[c]);
+      const float mrow = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+      // lazy rescale (FA4): move the reference max only when it grows by > 2^8
+      float alpha = 1.f;
+      if (mrow > m + 8.f) {                      // first live tile: m = -inf -> alpha = 0
+        alpha = ex2(m - mrow);
+        m = mrow;
+      }
+      const float nm = (m == -INFINITY) ? 0.f : -m;   // fully masked so far: p = 0
+      uint32_t pk[32];
+      float rs[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) rs[k] = 0.f;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const float p0 = ex2(fmaf(x[2 * c], sl2, nm)), p1 = ex2(fmaf(x[2 * c + 1], sl2, nm));
+        rs[c & 7] += p0 + p1;
         pk[c] = pack_bf16(p0, p1);
       }
-      l = l * alpha + rs;
-      m = mx;
-      if (j >= 1) {
-        mbar_wait(pv_done, (j - 1) & 1);         // O_{j-1} complete, P buffer free
+      l = l * alpha + (((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7])));
+      if (fs) fs[jj * 6 + 3] = clock64();
+      if (jj >= 1) {
+        mbar_wait(&pv_done[g], (jj - 1) & 1);    // O_g stable, P_g free
         fence_after_sync();
         if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
           for (int cc = 0; cc < D / 32; ++cc) {
             uint32_t o[32];
-            tmem_ld32(tO + lo + cc * 32, o);
+            tmem_ld32(tO + cc * 32, o);
 #pragma unroll
             for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(u2f(o[k]) * alpha);
-            tmem_st32(tO + lo + cc * 32, o);
+            tmem_st32(tO + cc * 32, o);
           }
         }
       }
+      if (fs) fs[jj * 6 + 4] = clock64();
 #pragma unroll
-      for (int g = 0; g < 16; ++g)
-        st_piece(sP, r, g, make_uint4(pk[4 * g], pk[4 * g + 1], pk[4 * g + 2], pk[4 * g + 3]));
+      for (int q = 0; q < 8; ++q)
+        st_piece(sPg, r, q, make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
       fence_proxy_async_smem();
       fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[g]);
+      if (fs) fs[jj * 6 + 5] = clock64();
     }
-    mbar_wait(pv_done, (nkv - 1) & 1);
+    // merge the two streams: O = (O_0 2^(m_0-M) + O_1 2^(m_1-M)) / (l_0 2^(m_0-M) + l_1 2^(m_1-M))
+    float* xch = reinterpret_cast<float*>(sm + L::XCH);
+    xch[g * 256 + r] = m;
+    xch[g * 256 + 128 + r] = l;
+    mbar_wait(&pv_done[g], (nkv - 1) & 1);
+    named_sync(1 + q4, 2 * 32);
+    const float m0 = xch[r], l0 = xch[128 + r], m1 = xch[256 + r], l1 = xch[384 + r];
+    const float M = fmaxf(m0, m1);
+    const float a0 = ex2(m0 - M), a1 = (m1 == -INFINITY) ? 0.f : ex2(m1 - M);
+    const float Lt = l0 * a0 + l1 * a1, inv = 1.f / Lt;
     fence_after_sync();
     const size_t row = (size_t)row0 + i * 128 + r;
-    store_row<D>(tO + lo, 1.f / l, out + row * hd + h * D);
-    lse[(size_t)bh * S + i * 128 + r] = m + __log2f(l);
+    __nv_bfloat16* dst = out + row * hd + h * D + g * (D / 2);
+    const uint32_t o0 = tmem + 256 + lo + g * (D / 2), o1 = o0 + 128;
+#pragma unroll 1
+    for (int cc = 0; cc < D / 64; ++cc) {
+      uint32_t x0[32], x1[32];
+      tmem_ld32_nowait(o0 + cc * 32, x0);
+      tmem_ld32_nowait(o1 + cc * 32, x1);
+      tmem_wait_ld();
+      uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float f[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          f[k] = fmaf(u2f(x0[8 * q + k]), a0, u2f(x1[8 * q + k]) * a1) * inv;
+        d4[q] = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
+                           pack_bf16(f[6], f[7]));
+      }
+    }
+    if (g == 0) lse[(size_t)bh * S + i * 128 + r] = M + __log2f(Lt);
+    if (tr && warp == 2 && lane == 0) tr[4] = gtimer();
   }
   fence_before_sync();
   __syncthreads();
@@ -274,14 +371,16 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     fence_after_sync();
     tmem_free512(tmem);
   }
+  if (tr && threadIdx.x == 0) tr[5] = gtimer();
 }
 
 // =================================================================== backward: dK, dV
+// CTA = kv tile j; sub-tiles over the q columns (q halves of tiles i >= j).
 template <int D>
 struct Bkv {
-  static constexpr int TB = 128 * D * 2;
-  static constexpr int K = 0, V = TB, Q = 2 * TB, DO = 3 * TB, PT = 4 * TB, DST = 4 * TB + PB,
-                       LD = 4 * TB + 2 * PB, BAR = LD + 2 * 256 * 4;
+  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 3;   // q / dO half stages
+  static constexpr int K = 0, V = TB, QD = 2 * TB, PT = QD + NST * 2 * HB, DST = PT + 2 * 16384,
+                       BAR = DST + 2 * 16384;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -292,27 +391,31 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
                 __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
                 float scale) {
   using L = Bkv<D>;
-  constexpr int TB = L::TB;
+  constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sK = sm + L::K, *sV = sm + L::V, *sQ = sm + L::Q, *sdO = sm + L::DO,
-          *sPT = sm + L::PT, *sdST = sm + L::DST;
-  float* sLD = reinterpret_cast<float*>(sm + L::LD);
+  uint8_t *sK = sm + L::K, *sV = sm + L::V, *sQD = sm + L::QD, *sPT = sm + L::PT,
+          *sdST = sm + L::DST;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t *kv_full = bar, *qdo_full = bar + 1, *qdo_empty = bar + 2, *st_full = bar + 3,
-           *st_free = bar + 4, *ps_full = bar + 5, *ps_empty = bar + 6, *acc_done = bar + 7;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 1 + NST,
+           *st_full = bar + 1 + 2 * NST, *st_free = st_full + 2, *ps_full = st_full + 4,
+           *ps_empty = st_full + 6, *acc_done = st_full + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(st_full + 9);
 
   const int nq = S / 128, BH = B * H;
   const int j = (int)blockIdx.x / BH;            // kv tile; small j = many q tiles, first
   const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
-  const int nit = nq - j, row0 = b * S;
+  const int nsub = 2 * (nq - j), row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(kv_full, 1); mbar_init(qdo_full, 1); mbar_init(qdo_empty, 1);
-    mbar_init(st_full, 1); mbar_init(st_free, 4); mbar_init(ps_full, 4);
-    mbar_init(ps_empty, 1); mbar_init(acc_done, 1);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < NST; ++s) { mbar_init(&qd_full[s], 1); mbar_init(&qd_empty[s], 1); }
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&st_full[g], 1); mbar_init(&st_free[g], GW);
+      mbar_init(&ps_full[g], GW); mbar_init(&ps_empty[g], 1);
+    }
+    mbar_init(acc_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm);
     prefetch_map(&tm_do);
@@ -321,97 +424,116 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
-  const uint32_t tmem = *tslot;
-  const uint32_t tST = tmem, tdPT = tmem + 128, tdV = tmem + 256, tdK = tmem + 384;
+  const uint32_t tmem = *tslot;   // slot g: S^T at g*128, dP^T at g*128 + 64; dV 256, dK 384
 
   if (warp == 0) {
     if (lane == 0) {
       mbar_expect_tx(kv_full, 2 * TB);
-      load_tile<D>(sK, &tm, kv_full, hd + h * D, row0 + j * 128);
-      load_tile<D>(sV, &tm, kv_full, 2 * hd + h * D, row0 + j * 128);
-      for (int it = 0; it < nit; ++it) {
-        const int i = j + it;
-        mbar_wait(qdo_empty, (it & 1) ^ 1);
-        mbar_expect_tx(qdo_full, 2 * TB);
-        load_tile<D>(sQ, &tm, qdo_full, h * D, row0 + i * 128);
-        load_tile<D>(sdO, &tm_do, qdo_full, h * D, row0 + i * 128);
+      load_rows<D, 128>(sK, &tm, kv_full, hd + h * D, row0 + j * 128);
+      load_rows<D, 128>(sV, &tm, kv_full, 2 * hd + h * D, row0 + j * 128);
+      for (int u = 0; u < nsub; ++u) {
+        const int st = u % NST, r = row0 + j * 128 + u * 64;   // q rows of sub-tile u
+        mbar_wait(&qd_empty[st], ((u / NST) & 1) ^ 1);
+        mbar_expect_tx(&qd_full[st], 2 * HB);
+        load_rows<D, 64>(sQD + st * 2 * HB, &tm, &qd_full[st], h * D, r);
+        load_rows<D, 64>(sQD + st * 2 * HB + HB, &tm_do, &qd_full[st], h * D, r);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16_f32(128, 128, false, false);
-      constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
-      mbar_wait(kv_full, 0);
-      for (int it = 0; it < nit; ++it) {
-        mbar_wait(qdo_full, it & 1);
-        if (it >= 1) mbar_wait(st_free, (it - 1) & 1);
+    constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
+    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
+    mbar_wait(kv_full, 0);
+    for (int u = 0; u <= nsub; ++u) {
+      if (u < nsub) {
+        const int st = u % NST, g = u & 1;
+        mbar_wait(&qd_full[st], (u / NST) & 1);
+        if (u >= 2) mbar_wait(&st_free[g], ((u - 2) >> 1) & 1);
         fence_after_sync();
-        mma_tile<false>(tST, sK, sQ, D / 16, id_s, false);
-        mma_tile<false>(tdPT, sV, sdO, D / 16, id_s, false);
-        umma_commit(st_full);
-        mbar_wait(ps_full, it & 1);
-        fence_after_sync();
-        mma_tile<true>(tdV, sPT, sdO, 8, id_d, it > 0);
-        mma_tile<true>(tdK, sdST, sQ, 8, id_d, it > 0);
-        umma_commit(qdo_empty);
-        umma_commit(ps_empty);
+        if (elect_one()) {
+          const uint8_t* q = sQD + st * 2 * HB;
+          mma_tile<64, false, D / 16>(tmem + g * 128, sK, q, id_s, false);
+          mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sV, q + HB, id_s, false);
+          umma_commit(&st_full[g]);
+        }
+        __syncwarp();
       }
-      umma_commit(acc_done);
+      if (u >= 1) {
+        const int v = u - 1, st = v % NST, g = v & 1;
+        mbar_wait(&ps_full[g], (v >> 1) & 1);
+        fence_after_sync();
+        if (elect_one()) {
+          const uint8_t* q = sQD + st * 2 * HB;
+          mma_tile<64, true, 4>(tmem + 256, sPT + g * 16384, q + HB, id_d, v > 0);
+          mma_tile<64, true, 4>(tmem + 384, sdST + g * 16384, q, id_d, v > 0);
+          umma_commit(&qd_empty[st]);
+          umma_commit(&ps_empty[g]);
+        }
+        __syncwarp();
+      }
     }
+    if (elect_one()) umma_commit(acc_done);
     __syncwarp();
   } else {
-    const int q4 = warp & 3, r = q4 * 32 + lane;
+    // thread = kv row r of the tile; group g owns the sub-tiles u = 2*it + g (64 q each)
+    const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tST = tmem + g * 128 + lo, tdPT = tST + 64;
+    uint8_t *sPTg = sPT + g * 16384, *sdSTg = sdST + g * 16384;
+    const int nit = nsub / 2;
     for (int it = 0; it < nit; ++it) {
-      const int i = j + it;
-      float* Ls = sLD + (it & 1) * 256;
-      Ls[r] = lse[(size_t)bh * S + i * 128 + r];
-      Ls[128 + r] = delta[(size_t)bh * S + i * 128 + r];
-      named_sync(1, 128);
-      mbar_wait(st_full, it & 1);
+      // lse / delta of the sub-tile's 64 queries: warp-uniform read-only loads (broadcast)
+      const size_t q0 = (size_t)bh * S + (j + it) * 128 + g * 64;
+      const float4* lq = reinterpret_cast<const float4*>(lse + q0);
+      const float4* dq4 = reinterpret_cast<const float4*>(delta + q0);
+      mbar_wait(&st_full[g], it & 1);
       fence_after_sync();
-      if (it >= 1) mbar_wait(ps_empty, (it - 1) & 1);
+      if (it >= 1) mbar_wait(&ps_empty[g], (it - 1) & 1);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t s32[32], p32[32];
-        tmem_ld32_nowait(tST + lo + c * 32, s32);
-        tmem_ld32_nowait(tdPT + lo + c * 32, p32);
+        tmem_ld32_nowait(tST + c * 32, s32);
+        tmem_ld32_nowait(tdPT + c * 32, p32);
+        float Ls[32], Ds[32];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 a = __ldg(lq + c * 8 + k), d = __ldg(dq4 + c * 8 + k);
+          Ls[4 * k] = a.x; Ls[4 * k + 1] = a.y; Ls[4 * k + 2] = a.z; Ls[4 * k + 3] = a.w;
+          Ds[4 * k] = d.x; Ds[4 * k + 1] = d.y; Ds[4 * k + 2] = d.z; Ds[4 * k + 3] = d.w;
+        }
         tmem_wait_ld();
         uint32_t pp[16], dd[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
           const int q = c * 32 + k;
-          float p0 = ex2(u2f(s32[k]) * sl2 - Ls[q]);
-          float p1 = ex2(u2f(s32[k + 1]) * sl2 - Ls[q + 1]);
+          float p0 = ex2(fmaf(u2f(s32[k]), sl2, -Ls[k]));
+          float p1 = ex2(fmaf(u2f(s32[k + 1]), sl2, -Ls[k + 1]));
           if (it == 0) {                          // diagonal tile: query before key
-            if (q < r) p0 = 0.f;
-            if (q + 1 < r) p1 = 0.f;
+            if (g * 64 + q < r) p0 = 0.f;
+            if (g * 64 + q + 1 < r) p1 = 0.f;
           }
-          const float d0 = p0 * (u2f(p32[k]) - Ls[128 + q]);
-          const float d1 = p1 * (u2f(p32[k + 1]) - Ls[128 + q + 1]);
           pp[k >> 1] = pack_bf16(p0, p1);
-          dd[k >> 1] = pack_bf16(d0, d1);
+          dd[k >> 1] = pack_bf16(p0 * (u2f(p32[k]) - Ds[k]), p1 * (u2f(p32[k + 1]) - Ds[k + 1]));
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          st_piece(sPT, r, c * 4 + g, make_uint4(pp[4 * g], pp[4 * g + 1], pp[4 * g + 2], pp[4 * g + 3]));
-          st_piece(sdST, r, c * 4 + g, make_uint4(dd[4 * g], dd[4 * g + 1], dd[4 * g + 2], dd[4 * g + 3]));
+        for (int q = 0; q < 4; ++q) {
+          st_piece(sPTg, r, c * 4 + q, make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]));
+          st_piece(sdSTg, r, c * 4 + q, make_uint4(dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]));
         }
       }
       fence_before_sync();
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(st_free);
-        mbar_arrive(ps_full);
+        mbar_arrive(&st_free[g]);
+        mbar_arrive(&ps_full[g]);
       }
     }
     mbar_wait(acc_done, 0);
     fence_after_sync();
     const size_t row = (size_t)row0 + j * 128 + r;
     __nv_bfloat16* d = dqkv + row * 3 * hd;
-    store_row<D>(tdV + lo, 1.f, d + 2 * hd + h * D);
-    store_row<D>(tdK + lo, scale, d + hd + h * D);
+    if (g == 0) store_row<D>(tmem + 256 + lo, 1.f, d + 2 * hd + h * D);
+    else store_row<D>(tmem + 384 + lo, scale, d + hd + h * D);
   }
   fence_before_sync();
   __syncthreads();
@@ -422,10 +544,11 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
 }
 
 // ======================================================================= backward: dQ
+// CTA = q tile i; sub-tiles over the kv columns (kv halves of tiles j <= i).
 template <int D>
 struct Bq {
-  static constexpr int TB = 128 * D * 2;
-  static constexpr int Q = 0, DO = TB, K = 2 * TB, V = 4 * TB, DS = 6 * TB, BAR = 6 * TB + PB;
+  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 4;   // kv half stages
+  static constexpr int Q = 0, DO = TB, KV = 2 * TB, DS = KV + NST * 2 * HB, BAR = DS + 2 * 16384;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -436,30 +559,30 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
               __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
               float scale) {
   using L = Bq<D>;
-  constexpr int TB = L::TB;
+  constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sQ = sm + L::Q, *sdO = sm + L::DO, *sK = sm + L::K, *sV = sm + L::V, *sdS = sm + L::DS;
+  uint8_t *sQ = sm + L::Q, *sdO = sm + L::DO, *sKV = sm + L::KV, *sdS = sm + L::DS;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t *qdo_full = bar, *k_full = bar + 1, *k_empty = bar + 3, *v_full = bar + 5,
-           *v_empty = bar + 7, *s_full = bar + 9, *s_free = bar + 10, *ds_full = bar + 11,
-           *ds_empty = bar + 12, *acc_done = bar + 13;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 14);
+  uint64_t *qd_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + NST,
+           *s_full = bar + 1 + 2 * NST, *s_free = s_full + 2, *ds_full = s_full + 4,
+           *ds_empty = s_full + 6, *acc_done = s_full + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 9);
 
   const int nq = S / 128, BH = B * H;
   const int i = nq - 1 - (int)blockIdx.x / BH;
   const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
-  const int nkv = i + 1, row0 = b * S;
+  const int nsub = 2 * (i + 1), row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
-    mbar_init(qdo_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1);
+    mbar_init(qd_full, 1);
+    for (int s = 0; s < NST; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&s_full[g], 1); mbar_init(&s_free[g], GW);
+      mbar_init(&ds_full[g], GW); mbar_init(&ds_empty[g], 1);
     }
-    mbar_init(s_full, 1); mbar_init(s_free, 4); mbar_init(ds_full, 4);
-    mbar_init(ds_empty, 1); mbar_init(acc_done, 1);
+    mbar_init(acc_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm);
     prefetch_map(&tm_do);
@@ -468,93 +591,100 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
-  const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem, tdP = tmem + 128, tdQ = tmem + 256;
+  const uint32_t tmem = *tslot;   // slot g: S at g*128, dP at g*128 + 64; dQ at 256
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(qdo_full, 2 * TB);
-      load_tile<D>(sQ, &tm, qdo_full, h * D, row0 + i * 128);
-      load_tile<D>(sdO, &tm_do, qdo_full, h * D, row0 + i * 128);
-      for (int jj = 0; jj < nkv; ++jj) {
-        const int s = jj & 1;
-        const uint32_t ph = (jj >> 1) & 1;
-        mbar_wait(&k_empty[s], ph ^ 1);
-        mbar_expect_tx(&k_full[s], TB);
-        load_tile<D>(sK + s * TB, &tm, &k_full[s], hd + h * D, row0 + jj * 128);
-        mbar_wait(&v_empty[s], ph ^ 1);
-        mbar_expect_tx(&v_full[s], TB);
-        load_tile<D>(sV + s * TB, &tm, &v_full[s], 2 * hd + h * D, row0 + jj * 128);
+      mbar_expect_tx(qd_full, 2 * TB);
+      load_rows<D, 128>(sQ, &tm, qd_full, h * D, row0 + i * 128);
+      load_rows<D, 128>(sdO, &tm_do, qd_full, h * D, row0 + i * 128);
+      for (int u = 0; u < nsub; ++u) {
+        const int st = u % NST, r = row0 + u * 64;      // kv rows of sub-tile u
+        mbar_wait(&kv_empty[st], ((u / NST) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * HB);
+        load_rows<D, 64>(sKV + st * 2 * HB, &tm, &kv_full[st], hd + h * D, r);
+        load_rows<D, 64>(sKV + st * 2 * HB + HB, &tm, &kv_full[st], 2 * hd + h * D, r);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t id_s = idesc_bf16_f32(128, 128, false, false);
-      constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
-      mbar_wait(qdo_full, 0);
-      for (int jj = 0; jj < nkv; ++jj) {
-        const int s = jj & 1;
-        const uint32_t ph = (jj >> 1) & 1;
-        mbar_wait(&k_full[s], ph);
-        mbar_wait(&v_full[s], ph);
-        if (jj >= 1) mbar_wait(s_free, (jj - 1) & 1);
+    constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
+    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
+    mbar_wait(qd_full, 0);
+    for (int u = 0; u <= nsub; ++u) {
+      if (u < nsub) {
+        const int st = u % NST, g = u & 1;
+        mbar_wait(&kv_full[st], (u / NST) & 1);
+        if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
         fence_after_sync();
-        mma_tile<false>(tS, sQ, sK + s * TB, D / 16, id_s, false);
-        mma_tile<false>(tdP, sdO, sV + s * TB, D / 16, id_s, false);
-        umma_commit(&v_empty[s]);
-        umma_commit(s_full);
-        mbar_wait(ds_full, jj & 1);
-        fence_after_sync();
-        mma_tile<true>(tdQ, sdS, sK + s * TB, 8, id_d, jj > 0);
-        umma_commit(&k_empty[s]);
-        umma_commit(ds_empty);
+        if (elect_one()) {
+          const uint8_t* kv = sKV + st * 2 * HB;
+          mma_tile<64, false, D / 16>(tmem + g * 128, sQ, kv, id_s, false);
+          mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sdO, kv + HB, id_s, false);
+          umma_commit(&s_full[g]);
+        }
+        __syncwarp();
       }
-      umma_commit(acc_done);
+      if (u >= 1) {
+        const int v = u - 1, st = v % NST, g = v & 1;
+        mbar_wait(&ds_full[g], (v >> 1) & 1);
+        fence_after_sync();
+        if (elect_one()) {
+          mma_tile<64, true, 4>(tmem + 256, sdS + g * 16384, sKV + st * 2 * HB, id_d, v > 0);
+          umma_commit(&kv_empty[st]);
+          umma_commit(&ds_empty[g]);
+        }
+        __syncwarp();
+      }
     }
+    if (elect_one()) umma_commit(acc_done);
     __syncwarp();
   } else {
-    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
-    const float lse_r = lse[(size_t)bh * S + i * 128 + r];
-    const float del_r = delta[(size_t)bh * S + i * 128 + r];
-    for (int jj = 0; jj < nkv; ++jj) {
-      mbar_wait(s_full, jj & 1);
+    const uint32_t tSg = tmem + g * 128 + lo, tdPg = tSg + 64;
+    uint8_t* sdSg = sdS + g * 16384;
+    const float nl = -lse[(size_t)bh * S + i * 128 + r];
+    const float del = delta[(size_t)bh * S + i * 128 + r];
+    const int nit = nsub / 2;
+    for (int jj = 0; jj < nit; ++jj) {
+      mbar_wait(&s_full[g], jj & 1);
       fence_after_sync();
-      if (jj >= 1) mbar_wait(ds_empty, (jj - 1) & 1);
+      if (jj >= 1) mbar_wait(&ds_empty[g], (jj - 1) & 1);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t s32[32], p32[32];
-        tmem_ld32_nowait(tS + lo + c * 32, s32);
-        tmem_ld32_nowait(tdP + lo + c * 32, p32);
+        tmem_ld32_nowait(tSg + c * 32, s32);
+        tmem_ld32_nowait(tdPg + c * 32, p32);
         tmem_wait_ld();
         uint32_t dd[16];
 #pragma unroll
         for (int k = 0; k < 32; k += 2) {
-          const int kv = c * 32 + k;
-          float p0 = ex2(u2f(s32[k]) * sl2 - lse_r);
-          float p1 = ex2(u2f(s32[k + 1]) * sl2 - lse_r);
+          const int kv = g * 64 + c * 32 + k;
+          float p0 = ex2(fmaf(u2f(s32[k]), sl2, nl));
+          float p1 = ex2(fmaf(u2f(s32[k + 1]), sl2, nl));
           if (jj == i) {                          // diagonal tile: key after query
             if (kv > r) p0 = 0.f;
             if (kv + 1 > r) p1 = 0.f;
           }
-          dd[k >> 1] = pack_bf16(p0 * (u2f(p32[k]) - del_r), p1 * (u2f(p32[k + 1]) - del_r));
+          dd[k >> 1] = pack_bf16(p0 * (u2f(p32[k]) - del), p1 * (u2f(p32[k + 1]) - del));
         }
 #pragma unroll
-        for (int g = 0; g < 4; ++g)
-          st_piece(sdS, r, c * 4 + g, make_uint4(dd[4 * g], dd[4 * g + 1], dd[4 * g + 2], dd[4 * g + 3]));
+        for (int q = 0; q < 4; ++q)
+          st_piece(sdSg, r, c * 4 + q, make_uint4(dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]));
       }
       fence_before_sync();
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(s_free);
-        mbar_arrive(ds_full);
+        mbar_arrive(&s_free[g]);
+        mbar_arrive(&ds_full[g]);
       }
     }
     mbar_wait(acc_done, 0);
     fence_after_sync();
     const size_t row = (size_t)row0 + i * 128 + r;
-    store_row<D>(tdQ + lo, scale, dqkv + row * 3 * hd + h * D);
+    store_row<D / 2>(tmem + 256 + lo + g * (D / 2), scale,
+                     dqkv + row * 3 * hd + h * D + g * (D / 2));
   }
   fence_before_sync();
   __syncthreads();
@@ -593,6 +723,7 @@ __global__ void delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfl
 
 // ------------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static unsigned long long* g_trace = nullptr;   // zi_attn_set_trace (diagnostics)
 
 static int encoder() {
   if (g_encode) return ZI_OK;
@@ -653,7 +784,7 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
   if ((rc = set_smem(fwd_kernel<D>, Fwd<D>::BYTES, attr)) != ZI_OK) return rc;
   const float sl2 = LOG2E / sqrtf((float)D);
   fwd_kernel<D><<<B * H * (S / 128), THREADS, Fwd<D>::BYTES, st>>>(
-      tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2);
+      tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace);
   return launch_status("zi_attn_fwd");
 }
 
@@ -687,6 +818,11 @@ static int bwd(const void* qkv, const void* out, const void* dout, const float* 
 }  // namespace zi
 
 extern "C" {
+
+int zi_attn_set_trace(void* buf) {
+  zi::attn::g_trace = static_cast<unsigned long long*>(buf);
+  return ZI_OK;
+}
 
 int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int head_dim,
                 void* stream) {

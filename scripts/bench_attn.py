@@ -27,7 +27,9 @@ def timeit(fn, n=20):
 
 
 def main():
-    B, H, S, D = (int(x) for x in sys.argv[1:5]) if len(sys.argv) >= 5 else (8, 16, 1024, 128)
+    once = "--once" in sys.argv
+    argv = [a for a in sys.argv[1:] if a != "--once"]
+    B, H, S, D = (int(x) for x in argv[:4]) if len(argv) >= 4 else (8, 16, 1024, 128)
     qkv = torch.randn(B * S, 3 * H * D, device="cuda").bfloat16()
     out = torch.empty(B * S, H * D, device="cuda", dtype=torch.bfloat16)
     lse = torch.empty(B * H * S, device="cuda")
@@ -35,6 +37,58 @@ def main():
     dout = torch.randn_like(out)
     dqkv = torch.empty_like(qkv)
     unit = 2.0 * B * H * S * S * D / 2      # one causal matmul
+    if "--trace" in sys.argv:               # per-CTA timeline of the forward
+        from paper_2104_07857_b200 import _lib
+        nct = B * H * (S // 128)
+        tr = torch.zeros(nct * 6 + 2 * 64 * 6 + 32 * 4, dtype=torch.int64, device="cuda")
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        torch.cuda.synchronize()
+        _lib.call("zi_attn_set_trace", tr.data_ptr())
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        torch.cuda.synchronize()
+        _lib.call("zi_attn_set_trace", None)
+        fine = tr[nct * 6:nct * 6 + 768].view(2, 64, 6).cpu().double()
+        mm = tr[nct * 6 + 768:].view(32, 4).cpu().double()
+        t = tr[:nct * 6].view(nct, 6).cpu().double()
+        t0 = t[:, 1].min()
+        t[:, 1:] -= t0
+        t[:, 1:] /= 1000.0
+        print("kernel span us", float(t[:, 5].max()))
+        for name, a, b in (("entry->operands", 1, 2), ("operands->last mma", 2, 3),
+                           ("last mma->softmax done", 3, 4), ("softmax done->exit", 4, 5),
+                           ("cta total", 1, 5)):
+            d = t[:, b] - t[:, a]
+            print(f"{name:24s} mean {float(d.mean()):6.2f} us  max {float(d.max()):6.2f}")
+        # gaps between consecutive CTAs on one SM
+        gaps = []
+        for sm in t[:, 0].unique():
+            rows = t[t[:, 0] == sm]
+            rows = rows[rows[:, 1].argsort()]
+            gaps += (rows[1:, 1] - rows[:-1, 5]).tolist()
+        g = torch.tensor(gaps)
+        print(f"inter-CTA gap on an SM: mean {float(g.mean()):.2f} us max {float(g.max()):.2f}; "
+              f"CTAs per SM {nct / t[:, 0].unique().numel():.1f}")
+        for g in range(2):
+            f = fine[g]
+            base = f[0, 0]
+            print(f"group {g} sub-tiles of CTA 0 (kcycles from its first wait): "
+                  "[start, S ready, S loaded, exps done, pv waited, P published]")
+            for jj in range(S // 128):
+                print("   ", [round(float(x - base) / 1000, 2) for x in f[jj]])
+        base = fine[0, 0, 0]
+        print("MMA thread of CTA 0 per u: [loop top, kv landed, s_free, p_full(u-1)] kcycles")
+        for u in range(2 * (S // 128) + 1):
+            print("   ", u, [round(float(x - base) / 1000, 2) if x > 0 else None for x in mm[u]])
+        for nkv in (1, 4, 8):
+            rows = t[(torch.arange(nct) // (B * H)) == (S // 128 - nkv)]
+            print(f"  nkv={nkv}: cta {float((rows[:, 5] - rows[:, 1]).mean()):.2f} us, "
+                  f"mma {float((rows[:, 3] - rows[:, 2]).mean()):.2f} us")
+        return
+    if once:                                 # one launch of each kernel (for ncu)
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        kernels.attn_bwd(qkv, out, dout, lse, delta, dqkv, B, H)
+        torch.cuda.synchronize()
+        return
     t_f = timeit(lambda: kernels.attn_fwd(qkv, out, lse, B, H))
     t_b = timeit(lambda: kernels.attn_bwd(qkv, out, dout, lse, delta, dqkv, B, H))
     leaf = qkv.detach().requires_grad_(True)
