@@ -330,6 +330,12 @@ int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int
                 void* stream);
 int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
                 void* dqkv, int B, int H, int S, int head_dim, void* stream);
+/* Tied-embedding gradient in a fixed order (csrc/embed.cu): out[v] = half_RNE(acc[v] +
+ * sum of dx[t] over the tokens t with id v, in sequence order). tokens int64 [T]; dx
+ * [T, hd] bf16 (dx_f32 = 0) or fp32; acc fp32 [V, hd]; out half [V, hd]; work int32
+ * [2*V + 1 + T]. Deterministic: counting sort with stable ranks, no float atomics. */
+int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, const float* acc, int V,
+                  int hd, void* out, int half_kind, int* work, void* stream);
 /* Diagnostics: per-CTA globaltimer records of zi_attn_fwd into buf (6 u64 per CTA: sm,
  * entry, operands in, last MMA issued, softmax done, exit); NULL turns it off. */
 int zi_attn_set_trace(void* buf);

@@ -121,6 +121,8 @@ SIGNATURES = {
                 c_int, c_int, c_int, c_int, c_void_p],
     "zi_gemm_set_profile": [c_void_p],
     "zi_attn_set_trace": [c_void_p],
+    "zi_embed_grad": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_int,
+                      c_void_p, c_void_p],
     "zi_attn_fwd": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
     "zi_attn_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                     c_int, c_void_p],

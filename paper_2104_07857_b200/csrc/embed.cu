@@ -1,0 +1,155 @@
+// Tied-embedding gradient in a fixed order (reductions in fixed order).
+//
+//   out[v, :] = half_RNE( acc[v, :] + sum_{t : tokens[t] == v, t ascending} dx[t, :] )
+//
+// acc is the head's fp32 contribution (dlogits^T hf, written by the head.dW GEMM); dx the
+// gradient reaching the embedding lookup. A scatter-add (index_add_) would sum a row's
+// tokens in whatever order its atomics land; here the tokens are counting-sorted by id
+// with a stable rank (the number of earlier equal ids), so every row sums its tokens in
+// sequence order and the gradient is bitwise reproducible.
+//
+//   count   counts[v] = #tokens with id v (integer atomics: order-free)
+//   scan    offsets = exclusive prefix sum of counts (one CTA)
+//   place   order[offsets[id_t] + rank_t] = t, rank_t = #{t' < t : id_t' == id_t}
+//   rows    one CTA per vocabulary row: fold acc + dx rows in order, round, store
+#include "common.cuh"
+
+namespace zi {
+namespace emb {
+
+__global__ void count_kernel(const int64_t* __restrict__ tok, int T, int V, int* __restrict__ counts) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) {
+    const int64_t v = tok[t];
+    if (v >= 0 && v < V) atomicAdd(&counts[v], 1);
+  }
+}
+
+// exclusive scan of counts[0..V) into offsets[0..V] (offsets[V] = T); one CTA of 1024
+__global__ void scan_kernel(const int* __restrict__ counts, int V, int* __restrict__ offsets) {
+  __shared__ int part[1024];
+  const int tid = threadIdx.x, per = (V + 1023) / 1024;
+  const int lo = min(V, tid * per), hi = min(V, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += counts[i];
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {           // Hillis-Steele inclusive scan
+    const int x = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += x;
+    __syncthreads();
+  }
+  int run = tid ? part[tid - 1] : 0;
+  for (int i = lo; i < hi; ++i) {
+    offsets[i] = run;
+    run += counts[i];
+  }
+  if (tid == 1023) offsets[V] = part[1023];
+}
+
+// stable placement: tokens staged in shared memory as int32
+__global__ void place_kernel(const int64_t* __restrict__ tok, int T, int V,
+                             const int* __restrict__ offsets, int* __restrict__ order) {
+  extern __shared__ int st[];
+  for (int i = threadIdx.x; i < T; i += blockDim.x) st[i] = (int)tok[i];
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const int v = st[t];
+  if (v < 0 || v >= V) return;
+  int rank = 0;
+  for (int k = 0; k < t; ++k) rank += (st[k] == v);
+  order[offsets[v] + rank] = t;
+}
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
+  const uint4 g = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 x = __bfloat1622float2(g2[q]);
+    f[2 * q] = x.x;
+    f[2 * q + 1] = x.y;
+  }
+}
+__device__ __forceinline__ void load8(const float* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+template <int KIND, typename TX>
+__global__ void rows_kernel(const TX* __restrict__ dx, const float* __restrict__ acc,
+                            const int* __restrict__ offsets, const int* __restrict__ order, int hd,
+                            uint16_t* __restrict__ out) {
+  const int v = blockIdx.x;
+  const int e = threadIdx.x * 8;                 // 8 consecutive elements per thread
+  if (e >= hd) return;
+  const size_t base = (size_t)v * hd + e;
+  const float4 a0 = *reinterpret_cast<const float4*>(acc + base);
+  const float4 a1 = *reinterpret_cast<const float4*>(acc + base + 4);
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const int k0 = offsets[v], k1 = offsets[v + 1];
+  for (int k = k0; k < k1; ++k) {                // the row's tokens in sequence order
+    float f[8];
+    load8(dx + (size_t)order[k] * hd + e, f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] += f[q];
+  }
+  const float r[8] = {a0.x + s[0], a0.y + s[1], a0.z + s[2], a0.w + s[3],
+                      a1.x + s[4], a1.y + s[5], a1.z + s[6], a1.w + s[7]};
+  uint4 o;
+  o.x = (uint32_t)Half<KIND>::narrow(r[0]) | ((uint32_t)Half<KIND>::narrow(r[1]) << 16);
+  o.y = (uint32_t)Half<KIND>::narrow(r[2]) | ((uint32_t)Half<KIND>::narrow(r[3]) << 16);
+  o.z = (uint32_t)Half<KIND>::narrow(r[4]) | ((uint32_t)Half<KIND>::narrow(r[5]) << 16);
+  o.w = (uint32_t)Half<KIND>::narrow(r[6]) | ((uint32_t)Half<KIND>::narrow(r[7]) << 16);
+  *reinterpret_cast<uint4*>(out + base) = o;
+}
+
+}  // namespace emb
+}  // namespace zi
+
+extern "C" {
+
+int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, const float* acc, int V,
+                  int hd, void* out, int half_kind, int* work, void* stream) {
+  ZI_CHECK_ARG(tokens && dx && acc && out && work, "zi_embed_grad: NULL argument");
+  ZI_CHECK_ARG(T >= 1 && V >= 1 && hd >= 8 && hd % 8 == 0 && hd / 8 <= 1024,
+               "zi_embed_grad: bad T/V/hd %d/%d/%d", T, V, hd);
+  ZI_CHECK_ARG((size_t)T * 4 <= 200 * 1024, "zi_embed_grad: T=%d tokens exceed the staging", T);
+  ZI_CHECK_ARG(half_kind == ZI_HALF_BF16 || half_kind == ZI_HALF_FP16,
+               "zi_embed_grad: bad half_kind %d", half_kind);
+  ZI_CHECK_ARG(zi::aligned(dx, 16) && zi::aligned(acc, 16) && zi::aligned(out, 16),
+               "zi_embed_grad: 16-byte alignment");
+  cudaStream_t s = (cudaStream_t)stream;
+  int* counts = work;              // [V]
+  int* offsets = work + V;         // [V + 1]
+  int* order = offsets + V + 1;    // [T]
+  ZI_CUDA(cudaMemsetAsync(counts, 0, (size_t)V * sizeof(int), s), "zi_embed_grad: memset");
+  zi::emb::count_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, T, V, counts);
+  zi::emb::scan_kernel<<<1, 1024, 0, s>>>(counts, V, offsets);
+  const size_t sh = (size_t)T * sizeof(int);
+  if (sh > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      ZI_CUDA(cudaFuncSetAttribute(zi::emb::place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024), "cudaFuncSetAttribute(place)");
+      attr = true;
+    }
+  }
+  zi::emb::place_kernel<<<(T + 255) / 256, 256, sh, s>>>(tokens, T, V, offsets, order);
+  const int threads = ((hd / 8 + 31) / 32) * 32;
+  auto* o = static_cast<uint16_t*>(out);
+  const auto* xb = static_cast<const __nv_bfloat16*>(dx);
+  const auto* xf = static_cast<const float*>(dx);
+  if (half_kind == ZI_HALF_BF16) {
+    if (dx_f32) zi::emb::rows_kernel<ZI_HALF_BF16><<<V, threads, 0, s>>>(xf, acc, offsets, order, hd, o);
+    else zi::emb::rows_kernel<ZI_HALF_BF16><<<V, threads, 0, s>>>(xb, acc, offsets, order, hd, o);
+  } else {
+    if (dx_f32) zi::emb::rows_kernel<ZI_HALF_FP16><<<V, threads, 0, s>>>(xf, acc, offsets, order, hd, o);
+    else zi::emb::rows_kernel<ZI_HALF_FP16><<<V, threads, 0, s>>>(xb, acc, offsets, order, hd, o);
+  }
+  return zi::launch_status("zi_embed_grad");
+}
+
+}  // extern "C"

@@ -183,6 +183,8 @@ class GPTZeroEngine:
         self.seed = seed
         self.half = half_dtype
         self.cdt = compute_dtype or half_dtype
+        if self.cdt == torch.bfloat16 and (cfg.seq % 128 or cfg.head_dim not in (64, 128)):
+            raise ValueError("bf16 attention (zi_attn) needs seq % 128 == 0 and head_dim 64 or 128")
         self.placement = placement or Placement()
         if self.placement.params not in (TierKind.DEVICE, TierKind.HOST):
             raise NotImplementedError("bf16 params: DEVICE or HOST tier")
@@ -401,6 +403,7 @@ class GPTZeroEngine:
             self.gwide = [torch.zeros(maxn, dtype=self.cdt, device=self.dev) for _ in range(nloc)]
         self.wte_acc = [torch.zeros(c.vocab, c.hd, dtype=torch.float32, device=self.dev)
                         for _ in range(nloc)]
+        self.emb_work = torch.empty(2 * c.vocab + 1 + c.tokens, dtype=torch.int32, device=self.dev)
         if not self.comm.is_local and self.N > 1:
             self.peer_gslots = [self.comm.share(self.gslots[0][k]) for k in range(2)]
             self.peer_gembed = self.comm.share(self.gembed[0])
@@ -620,8 +623,17 @@ class GPTZeroEngine:
         return x.reshape(-1, c.hd)
 
     def _attn_fwd(self, qkv):
+        """Causal attention of the block. bf16: libzinf's tcgen05 kernels (zi_attn_fwd; the
+        backward is fixed-order, so the step is bitwise reproducible). fp32 / fp16
+        compute (the SPEC-parity modes): the same math through torch's SDPA in that dtype."""
         c = self.cfg
         B, S, H, D = c.batch, c.seq, c.heads, c.head_dim
+        if self.cdt == torch.bfloat16:
+            o = torch.empty(B * S, c.hd, dtype=qkv.dtype, device=qkv.device)
+            lse = torch.empty(B * H * S, dtype=torch.float32, device=qkv.device)
+            kernels.attn_fwd(qkv, o, lse, B, H)
+            self.launches += 1
+            return o, (qkv, o, lse)
         leaf = qkv.detach().requires_grad_(True)
         with torch.enable_grad():
             q, k, v = leaf.view(B, S, 3, H, D).unbind(2)
@@ -632,6 +644,13 @@ class GPTZeroEngine:
 
     def _attn_bwd(self, do, saved):
         c = self.cfg
+        if self.cdt == torch.bfloat16:
+            qkv, o, lse = saved
+            dqkv = torch.empty_like(qkv)
+            delta = torch.empty_like(lse)
+            kernels.attn_bwd(qkv, o, do, lse, delta, dqkv, c.batch, c.heads)
+            self.launches += 3
+            return dqkv
         leaf, o4 = saved
         g4 = do.view(c.batch, c.seq, c.heads, c.head_dim).transpose(1, 2)
         (dqkv,) = torch.autograd.grad(o4, leaf, g4)
@@ -1240,16 +1259,20 @@ class GPTZeroEngine:
         for li in range(nloc):
             G, flat = self._grad_views(li, E, 0)
             tok = batches[li][0].reshape(-1)
-            acc = self.wte_acc[li]
-            acc.index_add_(0, tok, xs[li].float())
             dwpe = xs[li].view(c.batch, c.seq, c.hd).sum(0, dtype=torch.float32)
+            # tied wte: head contribution + the lookup's gradient rows, summed per vocabulary
+            # row in sequence order (zi_embed_grad: no float atomics) and rounded to half
             if G["wte"].dtype == torch.float32:
-                G["wte"].copy_(acc)
+                wte16 = torch.empty(c.vocab, c.hd, dtype=self.half, device=self.dev)
+                kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], wte16, self.emb_work)
+                kernels.cast_half_to_f32(wte16.view(-1), G["wte"].view(-1))
                 G["wpe"].copy_(dwpe)
-            else:  # fp32 accumulators -> RNE half contributions (SPEC.md:750)
-                kernels.cast_f32_to_half(acc.view(-1), G["wte"].view(-1))
-                kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
                 self.launches += 2
+            else:  # fp32 accumulators -> RNE half contributions (SPEC.md:750)
+                kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], G["wte"],
+                                   self.emb_work)
+                kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
+                self.launches += 5
             self._finish_grad(li, E, 0, flat)
         self._tspan(E.op, "compute", c0, self._tmark(cur))
         self._reduce_update(E, 0, consts)

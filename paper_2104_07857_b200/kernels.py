@@ -426,3 +426,20 @@ def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torc
     _lib.call("zi_attn_bwd", _dev(qkv, "qkv"), _dev(out, "out"), _dev(dout, "dout"),
               _dev(lse, "lse"), _dev(delta, "delta"), _dev(dqkv, "dqkv"), batch, heads, S, D,
               _stream(stream))
+
+
+def embed_grad(tokens: torch.Tensor, dx: torch.Tensor, acc: torch.Tensor, out: torch.Tensor,
+               work: torch.Tensor, stream=None) -> None:
+    """zi_embed_grad: out[v] = RNE(acc[v] + sum of dx rows of the tokens with id v, in
+    sequence order) — the tied wte gradient without float atomics."""
+    T = tokens.numel()
+    V, hd = acc.shape
+    if tokens.dtype != torch.int64 or dx.shape != (T, hd) or dx.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("tokens int64 [T]; dx bf16 / fp32 [T, hd]")
+    if acc.dtype != torch.float32 or out.shape != (V, hd):
+        raise ValueError("acc fp32 [V, hd]; out half [V, hd]")
+    if work.dtype != torch.int32 or work.numel() < 2 * V + 1 + T:
+        raise ValueError("work must be int32 with 2*V + 1 + T elements")
+    _lib.call("zi_embed_grad", _dev(tokens.reshape(-1), "tokens"), T, _dev(dx, "dx"),
+              int(dx.dtype == torch.float32), _dev(acc, "acc"), V, hd, _dev(out, "out"),
+              half_kind(out.dtype), _dev(work, "work"), _stream(stream))

@@ -26,7 +26,7 @@ spec = H.ModelSpec([L("linear", 8, 16, "relu"), L("tiled_linear", 16, 16, "gelu-
 with tempfile.TemporaryDirectory() as d, TierStore(1 << 30, 1 << 30, nvme_root=d) as st:
     H.run_training(spec, 2, H.HarnessPlacement.all(TierKind.DEVICE), 3, 7, st)
 
-c = eg.GPTConfig(nl=3, hd=128, heads=2, seq=64, vocab=256, batch=2)
+c = eg.GPTConfig(nl=3, hd=128, heads=2, seq=128, vocab=256, batch=2)
 pl = eg.Placement(TierKind.HOST, TierKind.HOST)
 eng = eg.GPTZeroEngine(c, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007,
                        param_cache=1, gemm_select="zi")

@@ -9,7 +9,7 @@ from paper_2104_07857_b200 import gpt as eg  # noqa: E402
 from paper_2104_07857_b200.comm import LocalComm  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "zi"
-c = eg.GPTConfig(nl=2, hd=128, heads=2, seq=64, vocab=256, batch=2)
+c = eg.GPTConfig(nl=2, hd=128, heads=2, seq=128, vocab=256, batch=2)
 eng = eg.GPTZeroEngine(c, LocalComm(2), lr=1e-3, gemm_select=mode)
 for s in range(2):
     eng.step([eg.synthetic_tokens(c, 7, r, s) for r in range(2)]).item()
