@@ -48,19 +48,25 @@ __global__ void scan_kernel(const int* __restrict__ counts, int V, int* __restri
   if (tid == 1023) offsets[V] = part[1023];
 }
 
-// stable placement: tokens staged in shared memory as int32
+// stable placement; earlier tokens stream through shared memory in tiles of int32 ids
+constexpr int PLACE_TILE = 8192;
+
 __global__ void place_kernel(const int64_t* __restrict__ tok, int T, int V,
                              const int* __restrict__ offsets, int* __restrict__ order) {
-  extern __shared__ int st[];
-  for (int i = threadIdx.x; i < T; i += blockDim.x) st[i] = (int)tok[i];
-  __syncthreads();
+  __shared__ int st[PLACE_TILE];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= T) return;
-  const int v = st[t];
-  if (v < 0 || v >= V) return;
+  const int v = t < T ? (int)tok[t] : -1;
+  const int tmax = min(T, (int)((blockIdx.x + 1) * blockDim.x));   // the block's last t + 1
   int rank = 0;
-  for (int k = 0; k < t; ++k) rank += (st[k] == v);
-  order[offsets[v] + rank] = t;
+  for (int k0 = 0; k0 < tmax; k0 += PLACE_TILE) {
+    const int n = min(PLACE_TILE, T - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) st[i] = (int)tok[k0 + i];
+    __syncthreads();
+    const int kend = min(n, t - k0);
+    for (int k = 0; k < kend; ++k) rank += (st[k] == v);
+  }
+  if (t < T && v >= 0 && v < V) order[offsets[v] + rank] = t;
 }
 
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
@@ -116,7 +122,6 @@ int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, cons
   ZI_CHECK_ARG(tokens && dx && acc && out && work, "zi_embed_grad: NULL argument");
   ZI_CHECK_ARG(T >= 1 && V >= 1 && hd >= 8 && hd % 8 == 0 && hd / 8 <= 1024,
                "zi_embed_grad: bad T/V/hd %d/%d/%d", T, V, hd);
-  ZI_CHECK_ARG((size_t)T * 4 <= 200 * 1024, "zi_embed_grad: T=%d tokens exceed the staging", T);
   ZI_CHECK_ARG(half_kind == ZI_HALF_BF16 || half_kind == ZI_HALF_FP16,
                "zi_embed_grad: bad half_kind %d", half_kind);
   ZI_CHECK_ARG(zi::aligned(dx, 16) && zi::aligned(acc, 16) && zi::aligned(out, 16),
@@ -128,16 +133,7 @@ int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, cons
   ZI_CUDA(cudaMemsetAsync(counts, 0, (size_t)V * sizeof(int), s), "zi_embed_grad: memset");
   zi::emb::count_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, T, V, counts);
   zi::emb::scan_kernel<<<1, 1024, 0, s>>>(counts, V, offsets);
-  const size_t sh = (size_t)T * sizeof(int);
-  if (sh > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      ZI_CUDA(cudaFuncSetAttribute(zi::emb::place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024), "cudaFuncSetAttribute(place)");
-      attr = true;
-    }
-  }
-  zi::emb::place_kernel<<<(T + 255) / 256, 256, sh, s>>>(tokens, T, V, offsets, order);
+  zi::emb::place_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, T, V, offsets, order);
   const int threads = ((hd / 8 + 31) / 32) * 32;
   auto* o = static_cast<uint16_t*>(out);
   const auto* xb = static_cast<const __nv_bfloat16*>(dx);
