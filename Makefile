@@ -10,7 +10,7 @@ LIB := paper_2104_07857_b200/libzinf.so
 
 all: $(LIB)
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/bulk.cuh include/zinf.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/common.cuh $(CSRC)/bulk.cuh $(CSRC)/tc.cuh include/zinf.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 

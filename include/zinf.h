@@ -317,6 +317,18 @@ enum { ZI_EPI_PLAIN = 0, ZI_EPI_GELU = 1, ZI_EPI_RESID = 2, ZI_EPI_DGELU = 3 };
 int zi_gemm_ex(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
                const void* bias, void* D, int ldd, const void* X, int ldx, void* D2, int ldd2,
                int epi, int M, int N, int K, void* stream);
+/* Stream-K GEMM behind the GPT step's linears (csrc/gemm_sk.cu): 2-SM 256 x 256 pair
+ * tiles, two TMEM accumulators, and a hybrid stream-K schedule that deals the last
+ * waves' k-blocks evenly over the CTA pairs. Same operands and epilogues as
+ * zi_gemm_ex; d_f32 = 1 writes fp32 D (epi = ZI_EPI_PLAIN, no bias). ws (256-byte
+ * aligned, >= zi_gemm_sk_workspace_bytes(), zeroed once before first use; its flags
+ * reset themselves) enables the split; ws = NULL runs whole tiles. One workspace per
+ * stream: launches sharing one must be stream-ordered. Results are deterministic
+ * (partials summed in a fixed order) for a given device. */
+size_t zi_gemm_sk_workspace_bytes(void);
+int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
+               const void* bias, void* D, int ldd, int d_f32, const void* X, int ldx, void* D2,
+               int ldd2, int epi, int M, int N, int K, void* ws, size_t ws_bytes, void* stream);
 /* Diagnostics: a device buffer of >= 148*16*8 u64 receiving clock64() stamps of the
  * wide-tile GEMM's pipeline (NULL turns it off). Not for production use. */
 int zi_gemm_set_profile(void* buf);

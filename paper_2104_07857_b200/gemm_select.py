@@ -1,16 +1,14 @@
-"""Per-shape choice between libzinf's tcgen05 GEMM and cuBLAS for the GPT step's linears.
+"""zi_gemm_sk vs cuBLAS on the GPT step's linears: the A/B comparison behind the bench's
+``gemm_sites`` column (and the engine's opt-in ``gemm_select="auto"`` mode).
 
-The step's GEMMs are plain library-shaped products, and at the GPT shapes (K = 2048 ..
-50304) neither implementation wins everywhere: zi_gemm beats cuBLAS on some input- and
-weight-gradient shapes, cuBLAS on most forwards (scripts/bench_gemm.py). Each linear of the
-block and the head is therefore one *site* with two candidate implementations that compute
-the same outputs — the zi candidate may fold the neighbouring elementwise pass into its
-epilogue (bias + GELU, bias + residual, GELU' for the fc1 gradient), the cuBLAS candidate
-runs that pass as a separate libzinf / torch kernel. ``tune`` times both on the site's real
-shapes with CUDA events (interleaved, best of several) once per process and caches the
-winner, so every engine in the process makes the same choice (results stay comparable).
+Each linear of the block and the head is one *site*. The product path runs every site on
+zi_gemm_sk (tcgen05 stream-K; the neighbouring elementwise pass folded into its epilogue
+where the site has one: bias + GELU, bias + residual, GELU' for the fc1 gradient). The
+cuBLAS candidate computes the same outputs with the pass as a separate libzinf / torch
+kernel. ``tune`` times both on the site's real shapes with CUDA events (interleaved, best
+of several) once per process and caches the result.
 
-``ZI_GEMM_SELECT`` = ``auto`` (default) | ``cublas`` | ``zi`` forces a choice.
+``ZI_GEMM_SELECT`` = ``zi`` (default) | ``cublas`` | ``auto`` forces a choice.
 """
 
 from __future__ import annotations
@@ -23,6 +21,7 @@ from . import kernels
 
 _CHOICE: dict = {}          # (site, shape...) -> "zi" | "cublas"
 _TIMES: dict = {}           # same key -> (zi_ms, cublas_ms), for reports
+_REPORT = False             # compare_gpt: time both candidates whatever the mode
 
 
 def aligned(*ts) -> bool:
@@ -52,7 +51,7 @@ def _time(fn, reps: int) -> float:
 
 def tune(key, zi_fn, cublas_fn, rounds: int = 3, reps: int = 5) -> str:
     mode = os.environ.get("ZI_GEMM_SELECT", "auto")
-    if mode in ("zi", "cublas"):
+    if mode in ("zi", "cublas") and not _REPORT:
         return mode
     if key in _CHOICE:
         return _CHOICE[key]
@@ -67,6 +66,18 @@ def tune(key, zi_fn, cublas_fn, rounds: int = 3, reps: int = 5) -> str:
     _CHOICE[key] = "zi" if z < c else "cublas"
     _TIMES[key] = (round(z, 4), round(c, 4))
     return _CHOICE[key]
+
+
+def compare_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
+    """Time zi_gemm_sk against cuBLAS at every site (the bench's comparison column);
+    returns :func:`report`."""
+    global _REPORT
+    _REPORT = True
+    try:
+        tune_gpt(T, hd, vocab, ws, device)
+    finally:
+        _REPORT = False
+    return report()
 
 
 def report() -> dict:
@@ -102,29 +113,29 @@ def tune_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
     # forward: qkv / proj (bias), fc1 (+ GELU), fc2 (+ bias + residual)
     for name, w, b, out in (("qkv.fwd", w3, b3, o3), ("proj.fwd", wp, bh, oh)):
         sites[name] = tune((name, T, w.shape[0], hd),
-                           lambda w=w, b=b, out=out: kernels.gemm(x, w, out, bias=b),
+                           lambda w=w, b=b, out=out: kernels.gemm_sk(x, w, out, bias=b),
                            lambda w=w, b=b, out=out: torch.addmm(b, x, w.t(), out=out))
     sites["fc1.fwd"] = tune(("fc1.fwd+gelu", T, H4, hd),
-                            lambda: kernels.gemm_ex(x, w1, o4, bias=b1, epi="gelu", out2=a4),
+                            lambda: kernels.gemm_sk(x, w1, o4, bias=b1, epi="gelu", out2=a4),
                             lambda: (torch.addmm(b1, x, w1.t(), out=o4), kernels.gelu_fwd(o4, a4)))
     sites["fc2.fwd"] = tune(("fc2.fwd+resid", T, hd, H4),
-                            lambda: kernels.gemm_ex(u, w2, oh, bias=bh, epi="resid", x=oh2),
+                            lambda: kernels.gemm_sk(u, w2, oh, bias=bh, epi="resid", x=oh2),
                             lambda: (torch.addmm(bh, u, w2.t(), out=oh), oh.add_(oh2)))
     # backward: weight gradients (both operands MN-major) and input gradients
     for name, dy, inp, gw in (("fc2.dW", x, u, gw2), ("fc1.dW", dy4, x, gw1),
                               ("proj.dW", x, x, gwp), ("qkv.dW", dy3, x, gw3)):
         sites[name] = tune((name, T, gw.shape[0], gw.shape[1]),
-                           lambda dy=dy, inp=inp, gw=gw: kernels.gemm(dy.t(), inp.t(), gw),
+                           lambda dy=dy, inp=inp, gw=gw: kernels.gemm_sk(dy.t(), inp.t(), gw),
                            lambda dy=dy, inp=inp, gw=gw: torch.mm(dy.t(), inp, out=gw))
     sites["fc2.dx"] = tune(("fc2.dx+dgelu", T, H4, hd),
-                           lambda: (kernels.gemm_ex(x, w2.t(), a4, epi="dgelu", x=u),
+                           lambda: (kernels.gemm_sk(x, w2.t(), a4, epi="dgelu", x=u),
                                     kernels.bias_grad(a4, db, ws)),
                            lambda: (torch.mm(x, w2, out=o4), kernels.bias_grad(o4, db, ws, u=u,
                                                                                 du=a4)))
     for name, dy, w, out in (("fc1.dx", dy4, w1, oh), ("proj.dx", x, wp, oh),
                              ("qkv.dx", dy3, w3, oh)):
         sites[name] = tune((name, T, hd, dy.shape[1]),
-                           lambda dy=dy, w=w, out=out: kernels.gemm(dy, w.t(), out),
+                           lambda dy=dy, w=w, out=out: kernels.gemm_sk(dy, w.t(), out),
                            lambda dy=dy, w=w, out=out: torch.mm(dy, w, out=out))
     del x, u, w3, w1, w2, wp, o3, o4, oh, oh2, a4, gw3, gw1, gw2, gwp, dy4, dy3
     # tied head: logits, dW (fp32 accumulator), dx
@@ -133,14 +144,14 @@ def tune_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
     acc = torch.empty(vocab, hd, dtype=torch.float32, device=device)
     dx = torch.empty(T, hd, dtype=bf, device=device)
     sites["head.fwd"] = tune(("head.fwd", T, vocab, hd),
-                             lambda: kernels.gemm(hf, wte, logits),
+                             lambda: kernels.gemm_sk(hf, wte, logits),
                              lambda: torch.mm(hf, wte.t(), out=logits))
     sites["head.dW"] = tune(("head.dW", vocab, hd, T),
-                            lambda: kernels.gemm(logits.t(), hf.t(), acc),
+                            lambda: kernels.gemm_sk(logits.t(), hf.t(), acc),
                             lambda: torch.ops.aten.mm.dtype_out(logits.t(), hf, torch.float32,
                                                                 out=acc))
     sites["head.dx"] = tune(("head.dx", T, hd, vocab),
-                            lambda: kernels.gemm(logits, wte.t(), dx),
+                            lambda: kernels.gemm_sk(logits, wte.t(), dx),
                             lambda: torch.mm(logits, wte, out=dx))
     del hf, wte, logits, acc, dx
     torch.cuda.synchronize()

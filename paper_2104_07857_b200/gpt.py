@@ -256,13 +256,12 @@ class GPTZeroEngine:
                       and fused)
         self.ws = kernels.Workspace(max(4 << 20, 2 * 148 * cfg.hd, 600 * 4 * cfg.hd),
                                     device=self.dev) if self.fused else None
-        # Per-site choice between zi_gemm (tcgen05, with the neighbouring elementwise
-        # pass folded into its epilogue where the site has one) and cuBLAS + a separate
-        # pass, timed once per process on this engine's shapes (gemm_select.py).
-        # "auto" (default, or ZI_GEMM_SELECT) tunes; "zi" / "cublas" force every site.
-        # The cross-rank barriers are stream memory operations (no SM held while a rank
-        # waits), so one process per GPU (DistComm) tunes the same way.
-        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", "auto")
+        # Every linear of the block and the head runs on zi_gemm_sk (tcgen05 stream-K,
+        # the neighbouring elementwise pass folded into its epilogue where the site has
+        # one): "zi", the default. "cublas" (cuBLAS + a separate pass) and "auto" (time
+        # both once per process, keep the faster per site; gemm_select.py) exist for A/B
+        # measurements only. ZI_GEMM_SELECT overrides.
+        mode = gemm_select or os.environ.get("ZI_GEMM_SELECT", "zi")
         if mode not in ("auto", "zi", "cublas"):
             raise ValueError("gemm_select must be 'auto', 'zi' or 'cublas'")
         self.gemm_select = mode
@@ -685,18 +684,21 @@ class GPTZeroEngine:
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
     def _zi(self, site: str, *ts) -> bool:
-        """Run ``site`` on zi_gemm: chosen for it, and the operands meet its alignment."""
+        """Run ``site`` on zi_gemm_sk (the product path); its operands must meet the
+        kernel's alignment contract — no silent library fallback."""
         if self.gsel.get(site) != "zi":
             return False
         from .gemm_select import aligned
-        return aligned(*ts)
+        if not aligned(*ts):
+            raise ValueError(f"{site}: operands not 16-byte aligned for zi_gemm_sk")
+        return True
 
     def _linear(self, site, x, w, b, out=None):
         """y = x w^T + b on the site's chosen GEMM."""
         if out is None:
             out = torch.empty(x.shape[0], w.shape[0], dtype=x.dtype, device=x.device)
         if self._zi(site, x, w, b, out):
-            kernels.gemm(x, w, out, bias=b)
+            kernels.gemm_sk(x, w, out, bias=b)
             self.launches += 1
         else:
             torch.addmm(b, x, w.t(), out=out)
@@ -705,7 +707,7 @@ class GPTZeroEngine:
     def _mm_dw(self, site, dy, inp, out):
         """out = dy^T inp (a weight gradient, written into its grad-bucket view)."""
         if self._zi(site, dy, inp, out):
-            kernels.gemm(dy.t(), inp.t(), out)
+            kernels.gemm_sk(dy.t(), inp.t(), out)
             self.launches += 1
         elif out.dtype == dy.dtype:
             torch.mm(dy.t(), inp, out=out)
@@ -717,7 +719,7 @@ class GPTZeroEngine:
         """dy w (an input gradient)."""
         out = torch.empty(dy.shape[0], w.shape[1], dtype=dy.dtype, device=dy.device)
         if self._zi(site, dy, w, out):
-            kernels.gemm(dy, w.t(), out)
+            kernels.gemm_sk(dy, w.t(), out)
             self.launches += 1
         else:
             torch.mm(dy, w, out=out)
@@ -738,13 +740,13 @@ class GPTZeroEngine:
         u = torch.empty(T, H4, dtype=h2.dtype, device=h2.device)
         a = torch.empty_like(u)
         if self._zi("fc1.fwd", h2, P["fc1_w"], P["fc1_b"], u, a):
-            kernels.gemm_ex(h2, P["fc1_w"], u, bias=P["fc1_b"], epi="gelu", out2=a)
+            kernels.gemm_sk(h2, P["fc1_w"], u, bias=P["fc1_b"], epi="gelu", out2=a)
         else:
             torch.addmm(P["fc1_b"], h2, P["fc1_w"].t(), out=u)
             kernels.gelu_fwd(u, a)
         y = torch.empty_like(x2)
         if self._zi("fc2.fwd", a, P["fc2_w"], P["fc2_b"], y, x2):
-            kernels.gemm_ex(a, P["fc2_w"], y, bias=P["fc2_b"], epi="resid", x=x2)
+            kernels.gemm_sk(a, P["fc2_w"], y, bias=P["fc2_b"], epi="resid", x=x2)
             self.launches += 1
         else:
             torch.addmm(P["fc2_b"], a, P["fc2_w"].t(), out=y)
@@ -756,13 +758,13 @@ class GPTZeroEngine:
         """bf16 block backward: bias grads via deterministic column sums, GELU
         backward fused with the fc1 bias grad (or into the fc2 input-gradient GEMM's
         epilogue), LayerNorm backward with the residual gradient folded in — all
-        libzinf; GEMMs on their sites' choice, attention via cuDNN."""
+        libzinf; GEMMs on zi_gemm_sk, attention on zi_attn (tcgen05)."""
         x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
         ws = self.ws
         self._mm_dw("fc2.dW", dy, a, G["fc2_w"])
         du = torch.empty_like(u)
         if self._zi("fc2.dx", dy, P["fc2_w"], du, u):  # du = (dy W2) * gelu'(u), then db1
-            kernels.gemm_ex(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
+            kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
             kernels.bias_grad(du, G["fc1_b"], ws)
             self.launches += 1
         else:
@@ -853,7 +855,7 @@ class GPTZeroEngine:
         _, hf, mf, rf = self._ln(x, PF["lnf_w"], PF["lnf_b"])
         logits = torch.empty(hf.shape[0], PE["wte"].shape[0], dtype=hf.dtype, device=hf.device)
         if self._zi("head.fwd", hf, PE["wte"], logits):
-            kernels.gemm(hf, PE["wte"], logits)
+            kernels.gemm_sk(hf, PE["wte"], logits)
             self.launches += 1
         else:
             torch.mm(hf, PE["wte"].t(), out=logits)

@@ -266,6 +266,57 @@ def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi:
     return out
 
 
+_SK_WS: dict = {}
+
+
+def sk_workspace(stream=None) -> torch.Tensor:
+    """The stream-K GEMM workspace of (device, stream): flags zeroed once (they reset
+    themselves), then one fp32 partial-accumulator slot per CTA. Launches sharing a
+    workspace must be stream-ordered, hence one per stream."""
+    s = stream if stream is not None else torch.cuda.current_stream()
+    key = (s.device.index, s.cuda_stream)
+    ws = _SK_WS.get(key)
+    if ws is None:
+        nbytes = int(_lib.load().zi_gemm_sk_workspace_bytes())
+        with torch.cuda.stream(s):
+            ws = torch.zeros((nbytes + 255) // 256 * 64, dtype=torch.float32, device=s.device)
+        _SK_WS[key] = ws
+    return ws
+
+
+def gemm_sk(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi: str = "plain",
+            x=None, out2=None, split: bool = True, stream=None) -> torch.Tensor:
+    """zi_gemm_sk: out = epi(a b^T) on the stream-K tcgen05 GEMM (include/zinf.h).
+
+    ``a`` (M, K) and ``b`` (N, K) as in :func:`gemm` (either may be an MN-major
+    transposed view). ``out`` is a row-major bf16 (M, N) view with the epilogues of
+    :func:`gemm_ex`, or fp32 (epi "plain", no bias). ``split=False`` runs whole
+    tiles (no workspace)."""
+    M, K = a.shape
+    N = b.shape[0]
+    if b.shape[1] != K or out.shape != (M, N) or out.stride(1) != 1:
+        raise ValueError("gemm_sk: shape mismatch or non-row-major output")
+    f32 = out.dtype == torch.float32
+    if out.dtype not in (torch.bfloat16, torch.float32) or (f32 and (epi != "plain" or bias is not None)):
+        raise ValueError("gemm_sk: bf16 output, or fp32 output without an epilogue")
+    for t, name in ((x, "x"), (out2, "out2")):
+        if t is not None and (t.shape != (M, N) or t.stride(1) != 1 or t.dtype != torch.bfloat16):
+            raise ValueError(f"gemm_sk: {name} must be a row-major bf16 (M, N) view")
+    pa, amn, lda = _operand(a, "a")
+    pb, bmn, ldb = _operand(b, "b")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    ws = sk_workspace(s) if split else None
+    _lib.call("zi_gemm_sk", pa, amn, lda, pb, bmn, ldb,
+              _dev(bias, "bias") if bias is not None else None, out.data_ptr(), out.stride(0),
+              int(f32), x.data_ptr() if x is not None else None,
+              x.stride(0) if x is not None else 0,
+              out2.data_ptr() if out2 is not None else None,
+              out2.stride(0) if out2 is not None else 0, EPI[epi], M, N, K,
+              ws.data_ptr() if ws is not None else None,
+              ws.numel() * 4 if ws is not None else 0, s.cuda_stream)
+    return out
+
+
 class Workspace:
     """fp32 scratch for the deterministic column reductions: 1024 self-resetting int
     counters (zeroed here once) followed by per-chunk partial rows. Use one workspace

@@ -326,9 +326,9 @@ def test_offload_graphed_matches_eager(params_host):
     from paper_2104_07857_b200.store import TierKind
     pl = Placement(params=TierKind.HOST if params_host else TierKind.DEVICE, optim=TierKind.HOST)
     a = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007,
-                         gemm_select="cublas")
+                         gemm_select="zi")
     b = eg.GPTZeroEngine(SMALL, LocalComm(2), lr=1e-3, placement=pl, offload_chunk=10_007,
-                         gemm_select="cublas")
+                         gemm_select="zi")
     for step in range(3):
         bs = batches_for(SMALL, 2, step)
         la, lb = a.step(bs).item(), b.step_graphed(bs).item()
@@ -350,7 +350,7 @@ def test_param_reuse_cache_matches(K, params_host, graph):
     pl = Placement(params=TierKind.HOST if params_host else TierKind.DEVICE,
                    optim=TierKind.HOST if params_host else TierKind.DEVICE)
     cfg = eg.GPTConfig(nl=5, hd=128, heads=2, seq=128, vocab=256, batch=2)
-    kw = dict(lr=1e-3, placement=pl, offload_chunk=10_007, gemm_select="cublas")
+    kw = dict(lr=1e-3, placement=pl, offload_chunk=10_007, gemm_select="zi")
     a = eg.GPTZeroEngine(cfg, LocalComm(2), **kw)
     b = eg.GPTZeroEngine(cfg, LocalComm(2), param_cache=K, **kw)
     assert b.K == min(K, cfg.nl - 1) and len(b.slots) == 2 + b.K
