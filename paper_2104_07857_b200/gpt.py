@@ -172,7 +172,8 @@ class GPTZeroEngine:
                  overlap_opt: bool | None = None, act_ckpt: str | None = None,
                  nvme_root: str | None = None, gemm_select: str | None = None,
                  offload_slots: int | None = None, nvme_direct: bool = False,
-                 fwd_state_prefetch_every: int = 2, param_cache: int = 0):
+                 fwd_state_prefetch_every: int = 2, param_cache: int = 0,
+                 prefetch_depths=(3, 2, 1), prefetch_budget: int | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("GPTZeroEngine needs a CUDA device (no CPU fallback)")
         _lib.load()
@@ -186,8 +187,23 @@ class GPTZeroEngine:
         if self.cdt == torch.bfloat16 and (cfg.seq % 128 or cfg.head_dim not in (64, 128)):
             raise ValueError("bf16 attention (zi_attn) needs seq % 128 == 0 and head_dim 64 or 128")
         self.placement = placement or Placement()
-        if self.placement.params not in (TierKind.DEVICE, TierKind.HOST):
-            raise NotImplementedError("bf16 params: DEVICE or HOST tier")
+        # bf16 params off HBM: pinned host DRAM, or .shard files on NVMe streamed
+        # NVMe -> pinned -> HBM -> gather (the nc / cg / gg stages of PAPER §6.2)
+        self.host_params = self.placement.params in (TierKind.HOST, TierKind.NVME)
+        self.nvme_params = self.placement.params is TierKind.NVME
+        if self.nvme_params and self.placement.optim is not TierKind.HOST:
+            raise NotImplementedError("params on NVMe: optimizer states in pinned host DRAM")
+        if self.nvme_params and compute_dtype not in (None, half_dtype):
+            raise NotImplementedError("params on NVMe: bf16 compute")
+        # prefetch plan: while fetch position p runs, issue the nc of
+        # p + d_nc, the cg of p + d_cg and the gg of p + d_gg; prefetch_budget (bytes,
+        # SPEC.md:621) delays an early nc / cg while the prefetched-but-unconsumed bytes
+        # would exceed it (a stage is always issued by the time its successor needs it)
+        d_nc, d_cg, d_gg = prefetch_depths
+        if not (d_nc >= d_cg >= d_gg >= 1) or d_gg != 1:
+            raise ValueError("prefetch depths need d_nc >= d_cg >= d_gg == 1")
+        self.depths = tuple(prefetch_depths)
+        self.prefetch_budget = prefetch_budget
         self.nvme = self.placement.optim is TierKind.NVME
         if self.nvme and (self.placement.params is not TierKind.DEVICE or not self.comm.is_local):
             raise NotImplementedError("NVMe optimizer states: params in HBM, simulated ranks")
@@ -236,7 +252,7 @@ class GPTZeroEngine:
         self._alloc_state()
         self._init_state()
         self.fwd_seq, self.bwd_seq = trace_schedule(self)
-        self.plan = plan_prefetch(self.fwd_seq, (1, 1, 1))
+        self.plan = plan_prefetch(self.fwd_seq, self.depths)
         self.gather_stream = torch.cuda.Stream(self.dev)
         self.h2d_stream = torch.cuda.Stream(self.dev)
         self.d2h_stream = torch.cuda.Stream(self.dev)
@@ -309,7 +325,7 @@ class GPTZeroEngine:
     def _alloc_state(self):
         nloc = len(self.ranks)
         A = self.arena_len
-        hp = self.placement.params is TierKind.HOST
+        hp = self.host_params
         ho = self.placement.optim is TierKind.HOST
 
         self._pinned = []
@@ -328,6 +344,15 @@ class GPTZeroEngine:
             self.p16 = mk(self.half, hp)
         else:  # peers gather from it over NVLink: an IPC-shareable allocation
             self.p16 = self.comm.alloc((nloc, A), self.half)
+        if self.nvme_params:
+            # bf16 param shards live in reference-format .shard files ({bucket}.p16/rank{r});
+            # the pinned arena above is the write-back staging the updates land in
+            import tempfile
+            from concurrent.futures import ThreadPoolExecutor
+            from .store import TierStore
+            root = self.nvme_root or tempfile.mkdtemp(prefix="zinf-nvme-params-")
+            self.pstore = TierStore(0, 0, nvme_root=root, workers=8)
+            self._io = ThreadPoolExecutor(max_workers=8, thread_name_prefix="zinf-nc")
         if self.nvme:  # optimizer states live in .shard files (nvme_opt.NvmeOptimizerStreamer)
             import tempfile
             from .nvme_opt import NvmeOptimizerStreamer
@@ -344,7 +369,7 @@ class GPTZeroEngine:
     def _init_state(self):
         """Shard-local counter-RNG init; never a full tensor."""
         ho = self.placement.optim is TierKind.HOST
-        hp = self.placement.params is TierKind.HOST
+        hp = self.host_params
         for li, r in enumerate(self.ranks):
             for b in self.buckets:
                 lo, hi = r * b.shard, min((r + 1) * b.shard, b.numel)
@@ -374,6 +399,12 @@ class GPTZeroEngine:
                 if hp:
                     self.p16[li, b.arena_off:b.arena_off + b.shard].copy_(p16)
         torch.cuda.synchronize()
+        if self.nvme_params:   # the initial bf16 shards become the param files
+            tickets = [self.pstore.write(self._pkey(b, r),
+                                         self.p16[li, b.arena_off:b.arena_off + b.shard],
+                                         TierKind.NVME)
+                       for li, r in enumerate(self.ranks) for b in self.buckets]
+            self.pstore.flush(tickets)
 
     def _alloc_work(self):
         c = self.cfg
@@ -406,7 +437,7 @@ class GPTZeroEngine:
         if not self.comm.is_local and self.N > 1:
             self.peer_gslots = [self.comm.share(self.gslots[0][k]) for k in range(2)]
             self.peer_gembed = self.comm.share(self.gembed[0])
-            if self.placement.params is TierKind.HOST:
+            if self.host_params:
                 # cg staging slots (embed + 2-slot ring) that peers gather from
                 shmax = max(b.shard for b in self.buckets)
                 self.pstage = [self.comm.alloc((shmax,), self.half) for _ in range(3)]
@@ -414,6 +445,30 @@ class GPTZeroEngine:
             else:
                 self.peer_p16 = self.comm.share(self.p16[0])
         self.events = {}
+        # staged fetch (params off HBM): cg staging slots in HBM (simulated ranks; with
+        # peers the IPC pstage ring plays that part) and, for NVMe params, pinned nc slots
+        # that the store workers read the shard files into
+        self._flist = self._fetch_list()
+        self._fplan = None
+        self.issue_log, self.nc_bytes = [], 0
+        self._staged, self._cg_ev, self._cg_free, self._cg_issued = {}, {}, {}, set()
+        self._nc_fut, self._nc_busy, self._nc_issued = {}, {}, set()
+        self._p16_wfut = {}
+        self._fpos = 0
+        if self.host_params:
+            shmax = max(b.shard for b in self.buckets)
+            self.CGS = self.depths[1] + 1
+            if self.comm.is_local:
+                self.cg_slots = [[torch.empty(shmax, dtype=self.half, device=self.dev)
+                                  for _ in range(nloc)] for _ in range(self.CGS)]
+            if self.nvme_params:
+                from .store import _PinnedBuffer
+                self.NCS = self.depths[0] + 1
+                per = shmax * torch.empty(0, dtype=self.half).element_size()
+                self._nc_buf = _PinnedBuffer(self.NCS * nloc * per)
+                flat = self._nc_buf.tensor.view(self.half)
+                self.nc_slots = [[flat[(k * nloc + li) * shmax:(k * nloc + li + 1) * shmax]
+                                  for li in range(nloc)] for k in range(self.NCS)]
         # offload engine: double-buffered HBM staging for optimizer-state chunks
         self.offload = self.placement.optim is TierKind.HOST
         self.opt_stream = torch.cuda.Stream(self.dev)
@@ -451,7 +506,7 @@ class GPTZeroEngine:
                 self._obucket[b.key] = idx
             # NS <= chunks per step: the in-order D2H stream then guarantees that chunk
             # q's previous-step write-back landed before its next H2D (slot reuse events)
-            want = self.offload_slots or (12 if self.placement.params is TierKind.HOST else 24)
+            want = self.offload_slots or (12 if self.host_params else 24)
             NS = max(3, min(want, len(self._ochunks)))
             self.stage = [[torch.empty(C, dtype=torch.float32, device=self.dev) for _ in range(3)]
                           for _ in range(NS)]
@@ -539,23 +594,42 @@ class GPTZeroEngine:
                 "serial_s": sf.serial_s + sb.serial_s, "forward": sf, "backward": sb}
 
     def _fetch(self, b: Bucket, slot: int, stream):
-        """Issue the gather of bucket b into ring slot `slot` on `stream`."""
+        """The gg stage of the step's next fetch position p: gather bucket b into
+        gathered slot `slot` on `stream`. It first issues what the prefetch plan
+        schedules while position p - 1 runs (the nc of p - 1 + d_nc, the cg of
+        p - 1 + d_cg) and whatever p itself still lacks."""
         if self.zero_copy:
             return
+        p = self._fpos
+        self._fpos += 1
+        self._advance(p)
+        staged = self.comm.is_local and self.host_params   # gg reads the cg staging slot
         dst = self.embed_slot if b.key == "embed" else self.slots[slot]
         with torch.cuda.stream(stream):
-            ev = self.p16_ready.pop(b.key, None)
-            if ev is not None:   # the previous step's updated bf16 shard is back in host DRAM
-                stream.wait_event(ev)
             t0 = self._tmark(stream)
-            if self.placement.params is TierKind.HOST:   # cg bytes over the host link
+            if self.host_params:   # cg bytes over the host link
                 self.fetch_bytes = getattr(self, "fetch_bytes", 0) + b.shard * len(self.ranks) * 2
-            if self.comm.is_local:
+            if staged:
+                stream.wait_event(self._cg_ev.pop(p))
+                k = p % self.CGS
+                shards = [self.cg_slots[k][li][:b.shard] for li in range(len(self.ranks))]
+                kernels.allgather(shards, b.shard, dst, b.numel,
+                                  use_copy_engine=self.copy_engine_gather)
+            elif self.comm.is_local:
                 shards = [self._shard_view(self.p16, li, b) for li in range(len(self.ranks))]
                 kernels.allgather(shards, b.shard, dst, b.numel,
-                                  use_copy_engine=self.copy_engine_gather or
-                                  self.placement.params is TierKind.HOST)
-            elif self.placement.params is TierKind.HOST:
+                                  use_copy_engine=self.copy_engine_gather)
+            elif self.host_params:
+                # source of our shard: the pinned arena, or the nc slot the NVMe read filled
+                if self.nvme_params:
+                    for f in self._nc_fut.pop(p):
+                        f.result()
+                    src = self.nc_slots[p % self.NCS][0][:b.shard]
+                else:
+                    ev = self.p16_ready.pop(b.key, None)
+                    if ev is not None:   # the previous step's bf16 shard is back in host DRAM
+                        stream.wait_event(ev)
+                    src = self._shard_view(self.p16, 0, b)
                 # ZeRO-Infinity fetch (PAPER §6.2): cg = H2D of our pinned shard into an
                 # IPC-shared HBM staging slot, then gg = P2P gather of every rank's slot.
                 # The gather-channel barrier before the gg makes all ranks' cg visible; the
@@ -568,7 +642,11 @@ class GPTZeroEngine:
                     self._pstage_n = getattr(self, "_pstage_n", 0) + 1
                     k = 1 + self._pstage_n % 2
                 stage = self.pstage[k]
-                stage[:b.shard].copy_(self._shard_view(self.p16, 0, b), non_blocking=True)
+                stage[:b.shard].copy_(src, non_blocking=True)
+                if self.nvme_params:   # the nc slot is free once this H2D has read it
+                    evb = torch.cuda.Event()
+                    evb.record(stream)
+                    self._nc_busy[p % self.NCS] = evb
                 self.comm.device_barrier(stream, channel=1)
                 kernels.allgather(self.peer_pstage[k], b.shard, dst, b.numel,
                                   use_copy_engine=self.copy_engine_gather)
@@ -583,11 +661,121 @@ class GPTZeroEngine:
                 wide = self.wide_embed if b.key == "embed" else self.wide_slots[slot]
                 kernels.cast_half_to_f32(dst[:b.numel], wide[:b.numel])
                 self.launches += 1
-            self._tspan(b.op, "cg" if self.placement.params is TierKind.HOST else "gg",
+            self._tspan(b.op, "cg" if (self.host_params and not staged) else "gg",
                         t0, self._tmark(stream))
             ev = torch.cuda.Event()
             ev.record(stream)
+        if staged:   # the cg slot may be refilled once this gather has read it
+            self._cg_free[p % self.CGS] = ev
+        self._staged.pop(p, None)
         self.events[(b.key, slot)] = ev
+
+    # ----------------------------------------------- staged fetch: nc / cg (PAPER §6.2)
+    def _fetch_list(self) -> list:
+        """The step's fetch positions in the order ``_fetch`` runs them: embed, the
+        blocks and the head (forward), then the blocks the backward gathers again (all
+        but the last one and the K reuse-cached ones, last to first)."""
+        blocks, E, FB = self.buckets[1:-1], self.buckets[0], self.buckets[-1]
+        nb = len(blocks)
+        back = [blocks[j] for j in range(nb - 2 - self.K, -1, -1)]
+        return [E] + blocks + [FB] + back
+
+    def _budget_ok(self, q: int) -> bool:
+        if self.prefetch_budget is None:
+            return True
+        need = self._flist[q].shard * len(self.ranks) * 2
+        return sum(self._staged.values()) + need <= self.prefetch_budget
+
+    def _advance(self, p: int) -> None:
+        """Issue the plan's nc / cg stages for fetch position p: the
+        eager set at p == 0, ``plan.issue(p - 1)`` otherwise, within the byte budget —
+        after p's own nc and cg if they are still missing (the copy FIFOs serve p first)."""
+        if not self.host_params:
+            return
+        self._nc(p, p, forced=True)
+        self._cg(p, p, forced=True)
+        todo = self._fplan.slots[0] if p == 0 else self._fplan.issue(p - 1)
+        for q in todo["nc"]:
+            self._nc(q, p, forced=False)
+        for q in todo["cg"]:
+            self._cg(q, p, forced=False)
+
+    def _nc(self, q: int, at: int, forced: bool) -> None:
+        """nc-transfer of fetch position q: every local rank's bf16 shard file is read
+        by a store worker into pinned nc slot q % NCS (after the slot's previous H2D
+        has read it, and after the file's last write-back)."""
+        if not self.nvme_params or q >= len(self._flist) or q in self._nc_issued:
+            return
+        if not forced and not self._budget_ok(q):
+            return
+        b = self._flist[q]
+        k = q % self.NCS
+        busy = self._nc_busy.pop(k, None)
+        futs = []
+        for li, r in enumerate(self.ranks):
+            view = self.nc_slots[k][li][:b.shard]
+            futs.append(self._io.submit(self._nc_job, self._pkey(b, r), view,
+                                        self._p16_wfut.get((b.key, r)), busy))
+        self._nc_fut[q] = futs
+        self._nc_issued.add(q)
+        self._staged[q] = b.shard * len(self.ranks) * 2
+        self.issue_log.append((at, "nc", q))
+        self.nc_bytes += b.shard * len(self.ranks) * 2
+
+    def _nc_job(self, key: str, view: torch.Tensor, wfut, busy) -> None:
+        if wfut is not None:
+            wfut.result()          # the file holds the last update (read after write)
+        if busy is not None:
+            busy.synchronize()     # the slot's previous H2D has read it
+        self.pstore.read_into(key, TierKind.NVME, view).wait()
+
+    def _wb_job(self, key: str, view: torch.Tensor, ev) -> None:
+        ev.synchronize()           # the updated bf16 shard landed in pinned memory
+        self.pstore.write_range(key, TierKind.NVME, 0, view).wait()
+
+    def _pkey(self, b: Bucket, r: int) -> str:
+        return f"{b.key}.p16/rank{r}"
+
+    def _cg(self, q: int, at: int, forced: bool) -> None:
+        """cg-transfer of fetch position q (simulated ranks): every local rank's shard,
+        from the pinned arena (HOST) or its nc slot (NVMe), H2D into cg staging slot
+        q % CGS, behind the gather that last read the slot."""
+        if not (self.comm.is_local and self.host_params) or q >= len(self._flist):
+            return
+        if q in self._cg_issued:
+            return
+        if not forced and not self._budget_ok(q):
+            return
+        b = self._flist[q]
+        k = q % self.CGS
+        h2d = self.h2d_stream
+        if self.nvme_params:
+            self._nc(q, at, forced=True)
+            for f in self._nc_fut.pop(q):
+                f.result()
+        with torch.cuda.stream(h2d):
+            ev_free = self._cg_free.pop(k, None)
+            if ev_free is not None:
+                h2d.wait_event(ev_free)
+            if self.nvme_params:
+                src = [self.nc_slots[q % self.NCS][li][:b.shard] for li in range(len(self.ranks))]
+            else:
+                evp = self.p16_ready.pop(b.key, None)
+                if evp is not None:   # the previous step's bf16 shard is back in host DRAM
+                    h2d.wait_event(evp)
+                src = [self._shard_view(self.p16, li, b) for li in range(len(self.ranks))]
+            t0 = self._tmark(h2d)
+            for li in range(len(self.ranks)):
+                self.cg_slots[k][li][:b.shard].copy_(src[li], non_blocking=True)
+            self._tspan(b.op, "cg", t0, self._tmark(h2d))
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        self._cg_ev[q] = ev
+        self._cg_issued.add(q)
+        if self.nvme_params:
+            self._nc_busy[q % self.NCS] = ev
+        self._staged[q] = b.shard * len(self.ranks) * 2
+        self.issue_log.append((at, "cg", q))
 
     def _pslot(self, i: int, nb: int) -> int:
         """Gathered-parameter slot of block i (i == nb: the head bucket): the last K
@@ -932,7 +1120,7 @@ class GPTZeroEngine:
                                      self._shard_view(self.p16, li, b))
                 for li, r in enumerate(self.ranks)]
             return
-        host_params = self.placement.params is TierKind.HOST
+        host_params = self.host_params
         with torch.cuda.stream(os_):
             t0 = self._tmark(os_)
             for li, r in enumerate(self.ranks):
@@ -995,7 +1183,7 @@ class GPTZeroEngine:
         cur = torch.cuda.current_stream()
         opt, d2h = self.opt_stream, self.d2h_stream
         opt.wait_stream(cur)                 # grads of bucket b are complete
-        host_params = self.placement.params is TierKind.HOST
+        host_params = self.host_params
         NS = len(self.stage)
         gouts = {li: self._gout(li, b) for li in range(len(self.ranks))}
         for q in self._obucket[b.key]:
@@ -1042,7 +1230,13 @@ class GPTZeroEngine:
         if host_params:
             ev = torch.cuda.Event()
             ev.record(self.p16_stream)
-            self.p16_ready[b.key] = ev
+            if self.nvme_params:   # nc lane, write direction: the shard file is updated from
+                self.p16_ready.pop(b.key, None)   # the arena once the D2H landed; the next
+                for li, r in enumerate(self.ranks):   # step's nc read of b waits on it
+                    self._p16_wfut[(b.key, r)] = self._io.submit(
+                        self._wb_job, self._pkey(b, r), self._shard_view(self.p16, li, b), ev)
+            else:
+                self.p16_ready[b.key] = ev
 
     @property
     def defer_writeback(self) -> bool:
@@ -1062,6 +1256,9 @@ class GPTZeroEngine:
         cur.wait_stream(self.d2h_stream)
         cur.wait_stream(self.h2d_stream)
         cur.wait_stream(self.p16_stream)
+        if self.nvme_params:   # the bf16 param files hold the last update
+            for f in list(self._p16_wfut.values()):
+                f.result()
 
     # ------------------------------------------------- activation checkpoints (PAPER §5.1.2)
     def _ckpt_save(self, li: int, i: int, x_in: torch.Tensor):
@@ -1161,9 +1358,25 @@ class GPTZeroEngine:
                 self.ev_d2h = [None] * len(self.ev_d2h)
         self._ckpt_saved.clear()
         self._ckpt_loaded.clear()
+        # the step's fetch positions and their nc / cg / gg plan
+        if self._fplan is None:
+            from .schedule import Op, OperatorSequence
+            ops = tuple(Op(b.op, (b.key,), 2 * b.numel, 1) for b in self._flist)
+            self._fplan = plan_prefetch(OperatorSequence(ops, "step"), self.depths)
+        self._fpos = 0
+        self.issue_log = []
+        self._staged.clear()
+        self._cg_ev.clear()
+        self._cg_issued.clear()
+        self._nc_fut.clear()
+        self._nc_issued.clear()
+        if torch.cuda.is_current_stream_capturing():
+            self._cg_free.clear()      # recorded outside the capture (and complete)
+        if self.host_params:
+            self.h2d_stream.wait_stream(cur)   # the cg lane forks from this step's start
         self._nvme_wait = {}
         self._t0 = self._tmark(cur)
-        host_params = self.placement.params is TierKind.HOST
+        host_params = self.host_params
         if self.offload and not host_params:   # state prefetch for the backward, during the forward
             self._ostate_prefetch()
         self._phase = "forward"
@@ -1286,7 +1499,7 @@ class GPTZeroEngine:
         if (self.offload and not self.defer_writeback) or self.nvme or self.act_ckpt == "host":
             cur.wait_stream(self.d2h_stream)  # ... and host transfers landed
             cur.wait_stream(self.h2d_stream)
-            if self.offload and self.placement.params is TierKind.HOST:
+            if self.offload and self.host_params:
                 cur.wait_stream(self.p16_stream)
                 self.p16_ready.clear()
         if gs is not cur:
@@ -1307,7 +1520,7 @@ class GPTZeroEngine:
         steps (real training steps) and captures; every call then replays.
         """
         cur = torch.cuda.current_stream()
-        if self.nvme:   # host-thread NVMe streaming cannot live inside a graph
+        if self.nvme or self.nvme_params:   # host-thread NVMe I/O cannot live in a graph
             return self.step(batches)
         if self._graph is None:
             if self.trace:
@@ -1378,12 +1591,22 @@ class GPTZeroEngine:
         return {n: self._shard_view(a, li, b) for n, a in
                 (("p16", self.p16), ("p32", self.p32), ("m", self.m), ("v", self.v))}
 
+    def param_file_shard(self, key: str, li: int = 0) -> torch.Tensor:
+        """Params on NVMe: rank li's bf16 shard of bucket ``key`` as its .shard file holds it."""
+        self.flush()
+        return self.pstore.read(self._pkey(self.by_key[key], self.ranks[li]), TierKind.NVME).wait()
+
     def close(self) -> None:
         """Stop the NVMe streamer thread (it references the engine) and its store."""
         if self.nvme and self.streamer is not None:
             self.streamer.close()
             self.store.close()
             self.streamer = None
+        if self.nvme_params and self._io is not None:
+            self.flush()
+            self._io.shutdown(wait=True)
+            self.pstore.close()
+            self._io = None
 
 
 def synthetic_tokens(cfg: GPTConfig, seed: int, rank: int, step: int = 0, device="cuda"):

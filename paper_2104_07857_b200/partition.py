@@ -103,6 +103,21 @@ def partition(full, world_size: int, tier: TierKind, store: TierStore, key: str 
     return pt
 
 
+# Pinned host staging buffers read by libzinf's asynchronous copies. torch's caching host
+# allocator only tracks its own copies, so a buffer dropped right after the launch could
+# be handed to the next NVMe read while the copy engine still reads it: keep each batch
+# alive until an event recorded after its consumer has completed.
+_inflight: list = []
+
+
+def _keep_until_done(bufs) -> None:
+    while _inflight and _inflight[0][0].query():
+        _inflight.pop(0)
+    ev = torch.cuda.Event()
+    ev.record()
+    _inflight.append((ev, bufs))
+
+
 def _device_shard(pt: PartitionedTensor, store: TierStore, rank: int) -> torch.Tensor:
     """A tensor the gather can read directly: HBM or pinned host (UVA)."""
     k = pt.shard_key(rank)
@@ -136,6 +151,8 @@ def allgather(pt: PartitionedTensor, store: TierStore, comm=None, out: torch.Ten
             shards = [_device_shard(pt, store, r) for r in range(pt.world_size)]
         kernels.allgather(shards, L, out, pt.full_len,
                           use_copy_engine=use_copy_engine or pt.tier is not TierKind.DEVICE)
+        if pt.tier is TierKind.NVME:
+            _keep_until_done(shards)
         return out
     mine = _device_shard(pt, store, comm.rank)
     if method == "nccl":

@@ -30,8 +30,9 @@ def _port():
 def _placement(name):
     from paper_2104_07857_b200.gpt import Placement
     from paper_2104_07857_b200.store import TierKind
-    D, H = TierKind.DEVICE, TierKind.HOST
-    return {"hbm": Placement(D, D), "params_host": Placement(H, D), "all_host": Placement(H, H)}[name]
+    D, H, V = TierKind.DEVICE, TierKind.HOST, TierKind.NVME
+    return {"hbm": Placement(D, D), "params_host": Placement(H, D), "all_host": Placement(H, H),
+            "params_nvme": Placement(V, H)}[name]
 
 
 def _rank_main(rank, world, port, q, placement="hbm", graph=False, cache=0):
@@ -52,6 +53,11 @@ def _rank_main(rank, world, port, q, placement="hbm", graph=False, cache=0):
             losses.append(run([eg.synthetic_tokens(c, 7, rank, step)]).item())
         torch.cuda.synchronize()
         out = {k: eng.shard(k, 0)["p32"].cpu().numpy() for k in eng.by_key}
+        if eng.nvme_params:   # the bf16 param files hold the update (nc lane, both ways)
+            for k in eng.by_key:
+                assert torch.equal(eng.param_file_shard(k, 0).view(torch.int16),
+                                   eng.shard(k, 0)["p16"].view(torch.int16)), k
+            eng.close()
         dist.barrier()
         comm.close()
         dist.destroy_process_group()
@@ -64,7 +70,8 @@ def _rank_main(rank, world, port, q, placement="hbm", graph=False, cache=0):
 @pytest.mark.parametrize("placement,graph,cache", [("hbm", False, 0), ("params_host", False, 0),
                                                    ("all_host", False, 0), ("hbm", True, 0),
                                                    ("params_host", True, 0),
-                                                   ("params_host", False, 1)])
+                                                   ("params_host", False, 1),
+                                                   ("params_nvme", False, 0)])
 def test_two_processes_match_local_comm(placement, graph, cache):
     """graph=True: each rank captures its step (P2P gathers, barriers with device-side
     epochs, RS + Adam over peer buckets) in a CUDA graph and replays it."""
