@@ -475,6 +475,9 @@ def run_ours(args):
     if world == 1 and not args.no_offload:
         store = _safe(store_leg)
         tiling = _safe(tiling_leg)
+        if offload is not None and not args.no_config3:
+            torch.cuda.empty_cache()   # the 10B leg's process needs ~90 GB of this GPU
+            offload["config3_real"] = _leg_subprocess("config3_real", args)
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -865,6 +868,120 @@ def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
             "loss_hbm": res["hbm"]["loss"], "loss_offload": res["offload"]["loss"]}
 
 
+def _hbm_step_ms(cfg, steps: int) -> float:
+    """Eager step time of ``cfg`` with every state in HBM (the offload legs' t_hbm)."""
+    import torch
+    from paper_2104_07857_b200 import gpt as eg
+    from paper_2104_07857_b200.comm import LocalComm
+    eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4)
+    bs = [eg.synthetic_tokens(cfg, 7, 0, s) for s in range(2)]
+    for w in range(2):
+        eng.step([bs[w % 2]])
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for s in range(steps):
+        eng.step([bs[s % 2]])
+    t1.record()
+    torch.cuda.synchronize()
+    del eng
+    torch.cuda.empty_cache()
+    return t0.elapsed_time(t1) / steps
+
+
+def config3_real_leg(args) -> dict:
+    """BASELINE config 3's model itself on one GPU: GPT 10B (50 layers, hidden 4096,
+    PAPER.md:677), 8 x 1024 tokens, bf16 params in HBM, all 10.3 G fp32 master / m / v
+    elements (124 GB) in pinned host DRAM, streamed through the H2D || zi_rs_adam_dc ||
+    D2H pipeline in the backward. At N=8 each GPU would hold 1/8 of those states; at
+    N=1 the whole 247 GB of state traffic per step crosses this GPU's own host link, so
+    the step is PCIe-bound by construction (the config3_equiv leg holds the N=8 per-GPU
+    balance). t_hbm, for SURVEY §8(d)'s hidden fraction, cannot be measured directly
+    (the states do not fit beside the activations in 180 GB): it is the linear fit
+    t(nl) = a + b * nl through all-in-HBM steps of the same model at 2 and 26 layers,
+    extrapolated to 50 (every block is the same work)."""
+    import dataclasses
+    import torch
+    from paper_2104_07857_b200 import gpt as eg
+    from paper_2104_07857_b200.comm import LocalComm
+    from paper_2104_07857_b200.store import TierKind, _mem_available, _PinnedBuffer
+    cfg = eg.GPT_10B
+    P = eg.param_count(cfg)
+    need = 12 * P
+    avail = _mem_available() or 0
+    if need > avail - _PinnedBuffer.HOST_RESERVE - (8 << 30):
+        return {"skipped": f"host DRAM: {need / 2**30:.0f} GiB of pinned optimizer state "
+                           f"needs more than the {avail / 2**30:.0f} GiB available"}
+    peak = host_link_peak()
+    steps = max(2, min(args.steps, 3))
+    t_init = time.perf_counter()
+    eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4,
+                           placement=eg.Placement(TierKind.DEVICE, TierKind.HOST))
+    init_s = time.perf_counter() - t_init
+    bs = [eg.synthetic_tokens(cfg, 7, 0, s) for s in range(2)]
+    eng.step([bs[0]])
+    torch.cuda.synchronize()
+    b0 = eng.offload_bytes
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for s in range(steps):
+        loss = eng.step([bs[(s + 1) % 2]])
+    eng.flush()
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    moved = (eng.offload_bytes - b0) / steps
+    eng.trace = True
+    eng.step([bs[0]])
+    tl = eng.timeline()
+    eng.trace = False
+    loss = float(loss.item())
+    eng.close()
+    del eng
+    torch.cuda.empty_cache()
+    t2 = _hbm_step_ms(dataclasses.replace(cfg, nl=2), steps)
+    t26 = _hbm_step_ms(dataclasses.replace(cfg, nl=26), steps)
+    t_hbm = t2 + (t26 - t2) * (cfg.nl - 2) / 24
+    t_xfer = moved / (peak["duplex_gbs"] * 1e9) * 1e3
+    exposed = ms - t_hbm
+    fl = eg.model_flops_per_step(cfg)
+    return {"workload": "GPT-10B (50 x 4096, BASELINE config 3's model) at N=1, 8 x 1024 tokens, "
+                        "bf16 params in HBM, fp32 master / m / v (all 10.3 G elements) in pinned "
+                        "host DRAM",
+            "params": P, "pinned_state_bytes": need, "engine_init_s": round(init_s, 1),
+            "ms_per_step_offload": round(ms, 1),
+            "tflops_offload": round(fl / (ms / 1e3) / 1e12, 1),
+            "loss": loss,
+            "host_bytes_per_step": int(moved),
+            "host_link_gbs": round(moved / (ms / 1e3) / 1e9, 1),
+            "host_link_peak": peak,
+            "ms_per_step_hbm_fit": round(t_hbm, 1),
+            "hbm_fit_points_ms": {"nl2": round(t2, 2), "nl26": round(t26, 2)},
+            "tflops_hbm_fit": round(fl / (t_hbm / 1e3) / 1e12, 1),
+            "transfer_ms_at_duplex_peak": round(t_xfer, 1),
+            "exposed_ms": round(exposed, 1),
+            "hidden_fraction": round(max(0.0, 1.0 - exposed / t_xfer), 4),
+            "timeline_pcie_hidden_behind_compute": round(tl.hidden_fraction(("pcie",)), 4),
+            "timeline_pcie_busy_s": round(tl.lane_busy_s("pcie"), 3),
+            "bound": "host link (N=1 carries all 8 ranks' state traffic)"}
+
+
+def _leg_subprocess(name: str, args, timeout: int = 1200) -> dict:
+    """Run one heavy leg in a fresh process (its pinned memory is the host's, and a
+    failure cannot take the main line with it); the child prints one JSON object."""
+    import subprocess
+    cmd = [sys.executable, os.path.abspath(__file__), "--leg", name,
+           "--steps", str(args.steps), "--warmup", str(args.warmup)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired:
+        return {"error": f"leg {name} timed out after {timeout} s"}
+    for line in reversed(r.stdout.strip().splitlines()):
+        if line.startswith("{"):
+            return json.loads(line)
+    return {"error": f"leg {name} exited {r.returncode}: {r.stderr.strip()[-300:]}"}
+
+
 def disk_peak(root: str, nbytes: int = 2 << 30) -> dict:
     """O_DIRECT write then read of one file through the native engine (8 threads,
     8 MiB pieces): the disk's own sequential bandwidth, the NVMe legs' denominator."""
@@ -952,8 +1069,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-config3", action="store_true", help="skip the real 10B offload leg")
+    ap.add_argument("--leg", default=None, choices=["config3_real"],
+                    help="run one heavy leg alone and print its JSON object")
     args = ap.parse_args()
     sys.path.insert(0, ROOT)
+    if args.leg == "config3_real":
+        import torch
+        torch.cuda.set_device(0)
+        print(json.dumps(_safe(config3_real_leg, args)), flush=True)
+        return 0
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
         print(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}",
               file=sys.stderr)
