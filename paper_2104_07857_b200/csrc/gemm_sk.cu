@@ -225,6 +225,12 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
 // side by side along N (a 256 x 512 cluster tile) that share A: CTA c of pair j loads
 // A rows [c*128 + j*64, +64) of the stage and multicasts them to CTA c of both pairs,
 // so each A byte crosses from L2 once per cluster (25 % less L2 -> SM traffic).
+// CL = 4 launches as a *preferred* cluster of 4 over regular clusters of 2: where a GPC
+// has no room for 4 more CTAs the hardware forms two pairs instead, so every SM runs.
+// The schedule is the same either way (blocks 4c .. 4c + 3 work on cluster tile items
+// of preferred cluster c, pair (blockIdx / 2) % 2 on its half); only the A loads differ
+// (a lone pair loads both 64-row halves itself), so the result does not depend on how
+// the clusters formed.
 // NS ring stages, EW epilogue warps (multiple of 4: EW / 4 warps share a TMEM lane
 // quadrant, splitting its 256 columns), BPW staging boxes per epilogue warp.
 template <bool A_MN, bool B_MN, int EPI, int NS, int EW, int BPW, int CL>
@@ -251,14 +257,20 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const uint32_t crank = rank & 1, pj = rank >> 1, lead = rank & ~1u;
+  // npair: pairs in this cluster as formed (CL = 4: 2, or 1 when it fell back to a pair);
+  // pj: which half of the cluster tile this pair computes (fixed by blockIdx); prank:
+  // the pair's index inside the formed cluster (multicast masks)
+  const uint32_t npair = CL == 4 ? cluster_nctarank() >> 1 : 1;
+  const uint32_t crank = rank & 1, prank = rank >> 1, lead = rank & ~1u;
+  const uint32_t pj = CL == 4 ? (blockIdx.x >> 1) & 1 : 0;
+  const uint32_t pos = blockIdx.x % CL;   // position in the (preferred) cluster: ws slots
   const bool leader = crank == 0;
   const int cid = blockIdx.x / CL;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NPAIR);        // every pair's MMAs released the slot
+      mbar_init(&empty[s], npair);        // every pair's MMAs released the slot
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tmem_full[a], 1);
@@ -299,11 +311,18 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (leader) mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
           if (NPAIR == 1) {
             load_rows<A_MN>(sA + s * A_BYTES, &tmA, lbar, kb * BK, m0);
-          } else {   // one 64-row box (K-major {64 k, 64 rows}; MN-major {64 mn, 64 k})
-            uint8_t* dst = sA + s * A_BYTES + pj * (A_BYTES / 2);
-            const int r = m0 + (int)pj * 64;
+          } else if (npair == 2) {   // one 64-row box (K-major {64 k, 64 rows}; MN-major {64 mn, 64 k})
+            uint8_t* dst = sA + s * A_BYTES + prank * (A_BYTES / 2);
+            const int r = m0 + (int)prank * 64;
             if (!A_MN) tma_load_2d_2sm_mc(dst, &tmA, lbar, kb * BK, r, (uint16_t)(AMASK << crank));
             else tma_load_2d_2sm_mc(dst, &tmA, lbar, r, kb * BK, (uint16_t)(AMASK << crank));
+          } else {                   // a lone pair: both 64-row boxes, no multicast
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint8_t* dst = sA + s * A_BYTES + h * (A_BYTES / 2);
+              if (!A_MN) tma_load_2d_2sm(dst, &tmA, lbar, kb * BK, m0 + 64 * h);
+              else tma_load_2d_2sm(dst, &tmA, lbar, m0 + 64 * h, kb * BK);
+            }
           }
           load_rows<B_MN>(sB + s * B_BYTES, &tmB, lbar, kb * BK, n0);
         }
@@ -316,8 +335,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       constexpr uint32_t idesc = idesc_bf16_f32(256, 256, A_MN, B_MN);
       constexpr uint64_t ka = A_MN ? (2 * 1024) >> 4 : 32 >> 4;   // per 16-deep k step
       constexpr uint64_t kb_ = B_MN ? (2 * 1024) >> 4 : 32 >> 4;
-      constexpr uint16_t ALL = (uint16_t)((1u << CL) - 1);
-      const uint16_t PAIR = (uint16_t)(0x3u << (2 * pj));
+      const uint16_t ALL = (uint16_t)((1u << (2 * npair)) - 1);
+      const uint16_t PAIR = (uint16_t)(0x3u << (2 * prank));
       const uint64_t da0 = sdesc_sw128(smem_u32(sA), A_MN ? MN_BOX_BYTES : 16);
       const uint64_t db0 = sdesc_sw128(smem_u32(sB), B_MN ? MN_BOX_BYTES : 16);
       Iter itr(sc, cid);
@@ -420,7 +439,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (lane == 0) {
             for (int qq = qlo; qq < qhi; ++qq) {
               if (sk_begin(sc, qq) == sk_begin(sc, qq + 1)) continue;   // empty range
-              const uint32_t* f = ws_flag + (size_t)(CL * qq + rank) * EW + e;
+              const uint32_t* f = ws_flag + (size_t)(CL * qq + pos) * EW + e;
               long long t0 = 0;
               while (ld_acquire(f) == 0) {
                 if (t0 == 0) t0 = clock64();
@@ -445,7 +464,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           for (int qq = qlo; qq < qhi; ++qq) {   // partials in cluster order
             if (sk_begin(sc, qq) == sk_begin(sc, qq + 1)) continue;
             const float4* s4 = reinterpret_cast<const float4*>(
-                                   ws_part + (size_t)(CL * qq + rank) * SLOT_FLOATS) +
+                                   ws_part + (size_t)(CL * qq + pos) * SLOT_FLOATS) +
                                (size_t)e * (CH * 16 * 32) + (size_t)c * 16 * 32 + lane;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -475,7 +494,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (w.role == ROLE_FINISH && lane == 0) {   // flags back to 0 for the next launch
           for (int qq = qlo; qq < qhi; ++qq)
             if (sk_begin(sc, qq) != sk_begin(sc, qq + 1))
-              ws_flag[(size_t)(CL * qq + rank) * EW + e] = 0u;
+              ws_flag[(size_t)(CL * qq + pos) * EW + e] = 0u;
         }
       }
       ++j;
@@ -611,13 +630,15 @@ static int max_clusters() {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) !=
         cudaSuccess)
       return 0;
+    // CL = 4 launches preferred clusters of 4 over regular pairs, so every resident pair
+    // runs: count resident pairs, two per preferred cluster
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL * 64);
+    cfg.gridDim = dim3(2 * 64);
     cfg.blockDim = dim3(64 + 32 * EW_);
     cfg.dynamicSmemBytes = SMEM;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.x = 2;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
@@ -625,8 +646,9 @@ static int max_clusters() {
     int c = 0;
     if (cudaOccupancyMaxActiveClusters(&c, kern, &cfg) != cudaSuccess || c <= 0) {
       cudaGetLastError();
-      c = sm_count() / CL;
+      c = sm_count() / 2;
     }
+    c = c * 2 / CL;
     n = c < sm_count() / CL ? c : sm_count() / CL;
   }
   return n;
@@ -664,13 +686,20 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   cfg.blockDim = dim3(64 + 32 * EW_);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (CL == 4) {   // clusters of 4 where a GPC has room, pairs elsewhere
+    at[1].id = cudaLaunchAttributePreferredClusterDimension;
+    at[1].val.preferredClusterDim.x = 4;
+    at[1].val.preferredClusterDim.y = 1;
+    at[1].val.preferredClusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
   ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, md, md2, static_cast<const __nv_bfloat16*>(bias),
                              static_cast<const uint16_t*>(X), ldx, M, N, sc, part, flag),
           "cudaLaunchKernelEx(zi_gemm_sk)");
