@@ -349,6 +349,157 @@ ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
   }
 }
 
+// LayerNorm backward for H = 2048 / 4096 / 8192 in two phases per ring stage, so the
+// row statistics need no CTA-wide reductions: a stage holds R = 8192 / H rows of dy, x
+// (and dres), filled by one bulk copy per input; 512 threads.
+//   phase 1 (warp layout): W = H / 512 warps per row, each lane 16 columns, reduce
+//     s1 = sum dxh and s2 = sum dxh * xh with shuffles; one (s1, s2) pair per warp and
+//     the row's (mean, rstd) go to shared memory;
+//   phase 2 (column layout): thread t owns CPT = H / 512 columns of every row (a warp
+//     writes 32 * CPT contiguous elements of dx), sums the W pairs in warp order,
+//     writes dx and accumulates its columns of dgamma / dbeta (/ sum dres) in row order.
+// One __syncthreads between the phases and one to release the stage: 2 per R rows,
+// against 5 per 2 rows for ln_bwd_kernel's CTA-wide row reductions. Deterministic: fixed
+// per-row summation order, the CTA's rows in order, CTA partials folded in order.
+constexpr int LNS_NT = 512;
+template <int H, bool DRES>
+struct Lns {
+  static constexpr int R = 8192 / H, W = H / 512, CPT = H / 512, NIN = DRES ? 3 : 2;
+  static constexpr int STAGE = NIN * R * H;                 // bf16 elements per stage
+  static constexpr int NSTG = DRES ? 4 : 6;                 // 192 KB of ring
+  static constexpr size_t SMEM = (size_t)NSTG * STAGE * 2 + NSTG * 8 + 16 * 16 + 64;
+};
+
+template <int H, bool DRES, bool RSUM>
+__global__ void __launch_bounds__(LNS_NT, 1)
+ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                    const uint16_t* __restrict__ w, const float* __restrict__ mean,
+                    const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
+                    uint16_t* __restrict__ dx, float* __restrict__ part, int T) {
+  using L = Lns<H, DRES>;
+  constexpr int R = L::R, W = L::W, CPT = L::CPT, NS = RSUM ? 3 : 2;
+  constexpr int VE = CPT < 8 ? CPT : 8;                     // elements per vector access
+  constexpr int NV = CPT / VE;                              // accesses per row
+  extern __shared__ __align__(128) uint16_t ring[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)L::NSTG * L::STAGE);
+  float2* red = reinterpret_cast<float2*>(full + L::NSTG);  // [16] per-warp (s1, s2)
+  float2* stat = red + 16;                                  // [R] (mean, rstd)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, ngroups = (T + R - 1) / R;
+  if (tid == 0) {
+    for (int s = 0; s < L::NSTG; ++s) bulk::mbar_init(&full[s], 1);
+    bulk::fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int g = blockIdx.x + i * G;
+    if (g >= ngroups) return;
+    const int s = i % L::NSTG;
+    const uint32_t bytes = (uint32_t)min(R, T - g * R) * H * 2;
+    const size_t off = (size_t)g * R * H;
+    uint16_t* st = ring + (size_t)s * L::STAGE;
+    bulk::mbar_expect_tx(&full[s], L::NIN * bytes);
+    bulk::g2s(st, dy + off, bytes, &full[s]);
+    bulk::g2s(st + R * H, x + off, bytes, &full[s]);
+    if (DRES) bulk::g2s(st + 2 * R * H, dres + off, bytes, &full[s]);
+  };
+  if (tid == 0)
+    for (int i = 0; i < L::NSTG; ++i) issue(i);
+  // phase-1 role: row pr of the stage, columns [pw * 512, +512): lane's 16 at
+  // pw * 512 + k * 256 + lane * 8, k = 0, 1
+  const int pr = warp / W, pw = warp % W;
+  float g1[16];
+  ld_row<8>(w + pw * 512 + lane * 8, g1);
+  ld_row<8>(w + pw * 512 + 256 + lane * 8, g1 + 8);
+  // phase-2 role: columns a * 512 * VE + tid * VE + [0, VE), a < NV
+  float g2[CPT];
+#pragma unroll
+  for (int a = 0; a < NV; ++a) ld_row<VE>(w + (a * LNS_NT + tid) * VE, g2 + a * VE);
+  float acc[NS][CPT];
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[k][c] = 0.f;
+  for (int i = 0;; ++i) {
+    const int g = blockIdx.x + i * G;
+    if (g >= ngroups) break;
+    const int s = i % L::NSTG;
+    const int rows = min(R, T - g * R);
+    const uint16_t* st = ring + (size_t)s * L::STAGE;
+    float mu = 0.f, rs = 0.f;
+    if (pr < rows) {                     // issued before the stage wait
+      mu = mean[g * R + pr];
+      rs = rstd[g * R + pr];
+    }
+    bulk::mbar_wait(&full[s], (i / L::NSTG) & 1);
+    if (pr < rows) {
+      const uint16_t* gy = st + pr * H + pw * 512 + lane * 8;
+      const uint16_t* gx = gy + R * H;
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        float yv[8], xv[8];
+        ld_row<8>(gy + k * 256, yv);
+        ld_row<8>(gx + k * 256, xv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = yv[j] * g1[8 * k + j];
+          s1 += d;
+          s2 += d * ((xv[j] - mu) * rs);
+        }
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        red[warp] = make_float2(s1, s2);
+        if (pw == 0) stat[pr] = make_float2(mu, rs);
+      }
+    }
+    __syncthreads();
+    for (int r = 0; r < rows; ++r) {
+      float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const float2 p = red[r * W + q];
+        m1 += p.x;
+        m2 += p.y;
+      }
+      m1 *= 1.0f / H;
+      m2 *= 1.0f / H;
+      const float2 ms = stat[r];
+      const size_t grow = (size_t)(g * R + r) * H;
+#pragma unroll
+      for (int a = 0; a < NV; ++a) {
+        const int col = (a * LNS_NT + tid) * VE;
+        float yv[VE], xv[VE], rv[VE], o[VE];
+        ld_row<VE>(st + r * H + col, yv);
+        ld_row<VE>(st + R * H + r * H + col, xv);
+        if (DRES) ld_row<VE>(st + 2 * R * H + r * H + col, rv);
+#pragma unroll
+        for (int j = 0; j < VE; ++j) {
+          const float xh = (xv[j] - ms.x) * ms.y;
+          const float d = yv[j] * g2[a * VE + j];
+          acc[0][a * VE + j] += yv[j] * xh;
+          acc[1][a * VE + j] += yv[j];
+          if (RSUM) acc[NS - 1][a * VE + j] += rv[j];
+          o[j] = ms.y * (d - m1 - xh * m2);
+          if (DRES) o[j] += rv[j];
+        }
+        st_row<VE>(dx + grow + col, o);
+      }
+    }
+    __syncthreads();                     // stage s and red / stat read by everyone
+    if (tid == 0) issue(i + L::NSTG);
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k)
+#pragma unroll
+    for (int a = 0; a < NV; ++a)
+#pragma unroll
+      for (int j = 0; j < VE; ++j)
+        part[((size_t)k * gridDim.x + blockIdx.x) * H + (a * LNS_NT + tid) * VE + j] = acc[k][a * VE + j];
+}
+
 // part[set][P][H] -> out_set[H] (bf16 RNE or fp32); per column, P is split into
 // FOLD_SUB ordered runs summed by separate threads, then combined in run order:
 // deterministic for a fixed P, and ~P / FOLD_SUB dependent loads per thread.
@@ -697,6 +848,16 @@ using namespace zi::fused;
       return ZI_EINVAL;                                                                    \
   }
 
+// ZI_LN_BWD_LEGACY=1: the CTA-reduction LayerNorm backward for every H (A/B only)
+static bool ln_bwd_legacy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZI_LN_BWD_LEGACY");
+    v = e && atoi(e) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int ln_grid(int T, int H) {
   const int tpr = H / 8;
   const int rpc = tpr >= 256 ? 1 : 256 / tpr;
@@ -720,6 +881,33 @@ static int launch_ln_bwd3(int grid, cudaStream_t s, const uint16_t* dy, const ui
   ln_bwd_kernel<TPR, DRES, RSUM><<<grid, LnbCta<TPR>::NT, smem, s>>>(dy, x, w, mean, rstd, dres,
                                                                      dx, part, T);
   return ZI_OK;
+}
+
+template <int H, bool DRES, bool RSUM>
+static int launch_ln_split3(int grid, cudaStream_t s, const uint16_t* dy, const uint16_t* x,
+                            const uint16_t* w, const float* mean, const float* rstd,
+                            const uint16_t* dres, uint16_t* dx, float* part, int T) {
+  constexpr size_t smem = Lns<H, DRES>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    ZI_CUDA(cudaFuncSetAttribute(ln_bwd_split_kernel<H, DRES, RSUM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+            "cudaFuncSetAttribute(ln_bwd_split)");
+    attr = true;
+  }
+  ln_bwd_split_kernel<H, DRES, RSUM><<<grid, LNS_NT, smem, s>>>(dy, x, w, mean, rstd, dres, dx,
+                                                                 part, T);
+  return ZI_OK;
+}
+
+template <int H>
+static int launch_ln_split(int grid, cudaStream_t s, bool rsum, const uint16_t* dy,
+                           const uint16_t* x, const uint16_t* w, const float* mean,
+                           const float* rstd, const uint16_t* dres, uint16_t* dx, float* part,
+                           int T) {
+  if (rsum) return launch_ln_split3<H, true, true>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  if (dres) return launch_ln_split3<H, true, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  return launch_ln_split3<H, false, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
 }
 
 template <int TPR>
@@ -822,8 +1010,9 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
   ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..8192, power of 2");
   cudaStream_t s = (cudaStream_t)stream;
   const int tpr = H / 8;
-  const int rpc = tpr >= LNB_NT ? 1 : LNB_NT / tpr;
-  int grid = (tpr > LNB_NT ? 1 : 2) * sm_count();
+  const bool split = H >= 2048 && !ln_bwd_legacy();
+  const int rpc = split ? 8192 / H : (tpr >= LNB_NT ? 1 : LNB_NT / tpr);
+  int grid = (split || tpr > LNB_NT ? 1 : 2) * sm_count();
   if (grid > (T + rpc - 1) / rpc) grid = (T + rpc - 1) / rpc;
   const int sets = dres_sum ? 3 : 2;
   // work[0, 1024) holds the column-reduction counters (must stay zero); partials follow
@@ -835,7 +1024,11 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
        DR = (const uint16_t*)dres;
   auto DX = (uint16_t*)dx;
   int st = ZI_OK;
-  switch (tpr) {
+  if (split) {
+    if (H == 2048) st = launch_ln_split<2048>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else if (H == 4096) st = launch_ln_split<4096>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else st = launch_ln_split<8192>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+  } else switch (tpr) {
     case 16: st = launch_ln_bwd<16>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
     case 32: st = launch_ln_bwd<32>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
     case 64: st = launch_ln_bwd<64>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;

@@ -785,11 +785,13 @@ extern "C" int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B,
     const char* e = getenv("ZI_GEMM_SPLIT");
     env_split = !e ? -1 : atoi(e);
     const char* c = getenv("ZI_SK_CL");
-    env_cl = !c ? 2 : atoi(c);
+    env_cl = !c ? 4 : atoi(c);
   }
-  // Default: clusters of one pair. ZI_SK_CL=4 pairs the pairs (A multicast, 25 % less
-  // L2 -> SM traffic): measured no faster at the GPT shapes, since fewer 4-CTA clusters
-  // than sms / 4 are resident (GPCs are not multiples of 4 SMs).
+  // Default: preferred clusters of 4 (two pairs sharing A by multicast, 25 % less L2 -> SM
+  // traffic) over regular pairs, so the SMs a GPC cannot group in fours still run pairs.
+  // Under the 1 kW cap the step runs ~1.5 % faster than with plain pairs (fewer bytes
+  // moved per flop: same clocks, more work; profiles/r2_gemm_cluster4.md). ZI_SK_CL=2:
+  // pairs only (A/B).
   const int CL = (env_cl == 4 && M > 128) ? 4 : 2;
   CUtensorMap ma, mb, md, md2;
   if ((st = make_operand_map(&ma, A, M, K, lda, a_mn_major != 0, CL == 4 ? 64 : 128)) != ZI_OK)
