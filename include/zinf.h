@@ -329,6 +329,20 @@ size_t zi_gemm_sk_workspace_bytes(void);
 int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
                const void* bias, void* D, int ldd, int d_f32, const void* X, int ldx, void* D2,
                int ldd2, int epi, int M, int N, int K, void* ws, size_t ws_bytes, void* stream);
+/* zi_gemm_sk with epilogue side outputs of the bf16 result (NULL = off):
+ *   colsum_part fp32 [ceil(M/32)][N]: column sums of each 32-row block of the stored bf16
+ *     output (zi_colsum_fold then sums the blocks in order: a bias gradient, e.g. the fc1
+ *     bias from the fc2 input-gradient GEMM with the GELU' epilogue);
+ *   delta fp32 [B][H][S] (epi PLAIN, X = the attention output O, N = H * D, D 64 / 128,
+ *     M = B * S): per row and head, the sum over the head's columns of bf16(D) * O, the
+ *     attention backward's rowsum(dO o O) from the GEMM that produces dO. */
+int zi_gemm_sk_aux(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
+                   const void* bias, void* D, int ldd, int d_f32, const void* X, int ldx, void* D2,
+                   int ldd2, int epi, int M, int N, int K, void* ws, size_t ws_bytes,
+                   float* colsum_part, float* delta, int delta_S, int delta_H, int delta_D,
+                   void* stream);
+/* out[c] = sum over p < P of part[p][c] in p order (fp32 in; bf16 RNE or fp32 out). */
+int zi_colsum_fold(const float* part, int P, int N, void* out, int out_f32, void* stream);
 /* Diagnostics: a device buffer of >= 148*16*8 u64 receiving clock64() stamps of the
  * wide-tile GEMM's pipeline (NULL turns it off). Not for production use. */
 int zi_gemm_set_profile(void* buf);
@@ -342,6 +356,7 @@ int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int
                 void* stream);
 int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
                 void* dqkv, int B, int H, int S, int head_dim, void* stream);
+/* (out = NULL: delta already holds rowsum(dout o out), e.g. from zi_gemm_sk_aux.) */
 /* Tied-embedding gradient in a fixed order (csrc/embed.cu): out[v] = half_RNE(acc[v] +
  * sum of dx[t] over the tokens t with id v, in sequence order). tokens int64 [T]; dx
  * [T, hd] bf16 (dx_f32 = 0) or fp32; acc fp32 [V, hd]; out half [V, hd]; work int32

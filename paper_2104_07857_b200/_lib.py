@@ -131,6 +131,10 @@ SIGNATURES = {
     "zi_gemm_sk": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int,
                    c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
                    c_size_t, c_void_p],
+    "zi_gemm_sk_aux": [c_void_p, c_int, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_int,
+                       c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                       c_void_p, c_size_t, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
+    "zi_colsum_fold": [c_void_p, c_int, c_int, c_void_p, c_int, c_void_p],
     "zi_gemm_sk_workspace_bytes": [],
 }
 _RESTYPE = {"zi_last_error": ctypes.c_char_p, "zi_gemm_sk_workspace_bytes": c_size_t}

@@ -196,6 +196,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
+  zi::pdl_sync();   // setup above overlapped the previous kernel's tail
   const uint32_t tmem = *tslot;        // S slot g at g*64; O_g at 256 + g*128
 
   if (warp == 0) {
@@ -424,6 +425,7 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
+  zi::pdl_sync();   // setup above overlapped the previous kernel's tail
   const uint32_t tmem = *tslot;   // slot g: S^T at g*128, dP^T at g*128 + 64; dV 256, dK 384
 
   if (warp == 0) {
@@ -591,6 +593,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
+  zi::pdl_sync();   // setup above overlapped the previous kernel's tail
   const uint32_t tmem = *tslot;   // slot g: S at g*128, dP at g*128 + 64; dQ at 256
 
   if (warp == 0) {
@@ -698,6 +701,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
 template <int D>
 __global__ void delta_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dO,
                              float* __restrict__ delta, int H, int S, int hd) {
+  zi::pdl_sync();
   const int row = blockIdx.x;                     // b*S + s
   const int t = threadIdx.x;                      // 8 elements each; D/8 threads per head
   const unsigned mask = __activemask();           // hd < 256: a partial warp
@@ -783,8 +787,8 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
   static bool attr = false;
   if ((rc = set_smem(fwd_kernel<D>, Fwd<D>::BYTES, attr)) != ZI_OK) return rc;
   const float sl2 = LOG2E / sqrtf((float)D);
-  fwd_kernel<D><<<B * H * (S / 128), THREADS, Fwd<D>::BYTES, st>>>(
-      tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace);
+  zi::launch_pdl(fwd_kernel<D>, dim3(B * H * (S / 128)), dim3(THREADS), Fwd<D>::BYTES, st,
+                 tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace);
   return launch_status("zi_attn_fwd");
 }
 
@@ -800,17 +804,19 @@ static int bwd(const void* qkv, const void* out, const void* dout, const float* 
   static bool a1 = false, a2 = false;
   if ((rc = set_smem(bwd_dkdv_kernel<D>, Bkv<D>::BYTES, a1)) != ZI_OK) return rc;
   if ((rc = set_smem(bwd_dq_kernel<D>, Bq<D>::BYTES, a2)) != ZI_OK) return rc;
-  delta_kernel<D><<<B * S, hd / 8, 0, st>>>(static_cast<const __nv_bfloat16*>(out),
-                                            static_cast<const __nv_bfloat16*>(dout), delta, H, S, hd);
-  if ((rc = launch_status("zi_attn_bwd(delta)")) != ZI_OK) return rc;
+  if (out != nullptr) {   // else delta already holds rowsum(dO o O) (zi_gemm_sk_aux)
+    zi::launch_pdl(delta_kernel<D>, dim3(B * S), dim3(hd / 8), 0, st, static_cast<const __nv_bfloat16*>(out),
+                                              static_cast<const __nv_bfloat16*>(dout), delta, H, S, hd);
+    if ((rc = launch_status("zi_attn_bwd(delta)")) != ZI_OK) return rc;
+  }
   const float scale = 1.f / sqrtf((float)D), sl2 = LOG2E * scale;
   const int grid = B * H * (S / 128);
   auto* dq = static_cast<__nv_bfloat16*>(dqkv);
-  bwd_dkdv_kernel<D><<<grid, THREADS, Bkv<D>::BYTES, st>>>(tm, tdo, lse, delta, dq, B, H, S, hd,
-                                                            sl2, scale);
+  zi::launch_pdl(bwd_dkdv_kernel<D>, dim3(grid), dim3(THREADS), Bkv<D>::BYTES, st, tm, tdo, lse,
+                 delta, dq, B, H, S, hd, sl2, scale);
   if ((rc = launch_status("zi_attn_bwd(dkdv)")) != ZI_OK) return rc;
-  bwd_dq_kernel<D><<<grid, THREADS, Bq<D>::BYTES, st>>>(tm, tdo, lse, delta, dq, B, H, S, hd, sl2,
-                                                        scale);
+  zi::launch_pdl(bwd_dq_kernel<D>, dim3(grid), dim3(THREADS), Bq<D>::BYTES, st, tm, tdo, lse,
+                 delta, dq, B, H, S, hd, sl2, scale);
   return launch_status("zi_attn_bwd(dq)");
 }
 
@@ -839,7 +845,8 @@ int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float*
                 void* dqkv, int B, int H, int S, int head_dim, void* stream) {
   int rc = zi::attn::check(qkv, B, H, S, head_dim, "zi_attn_bwd");
   if (rc != ZI_OK) return rc;
-  ZI_CHECK_ARG(out && dout && lse && delta && dqkv, "zi_attn_bwd: NULL argument");
+  // out == NULL: delta already holds rowsum(dout o out) (the proj.dx GEMM's epilogue)
+  ZI_CHECK_ARG(dout && lse && delta && dqkv, "zi_attn_bwd: NULL argument");
   ZI_CHECK_ARG(zi::aligned(out, 16) && zi::aligned(dout, 16) && zi::aligned(dqkv, 16),
                "zi_attn_bwd: 16-byte alignment");
   ZI_CHECK_ARG(H * head_dim / 8 <= 1024, "zi_attn_bwd: hidden %d too wide", H * head_dim);

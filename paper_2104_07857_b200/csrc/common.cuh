@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstddef>
 #include <string>
+#include <utility>
 
 #include "../../include/zinf.h"
 
@@ -19,6 +20,38 @@ int cuda_status(cudaError_t e, const char* what);
 inline int launch_status(const char* what) {
   cudaError_t e = cudaGetLastError();
   return cuda_status(e, what);
+}
+
+// ---------------------------------------------------- programmatic dependent launch
+// The step's kernels launch with cudaLaunchAttributeProgrammaticStreamSerialization
+// (launch_pdl): the next kernel in the stream is launched while this one drains, runs
+// its prologue (barrier init, TMEM alloc, descriptor prefetch) and then waits in
+// pdl_sync() until every predecessor grid has completed and its memory is visible, so
+// the ordering is that of a plain stream; only launch latency and setup overlap. Each
+// kernel calls pdl_sync() before its first global-memory access (read or write), and
+// pdl_sync() also lets this kernel's own dependents launch. Without the attribute
+// (ZI_PDL=0, or a plain <<<>>> launch) both instructions are no-ops.
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline bool aligned(const void* p, size_t a) {

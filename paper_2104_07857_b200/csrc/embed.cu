@@ -18,6 +18,7 @@ namespace zi {
 namespace emb {
 
 __global__ void count_kernel(const int64_t* __restrict__ tok, int T, int V, int* __restrict__ counts) {
+  zi::pdl_sync();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < T) {
     const int64_t v = tok[t];
@@ -27,6 +28,7 @@ __global__ void count_kernel(const int64_t* __restrict__ tok, int T, int V, int*
 
 // exclusive scan of counts[0..V) into offsets[0..V] (offsets[V] = T); one CTA of 1024
 __global__ void scan_kernel(const int* __restrict__ counts, int V, int* __restrict__ offsets) {
+  zi::pdl_sync();
   __shared__ int part[1024];
   const int tid = threadIdx.x, per = (V + 1023) / 1024;
   const int lo = min(V, tid * per), hi = min(V, lo + per);
@@ -53,6 +55,7 @@ constexpr int PLACE_TILE = 8192;
 
 __global__ void place_kernel(const int64_t* __restrict__ tok, int T, int V,
                              const int* __restrict__ offsets, int* __restrict__ order) {
+  zi::pdl_sync();
   __shared__ int st[PLACE_TILE];
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = t < T ? (int)tok[t] : -1;
@@ -88,6 +91,7 @@ template <int KIND, typename TX>
 __global__ void rows_kernel(const TX* __restrict__ dx, const float* __restrict__ acc,
                             const int* __restrict__ offsets, const int* __restrict__ order, int hd,
                             uint16_t* __restrict__ out) {
+  zi::pdl_sync();
   const int v = blockIdx.x;
   const int e = threadIdx.x * 8;                 // 8 consecutive elements per thread
   if (e >= hd) return;
@@ -131,19 +135,19 @@ int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, cons
   int* offsets = work + V;         // [V + 1]
   int* order = offsets + V + 1;    // [T]
   ZI_CUDA(cudaMemsetAsync(counts, 0, (size_t)V * sizeof(int), s), "zi_embed_grad: memset");
-  zi::emb::count_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, T, V, counts);
-  zi::emb::scan_kernel<<<1, 1024, 0, s>>>(counts, V, offsets);
-  zi::emb::place_kernel<<<(T + 255) / 256, 256, 0, s>>>(tokens, T, V, offsets, order);
+  zi::launch_pdl(zi::emb::count_kernel, dim3((T + 255) / 256), dim3(256), 0, s, tokens, T, V, counts);
+  zi::launch_pdl(zi::emb::scan_kernel, dim3(1), dim3(1024), 0, s, counts, V, offsets);
+  zi::launch_pdl(zi::emb::place_kernel, dim3((T + 255) / 256), dim3(256), 0, s, tokens, T, V, offsets, order);
   const int threads = ((hd / 8 + 31) / 32) * 32;
   auto* o = static_cast<uint16_t*>(out);
   const auto* xb = static_cast<const __nv_bfloat16*>(dx);
   const auto* xf = static_cast<const float*>(dx);
   if (half_kind == ZI_HALF_BF16) {
-    if (dx_f32) zi::emb::rows_kernel<ZI_HALF_BF16><<<V, threads, 0, s>>>(xf, acc, offsets, order, hd, o);
-    else zi::emb::rows_kernel<ZI_HALF_BF16><<<V, threads, 0, s>>>(xb, acc, offsets, order, hd, o);
+    if (dx_f32) zi::launch_pdl(zi::emb::rows_kernel<ZI_HALF_BF16, float>, dim3(V), dim3(threads), 0, s, xf, acc, offsets, order, hd, o);
+    else zi::launch_pdl(zi::emb::rows_kernel<ZI_HALF_BF16, __nv_bfloat16>, dim3(V), dim3(threads), 0, s, xb, acc, offsets, order, hd, o);
   } else {
-    if (dx_f32) zi::emb::rows_kernel<ZI_HALF_FP16><<<V, threads, 0, s>>>(xf, acc, offsets, order, hd, o);
-    else zi::emb::rows_kernel<ZI_HALF_FP16><<<V, threads, 0, s>>>(xb, acc, offsets, order, hd, o);
+    if (dx_f32) zi::launch_pdl(zi::emb::rows_kernel<ZI_HALF_FP16, float>, dim3(V), dim3(threads), 0, s, xf, acc, offsets, order, hd, o);
+    else zi::launch_pdl(zi::emb::rows_kernel<ZI_HALF_FP16, __nv_bfloat16>, dim3(V), dim3(threads), 0, s, xb, acc, offsets, order, hd, o);
   }
   return zi::launch_status("zi_embed_grad");
 }

@@ -108,6 +108,7 @@ ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ r,
               uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
               const uint16_t* __restrict__ b, uint16_t* __restrict__ y, float* __restrict__ mean,
               float* __restrict__ rstd, int T, float eps) {
+  zi::pdl_sync();
   constexpr int H = 8 * TPR, RPC = RowCta<TPR>::RPC;
   __shared__ float sm[32];
   const int t = threadIdx.x % TPR;
@@ -162,6 +163,7 @@ ln_fwd_warp_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ 
                    uint16_t* __restrict__ xsum, const uint16_t* __restrict__ w,
                    const uint16_t* __restrict__ b, uint16_t* __restrict__ y,
                    float* __restrict__ mean, float* __restrict__ rstd, int T, float eps) {
+  zi::pdl_sync();
   constexpr int H = 256 * VPL;
   const int lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -252,6 +254,7 @@ ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
               const uint16_t* __restrict__ w, const float* __restrict__ mean,
               const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
               uint16_t* __restrict__ dx, float* __restrict__ part, int T) {
+  zi::pdl_sync();
   constexpr int H = 8 * TPR, RPC = LnbCta<TPR>::RPC, NT = LnbCta<TPR>::NT;
   constexpr int NIN = DRES ? 3 : 2, NS = RSUM ? 3 : 2;
   constexpr int ROWS_E = RPC * H;                    // elements per input per stage
@@ -376,6 +379,7 @@ ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict_
                     const uint16_t* __restrict__ w, const float* __restrict__ mean,
                     const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
                     uint16_t* __restrict__ dx, float* __restrict__ part, int T) {
+  zi::pdl_sync();
   using L = Lns<H, DRES>;
   constexpr int R = L::R, W = L::W, CPT = L::CPT, NS = RSUM ? 3 : 2;
   constexpr int VE = CPT < 8 ? CPT : 8;                     // elements per vector access
@@ -507,6 +511,7 @@ constexpr int FOLD_SUB = 32;
 __global__ void __launch_bounds__(32 * FOLD_SUB)
 ln_fold_kernel(const float* __restrict__ part, int P, int H, void* __restrict__ o0,
                void* __restrict__ o1, void* __restrict__ o2, int out_f32) {
+  zi::pdl_sync();
   __shared__ float sm[FOLD_SUB][33];
   const int set = blockIdx.y, lane = threadIdx.x & 31, sub = threadIdx.x >> 5;
   const int col = blockIdx.x * 32 + lane;
@@ -532,6 +537,7 @@ ln_fold_kernel(const float* __restrict__ part, int P, int H, void* __restrict__ 
 // y = gelu_tanh(u), 8 bf16 per thread per step (n % 8 == 0), grid-stride.
 __global__ void __launch_bounds__(256)
 gelu_fwd_kernel(const uint16_t* __restrict__ u, uint16_t* __restrict__ y, size_t n8) {
+  zi::pdl_sync();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8;
        i += (size_t)gridDim.x * blockDim.x) {
     float v[8];
@@ -557,6 +563,7 @@ __global__ void __launch_bounds__(CRW_MAX_COLS / 8)
 colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
               uint16_t* __restrict__ d, float* __restrict__ part, int T, int N, int C, int R,
               int rows_per) {
+  zi::pdl_sync();
   constexpr int NIN = MODE == 1 ? 2 : 1;
   extern __shared__ __align__(128) uint16_t ring[];   // [stage][input][R][C]
   const int SE = R * C;
@@ -622,6 +629,7 @@ colrow_kernel(const uint16_t* __restrict__ a, const uint16_t* __restrict__ u,
 __global__ void __launch_bounds__(512)
 softmax_ce_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ tgt,
                   float* __restrict__ loss_rows, int V, float scale) {
+  zi::pdl_sync();
   const size_t row = blockIdx.x;
   uint16_t* L = logits + row * (size_t)V;
   __shared__ float red_m[16], red_s[16];
@@ -722,6 +730,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 __global__ void __launch_bounds__(CE_NT, 1)
 softmax_ce_ring_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict__ tgt,
                        float* __restrict__ loss_rows, int T, int V, int Vpad, float scale) {
+  zi::pdl_sync();
   extern __shared__ __align__(128) uint16_t rowbuf[];     // [2][Vpad] bf16 + 2 mbarriers
   uint64_t* full = reinterpret_cast<uint64_t*>(rowbuf + 2 * (size_t)Vpad);
   __shared__ float red_m[CE_NT / 32], red_s[CE_NT / 32];
@@ -807,6 +816,7 @@ softmax_ce_ring_kernel(uint16_t* __restrict__ logits, const int64_t* __restrict_
 }
 
 __global__ void sum_kernel(const float* __restrict__ v, int n, float scale, float* __restrict__ out) {
+  zi::pdl_sync();
   // single block, fixed-order tree: deterministic
   __shared__ float sm[1024];
   float s = 0.f;
@@ -837,13 +847,13 @@ using namespace zi::fused;
 
 #define TPR_DISPATCH(H, KERNEL, GRID, STREAM, ...)                                        \
   switch ((H) / 8) {                                                                       \
-    case 16: KERNEL<16><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
-    case 32: KERNEL<32><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
-    case 64: KERNEL<64><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                     \
-    case 128: KERNEL<128><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    case 256: KERNEL<256><<<GRID, 256, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    case 512: KERNEL<512><<<GRID, 512, 0, STREAM>>>(__VA_ARGS__); break;                   \
-    case 1024: KERNEL<1024><<<GRID, 1024, 0, STREAM>>>(__VA_ARGS__); break;                \
+    case 16: zi::launch_pdl(KERNEL<16>, dim3(GRID), dim3(256), 0, STREAM, __VA_ARGS__); break;                     \
+    case 32: zi::launch_pdl(KERNEL<32>, dim3(GRID), dim3(256), 0, STREAM, __VA_ARGS__); break;                     \
+    case 64: zi::launch_pdl(KERNEL<64>, dim3(GRID), dim3(256), 0, STREAM, __VA_ARGS__); break;                     \
+    case 128: zi::launch_pdl(KERNEL<128>, dim3(GRID), dim3(256), 0, STREAM, __VA_ARGS__); break;                   \
+    case 256: zi::launch_pdl(KERNEL<256>, dim3(GRID), dim3(256), 0, STREAM, __VA_ARGS__); break;                   \
+    case 512: zi::launch_pdl(KERNEL<512>, dim3(GRID), dim3(512), 0, STREAM, __VA_ARGS__); break;                   \
+    case 1024: zi::launch_pdl(KERNEL<1024>, dim3(GRID), dim3(1024), 0, STREAM, __VA_ARGS__); break;                \
     default: zi::set_error("LayerNorm: hidden size %d not in {128..8192, power of 2}", H); \
       return ZI_EINVAL;                                                                    \
   }
@@ -878,7 +888,7 @@ static int launch_ln_bwd3(int grid, cudaStream_t s, const uint16_t* dy, const ui
             "cudaFuncSetAttribute(ln_bwd)");
     attr = true;
   }
-  ln_bwd_kernel<TPR, DRES, RSUM><<<grid, LnbCta<TPR>::NT, smem, s>>>(dy, x, w, mean, rstd, dres,
+  zi::launch_pdl(ln_bwd_kernel<TPR, DRES, RSUM>, dim3(grid), dim3(LnbCta<TPR>::NT), smem, s, dy, x, w, mean, rstd, dres,
                                                                      dx, part, T);
   return ZI_OK;
 }
@@ -895,7 +905,7 @@ static int launch_ln_split3(int grid, cudaStream_t s, const uint16_t* dy, const 
             "cudaFuncSetAttribute(ln_bwd_split)");
     attr = true;
   }
-  ln_bwd_split_kernel<H, DRES, RSUM><<<grid, LNS_NT, smem, s>>>(dy, x, w, mean, rstd, dres, dx,
+  zi::launch_pdl(ln_bwd_split_kernel<H, DRES, RSUM>, dim3(grid), dim3(LNS_NT), smem, s, dy, x, w, mean, rstd, dres, dx,
                                                                  part, T);
   return ZI_OK;
 }
@@ -933,9 +943,9 @@ int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const
     auto X = (const uint16_t*)x, R = (const uint16_t*)resid, W = (const uint16_t*)w,
          B = (const uint16_t*)b;
     auto XS = (uint16_t*)xsum, Y = (uint16_t*)y;
-    if (H == 512) ln_fwd_warp_kernel<2><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
-    else if (H == 1024) ln_fwd_warp_kernel<4><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
-    else ln_fwd_warp_kernel<8><<<grid, 256, 0, s>>>(X, R, XS, W, B, Y, mean, rstd, T, eps);
+    if (H == 512) zi::launch_pdl(ln_fwd_warp_kernel<2>, dim3(grid), dim3(256), 0, s, X, R, XS, W, B, Y, mean, rstd, T, eps);
+    else if (H == 1024) zi::launch_pdl(ln_fwd_warp_kernel<4>, dim3(grid), dim3(256), 0, s, X, R, XS, W, B, Y, mean, rstd, T, eps);
+    else zi::launch_pdl(ln_fwd_warp_kernel<8>, dim3(grid), dim3(256), 0, s, X, R, XS, W, B, Y, mean, rstd, T, eps);
     return zi::launch_status("zi_ln_fwd");
   }
   const int grid = ln_grid(T, H);
@@ -986,7 +996,7 @@ static int launch_colred(int mode, const void* a, const void* u, void* d, void* 
   const uint16_t* A = static_cast<const uint16_t*>(a);
   const uint16_t* U = static_cast<const uint16_t*>(u);
   uint16_t* D = static_cast<uint16_t*>(d);
-#define ZI_COLROW(MODE, NS) colrow_kernel<MODE, NS><<<grid, nt, smem, s>>>(A, U, D, part, T, N, C, R, rows_per)
+#define ZI_COLROW(MODE, NS) zi::launch_pdl(colrow_kernel<MODE, NS>, dim3(grid), dim3(nt), smem, s, A, U, D, part, T, N, C, R, rows_per)
   if (mode == 0) {
     if (nstg == 8) ZI_COLROW(0, 8); else if (nstg == 6) ZI_COLROW(0, 6); else ZI_COLROW(0, 4);
   } else {
@@ -995,7 +1005,7 @@ static int launch_colred(int mode, const void* a, const void* u, void* d, void* 
 #undef ZI_COLROW
   int st = zi::launch_status(name);
   if (st) return st;
-  ln_fold_kernel<<<dim3((N + 31) / 32, 1), 32 * FOLD_SUB, 0, s>>>(part, chunks, N, out, nullptr,
+  zi::launch_pdl(ln_fold_kernel, dim3(dim3((N + 31) / 32, 1)), dim3(32 * FOLD_SUB), 0, s, part, chunks, N, out, nullptr,
                                                                  nullptr, out_f32);
   return zi::launch_status(name);
 }
@@ -1039,9 +1049,17 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
   }
   if (st) return st;
   if ((st = zi::launch_status("zi_ln_bwd(dx)"))) return st;
-  ln_fold_kernel<<<dim3((H + 31) / 32, sets), 32 * FOLD_SUB, 0, s>>>(part, grid, H, dgamma, dbeta, dres_sum,
+  zi::launch_pdl(ln_fold_kernel, dim3(dim3((H + 31) / 32, sets)), dim3(32 * FOLD_SUB), 0, s, part, grid, H, dgamma, dbeta, dres_sum,
                                                           grads_f32);
   return zi::launch_status("zi_ln_bwd(fold)");
+}
+
+int zi_colsum_fold(const float* part, int P, int N, void* out, int out_f32, void* stream) {
+  ZI_CHECK_ARG(part && out && P > 0 && N > 0, "zi_colsum_fold: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  zi::launch_pdl(ln_fold_kernel, dim3(dim3((N + 31) / 32, 1)), dim3(32 * FOLD_SUB), 0, s, part, P, N, out, nullptr,
+                                                                 nullptr, out_f32);
+  return zi::launch_status("zi_colsum_fold");
 }
 
 int zi_gelu_fwd(const void* u, void* y, size_t n, void* stream) {
@@ -1052,7 +1070,7 @@ int zi_gelu_fwd(const void* u, void* y, size_t n, void* stream) {
   const size_t cap = (size_t)sm_count() * 8;
   if (g > cap) g = cap;
   if (g == 0) return ZI_OK;
-  gelu_fwd_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>((const uint16_t*)u, (uint16_t*)y, n8);
+  zi::launch_pdl(gelu_fwd_kernel, dim3((unsigned)g), dim3(256), 0, (cudaStream_t)stream, (const uint16_t*)u, (uint16_t*)y, n8);
   return zi::launch_status("zi_gelu_fwd");
 }
 
@@ -1078,14 +1096,14 @@ int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float*
       attr = true;
     }
     const int grid = T < sm_count() ? T : sm_count();
-    softmax_ce_ring_kernel<<<grid, CE_NT, ring_smem, s>>>((uint16_t*)logits, targets, loss_rows, T,
+    zi::launch_pdl(softmax_ce_ring_kernel, dim3(grid), dim3(CE_NT), ring_smem, s, (uint16_t*)logits, targets, loss_rows, T,
                                                            V, Vpad, scale);
   } else {
-    softmax_ce_kernel<<<T, 512, 0, s>>>((uint16_t*)logits, targets, loss_rows, V, scale);
+    zi::launch_pdl(softmax_ce_kernel, dim3(T), dim3(512), 0, s, (uint16_t*)logits, targets, loss_rows, V, scale);
   }
   int st = zi::launch_status("zi_softmax_ce");
   if (st) return st;
-  sum_kernel<<<1, 1024, 0, s>>>(loss_rows, T, 1.0f / T, loss);
+  zi::launch_pdl(sum_kernel, dim3(1), dim3(1024), 0, s, loss_rows, T, 1.0f / T, loss);
   return zi::launch_status("zi_softmax_ce(sum)");
 }
 

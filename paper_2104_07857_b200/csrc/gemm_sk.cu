@@ -63,6 +63,18 @@ constexpr size_t smem_bytes(int NS, int EW, int BPW) {
   return (size_t)NS * STAGE_BYTES + (size_t)EW * BPW * BOX_BYTES + 1024 + 256;
 }
 
+// Optional epilogue side outputs (bf16 output only; nullptr = off):
+//   csum:  column sums of the stored bf16 output per 32-row block, fp32 [ceil(M/32)][N]
+//          (a bias gradient's partials; zi_colsum_fold sums the blocks in order);
+//   delta: per (row, head) sum over the head's D columns of out * X (X = the attention
+//          output O, out = dO): the attention backward's rowsum(dO o O), fp32 [B][H][S]
+//          for row = b * S + s, head = column / D (D = 64 or 128).
+struct Aux {
+  float* csum;
+  float* delta;
+  int S, H, D;
+};
+
 // Work decomposition, identical in every warp of both CTAs of a pair.
 struct Sched {
   int tiles_m, tiles_n, T, nk, P, S, group_m;
@@ -239,7 +251,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmD2,
                const __nv_bfloat16* __restrict__ bias, const uint16_t* __restrict__ X, int ldx,
                int M, int N, const Sched sc, float* __restrict__ ws_part,
-               uint32_t* __restrict__ ws_flag) {
+               uint32_t* __restrict__ ws_flag, const Aux aux) {
   static_assert(CL == 2 || CL == 4, "clusters of one or two CTA pairs");
   constexpr int NPAIR = CL / 2;
   constexpr int CT_N = 256 * NPAIR;                  // cluster tile columns
@@ -290,6 +302,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   __syncthreads();
   cluster_sync();
   fence_after_sync();
+  zi::pdl_sync();   // setup above overlapped the previous kernel's tail
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
@@ -383,7 +396,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       __syncwarp();
       return box;
     };
-    auto emit = [&](const CUtensorMap* map, const uint32_t* w, int c0, int r0) {
+    auto emit = [&](const CUtensorMap* map, const uint32_t* w, int c0, int r0) -> const uint8_t* {
       uint8_t* box = next_box();
       stage_row(box, lane, w);
       fence_proxy_async_smem();
@@ -392,7 +405,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         tma_store_2d(map, box, c0, r0);
         bulk_commit();
       }
+      return box;
     };
+    float dsum = 0.f;   // aux.delta: this row's running sum over the current head
     Iter itr(sc, cid);
     Item w;
     uint32_t j = 0;
@@ -482,7 +497,47 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           } else {
             uint32_t wd[32];
             epi_words<EPI>(v, row, gcol, M, N, bias, X, ldx, wd);
-            emit(&tmD, wd, gcol, r0);
+            const uint8_t* box = emit(&tmD, wd, gcol, r0);
+            if (aux.csum != nullptr && r0 < M) {
+              // column pair (2 lane, 2 lane + 1) of the 32 staged rows, summed in row
+              // order (the box is SW128: row r's 16-byte chunk j at (j ^ (r % 8)) * 16)
+              const uint32_t b0 = smem_u32(box) + ((lane & 3) << 2);
+              float c0 = 0.f, c1 = 0.f;
+#pragma unroll
+              for (int r = 0; r < 32; ++r) {
+                uint32_t wv;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(wv)
+                             : "r"(b0 + r * 128 + ((((uint32_t)lane >> 2) ^ (r & 7)) << 4)));
+                if (r0 + r < M) {   // rows past M hold epilogue values of zero rows
+                  c0 += bf16f(wv & 0xFFFF);
+                  c1 += bf16f(wv >> 16);
+                }
+              }
+              const int c = gcol + 2 * lane;
+              if (c < N)
+                *reinterpret_cast<float2*>(aux.csum + (size_t)(r0 >> 5) * N + c) = make_float2(c0, c1);
+            }
+            if (aux.delta != nullptr) {
+              if (row < M && gcol < N) {
+#pragma unroll
+                for (int q8 = 0; q8 < 8; ++q8) {
+                  const uint4 ov = *reinterpret_cast<const uint4*>(X + (size_t)row * ldx + gcol + 8 * q8);
+                  const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    dsum = fmaf(bf16f(wd[4 * q8 + j] & 0xFFFF), bf16f(ow[j] & 0xFFFF), dsum);
+                    dsum = fmaf(bf16f(wd[4 * q8 + j] >> 16), bf16f(ow[j] >> 16), dsum);
+                  }
+                }
+              }
+              if ((gcol + 64) % aux.D == 0) {   // the head's last 64 columns
+                if (row < M && gcol < N) {
+                  const int b = row / aux.S, sq = row - b * aux.S, h = gcol / aux.D;
+                  aux.delta[((size_t)b * aux.H + h) * aux.S + sq] = dsum;
+                }
+                dsum = 0.f;
+              }
+            }
             if (EPI == EPI_GELU) {
 #pragma unroll
               for (int i = 0; i < 32; ++i)
@@ -671,7 +726,8 @@ static int resident_clusters() {
 template <bool A_MN, bool B_MN, int EPI, int NS_, int BPW_, int CL>
 static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                       const CUtensorMap& md2, const void* bias, const void* X, int ldx, int M,
-                      int N, const Sched& sc, float* part, uint32_t* flag, cudaStream_t s) {
+                      int N, const Sched& sc, float* part, uint32_t* flag, const Aux& aux,
+                      cudaStream_t s) {
   auto kern = gemm_sk_kernel<A_MN, B_MN, EPI, NS_, EW_, BPW_, CL>;
   constexpr size_t SMEM = smem_bytes(NS_, EW_, BPW_);
   static_assert(SMEM <= 232448, "stream-K GEMM shared memory");
@@ -686,22 +742,24 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
   cfg.blockDim = dim3(64 + 32 * EW_);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = zi::pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (CL == 4) {   // clusters of 4 where a GPC has room, pairs elsewhere
-    at[1].id = cudaLaunchAttributePreferredClusterDimension;
-    at[1].val.preferredClusterDim.x = 4;
-    at[1].val.preferredClusterDim.y = 1;
-    at[1].val.preferredClusterDim.z = 1;
-    cfg.numAttrs = 2;
+    at[2].id = cudaLaunchAttributePreferredClusterDimension;
+    at[2].val.preferredClusterDim.x = 4;
+    at[2].val.preferredClusterDim.y = 1;
+    at[2].val.preferredClusterDim.z = 1;
+    cfg.numAttrs = 3;
   }
   ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, md, md2, static_cast<const __nv_bfloat16*>(bias),
-                             static_cast<const uint16_t*>(X), ldx, M, N, sc, part, flag),
+                             static_cast<const uint16_t*>(X), ldx, M, N, sc, part, flag, aux),
           "cudaLaunchKernelEx(zi_gemm_sk)");
   return launch_status("zi_gemm_sk");
 }
@@ -711,22 +769,22 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
 template <bool A_MN, bool B_MN, int EPI, int CL>
 static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                   const CUtensorMap& md2, const void* bias, const void* X, int ldx, int M, int N,
-                  const Sched& sc, float* part, uint32_t* flag, cudaStream_t s) {
+                  const Sched& sc, float* part, uint32_t* flag, const Aux& aux, cudaStream_t s) {
   if (sk_cfg() == 4)
-    return launch_cfg<A_MN, B_MN, EPI, 4, 2, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-  return launch_cfg<A_MN, B_MN, EPI, 6, 1, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
+    return launch_cfg<A_MN, B_MN, EPI, 4, 2, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+  return launch_cfg<A_MN, B_MN, EPI, 6, 1, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
 }
 
 template <bool A_MN, bool B_MN, int CL>
 static int dispatch(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& md,
                     const CUtensorMap& md2, const void* bias, const void* X, int ldx, int M, int N,
-                    const Sched& sc, float* part, uint32_t* flag, cudaStream_t s) {
+                    const Sched& sc, float* part, uint32_t* flag, const Aux& aux, cudaStream_t s) {
   switch (epi) {
-    case EPI_PLAIN: return launch<A_MN, B_MN, EPI_PLAIN, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-    case EPI_GELU: return launch<A_MN, B_MN, EPI_GELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-    case EPI_RESID: return launch<A_MN, B_MN, EPI_RESID, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-    case EPI_DGELU: return launch<A_MN, B_MN, EPI_DGELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-    case EPI_F32: return launch<A_MN, B_MN, EPI_F32, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
+    case EPI_PLAIN: return launch<A_MN, B_MN, EPI_PLAIN, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_GELU: return launch<A_MN, B_MN, EPI_GELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_RESID: return launch<A_MN, B_MN, EPI_RESID, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_DGELU: return launch<A_MN, B_MN, EPI_DGELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_F32: return launch<A_MN, B_MN, EPI_F32, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
   }
   set_error("zi_gemm_sk: unknown epilogue %d", epi);
   return ZI_EINVAL;
@@ -736,10 +794,10 @@ template <int CL>
 static int dispatch_major(int a_mn, int b_mn, int epi, const CUtensorMap& ma, const CUtensorMap& mb,
                           const CUtensorMap& md, const CUtensorMap& md2, const void* bias,
                           const void* X, int ldx, int M, int N, const Sched& sc, float* part,
-                          uint32_t* flag, cudaStream_t s) {
-  if (a_mn) return dispatch<true, true, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-  if (b_mn) return dispatch<false, true, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
-  return dispatch<false, false, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, s);
+                          uint32_t* flag, const Aux& aux, cudaStream_t s) {
+  if (a_mn) return dispatch<true, true, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+  if (b_mn) return dispatch<false, true, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+  return dispatch<false, false, CL>(epi, ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
 }
 
 }  // namespace gsk
@@ -750,11 +808,19 @@ extern "C" size_t zi_gemm_sk_workspace_bytes(void) {
          (size_t)zi::gsk::sm_count() * zi::gsk::SLOT_FLOATS * sizeof(float);
 }
 
-extern "C" int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major,
-                          int ldb, const void* bias, void* D, int ldd, int d_f32, const void* X,
-                          int ldx, void* D2, int ldd2, int epi, int M, int N, int K, void* ws,
-                          size_t ws_bytes, void* stream) {
+extern "C" int zi_gemm_sk_aux(const void* A, int a_mn_major, int lda, const void* B,
+                              int b_mn_major, int ldb, const void* bias, void* D, int ldd,
+                              int d_f32, const void* X, int ldx, void* D2, int ldd2, int epi,
+                              int M, int N, int K, void* ws, size_t ws_bytes, float* colsum_part,
+                              float* delta, int delta_S, int delta_H, int delta_D, void* stream) {
   using namespace zi::gsk;
+  ZI_CHECK_ARG(!(colsum_part || delta) || !d_f32, "zi_gemm_sk_aux: side outputs need bf16 output");
+  ZI_CHECK_ARG(!colsum_part || zi::aligned(colsum_part, 8), "zi_gemm_sk_aux: colsum_part 8-byte aligned");
+  ZI_CHECK_ARG(!delta || (epi == ZI_EPI_PLAIN && X && (delta_D == 64 || delta_D == 128) &&
+                          delta_S > 0 && delta_H > 0 && N == delta_H * delta_D &&
+                          M % delta_S == 0),
+               "zi_gemm_sk_aux: delta needs the plain epilogue, X = O, D in {64, 128}, "
+               "N = H * D and M = B * S");
   ZI_CHECK_ARG(A && B && D, "zi_gemm_sk: NULL operand");
   ZI_CHECK_ARG(M > 0 && N > 0 && K > 0, "zi_gemm_sk: empty shape");
   ZI_CHECK_ARG(lda % 8 == 0 && ldb % 8 == 0, "zi_gemm_sk: lda / ldb must be multiples of 8");
@@ -772,7 +838,7 @@ extern "C" int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B,
   }
   ZI_CHECK_ARG(epi != ZI_EPI_GELU || (D2 && ldd2 % 8 == 0 && ldd2 >= N && zi::aligned(D2, 16)),
                "zi_gemm_sk: GELU epilogue needs D2");
-  ZI_CHECK_ARG((epi != ZI_EPI_RESID && epi != ZI_EPI_DGELU) ||
+  ZI_CHECK_ARG((epi != ZI_EPI_RESID && epi != ZI_EPI_DGELU && !delta) ||
                (X && ldx % 8 == 0 && ldx >= N && zi::aligned(X, 16)),
                "zi_gemm_sk: epilogue needs X");
   ZI_CHECK_ARG(!ws || ws_bytes >= zi_gemm_sk_workspace_bytes(),
@@ -809,9 +875,18 @@ extern "C" int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B,
   float* part = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + FLAG_BYTES) : nullptr;
   const int e = d_f32 ? EPI_F32 : epi;
   cudaStream_t s = (cudaStream_t)stream;
+  const Aux aux = {colsum_part, delta, delta_S, delta_H, delta_D};
   if (CL == 4)
     return dispatch_major<4>(a_mn_major, b_mn_major, e, ma, mb, md, md2, bias, X, ldx, M, N, sc,
-                             part, flag, s);
+                             part, flag, aux, s);
   return dispatch_major<2>(a_mn_major, b_mn_major, e, ma, mb, md, md2, bias, X, ldx, M, N, sc,
-                           part, flag, s);
+                           part, flag, aux, s);
+}
+
+extern "C" int zi_gemm_sk(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major,
+                          int ldb, const void* bias, void* D, int ldd, int d_f32, const void* X,
+                          int ldx, void* D2, int ldd2, int epi, int M, int N, int K, void* ws,
+                          size_t ws_bytes, void* stream) {
+  return zi_gemm_sk_aux(A, a_mn_major, lda, B, b_mn_major, ldb, bias, D, ldd, d_f32, X, ldx, D2,
+                        ldd2, epi, M, N, K, ws, ws_bytes, nullptr, nullptr, 0, 0, 0, stream);
 }

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256)
 adam_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
             const float* __restrict__ g, uint16_t* __restrict__ ph, size_t n, size_t n8,
             zi_adam_consts c) {
+  zi::pdl_sync();
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = tid; i < n8; i += stride) {
@@ -92,6 +93,7 @@ rs_kernel(Contribs cb, int K, size_t off, size_t n, size_t nvec8, size_t clen, f
           float* __restrict__ out_or_g, float* __restrict__ p, float* __restrict__ m,
           float* __restrict__ v, uint16_t* __restrict__ ph, zi_adam_consts c,
           const zi_adam_consts* __restrict__ cdev) {
+  zi::pdl_sync();
   if (ADAM && cdev != nullptr) c = *cdev;  // constants advanced on the device (CUDA graphs)
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -172,10 +174,10 @@ int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t c
   cudaStream_t s = (cudaStream_t)stream;
   uint16_t* ph = static_cast<uint16_t*>(p_half);
   if (half_kind == ZI_HALF_BF16)
-    rs_kernel<ZI_HALF_BF16, ADAM><<<grid, block, 0, s>>>(cb, K, off, n, nvec8, clen, scale,
+    zi::launch_pdl(rs_kernel<ZI_HALF_BF16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8, clen, scale,
                                                           out_or_g, p, m, v, ph, cc, cdev);
   else
-    rs_kernel<ZI_HALF_FP16, ADAM><<<grid, block, 0, s>>>(cb, K, off, n, nvec8, clen, scale,
+    zi::launch_pdl(rs_kernel<ZI_HALF_FP16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8, clen, scale,
                                                           out_or_g, p, m, v, ph, cc, cdev);
   return launch_status(name);
 }
@@ -184,6 +186,7 @@ int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t c
 // host-side folding (oracle/adam.py AdamConsts.make): doubles rounded once.
 __global__ void adam_advance_kernel(double lr, double b1, double b2, double eps, int* step,
                                     zi_adam_consts* out) {
+  zi::pdl_sync();
   const int t = *step + 1;
   *step = t;
   zi_adam_consts c;
@@ -203,6 +206,7 @@ __global__ void adam_advance_kernel(double lr, double b1, double b2, double eps,
 template <typename T>
 __global__ void __launch_bounds__(256)
 rs_full_kernel(Contribs cb, int K, size_t off, size_t n, size_t clen, T scale, T* __restrict__ out) {
+  zi::pdl_sync();
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const size_t gi = off + i;
@@ -238,10 +242,10 @@ int zi_reduce_scatter(const void* const* contribs, int n_contrib, size_t shard_o
   const int grid = zi::grid_for(shard_elems, 256);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == ZI_DT_F32)
-    zi::rs_full_kernel<float><<<grid, 256, 0, s>>>(cb, n_contrib, shard_offset, shard_elems,
+    zi::launch_pdl(zi::rs_full_kernel<float>, dim3(grid), dim3(256), 0, s, cb, n_contrib, shard_offset, shard_elems,
                                                    contrib_len, (float)scale, static_cast<float*>(out));
   else
-    zi::rs_full_kernel<double><<<grid, 256, 0, s>>>(cb, n_contrib, shard_offset, shard_elems,
+    zi::launch_pdl(zi::rs_full_kernel<double>, dim3(grid), dim3(256), 0, s, cb, n_contrib, shard_offset, shard_elems,
                                                     contrib_len, scale, static_cast<double*>(out));
   return zi::launch_status("zi_reduce_scatter");
 }
@@ -261,9 +265,9 @@ int zi_adam_step(float* p, float* m, float* v, const float* g, void* p_half, siz
   cudaStream_t s = (cudaStream_t)stream;
   uint16_t* ph = static_cast<uint16_t*>(p_half);
   if (half_kind == ZI_HALF_BF16)
-    zi::adam_kernel<ZI_HALF_BF16><<<grid, block, 0, s>>>(p, m, v, g, ph, n, n8, *c);
+    zi::launch_pdl(zi::adam_kernel<ZI_HALF_BF16>, dim3(grid), dim3(block), 0, s, p, m, v, g, ph, n, n8, *c);
   else
-    zi::adam_kernel<ZI_HALF_FP16><<<grid, block, 0, s>>>(p, m, v, g, ph, n, n8, *c);
+    zi::launch_pdl(zi::adam_kernel<ZI_HALF_FP16>, dim3(grid), dim3(block), 0, s, p, m, v, g, ph, n, n8, *c);
   return zi::launch_status("zi_adam_step");
 }
 
@@ -295,7 +299,7 @@ int zi_rs_adam_dc(const void* const* contribs, int n_contrib, size_t shard_offse
 int zi_adam_advance(double lr, double beta1, double beta2, double eps, int* step_dev,
                     zi_adam_consts* consts_dev, void* stream) {
   ZI_CHECK_ARG(step_dev && consts_dev, "zi_adam_advance: NULL device pointer");
-  zi::adam_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(lr, beta1, beta2, eps, step_dev,
+  zi::launch_pdl(zi::adam_advance_kernel, dim3(1), dim3(1), 0, (cudaStream_t)stream, lr, beta1, beta2, eps, step_dev,
                                                             consts_dev);
   return zi::launch_status("zi_adam_advance");
 }

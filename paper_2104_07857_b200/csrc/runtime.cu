@@ -2,6 +2,7 @@
 // Host tier of the offload engine (reference BufferPool / IoTicket,
 // store.py:81-153): pinned cudaHostAlloc buffers + copy-engine transfers;
 // tickets are CUDA events.
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -11,6 +12,15 @@
 namespace zi {
 
 static thread_local char g_err[1024] = "";
+
+bool pdl_enabled() {   // ZI_PDL=0: plain stream serialisation (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZI_PDL");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;

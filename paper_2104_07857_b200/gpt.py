@@ -272,6 +272,12 @@ class GPTZeroEngine:
                       and fused)
         self.ws = kernels.Workspace(max(4 << 20, 2 * 148 * cfg.hd, 600 * 4 * cfg.hd),
                                     device=self.dev) if self.fused else None
+        # GEMM epilogue side outputs (fc1 bias colsum, attention delta); ZI_EPI_AUX=0
+        # runs the separate passes instead (A/B only)
+        self.epi_aux = os.environ.get("ZI_EPI_AUX", "1") != "0"
+        # fc2.dx epilogue's 32-row block column sums of du (the fc1 bias gradient)
+        self._csum = torch.empty(-(-cfg.tokens // 32) * 4 * cfg.hd if self.fused else 0,
+                                 dtype=torch.float32, device=self.dev)
         # Every linear of the block and the head runs on zi_gemm_sk (tcgen05 stream-K,
         # the neighbouring elementwise pass folded into its epilogue where the site has
         # one): "zi", the default. "cublas" (cuBLAS + a separate pass) and "auto" (time
@@ -829,19 +835,30 @@ class GPTZeroEngine:
         o = o4.detach().transpose(1, 2).reshape(B * S, c.hd)
         return o, (leaf, o4)
 
-    def _attn_bwd(self, do, saved):
+    def _attn_bwd(self, do, saved, delta=None):
+        """delta given: rowsum(do o o) was formed by the GEMM that produced do."""
         c = self.cfg
         if self.cdt == torch.bfloat16:
             qkv, o, lse = saved
             dqkv = torch.empty_like(qkv)
-            delta = torch.empty_like(lse)
-            kernels.attn_bwd(qkv, o, do, lse, delta, dqkv, c.batch, c.heads)
-            self.launches += 3
+            given = delta is not None
+            if not given:
+                delta = torch.empty_like(lse)
+            kernels.attn_bwd(qkv, None if given else o, do, lse, delta, dqkv, c.batch, c.heads)
+            self.launches += 2 if given else 3
             return dqkv
         leaf, o4 = saved
         g4 = do.view(c.batch, c.seq, c.heads, c.head_dim).transpose(1, 2)
         (dqkv,) = torch.autograd.grad(o4, leaf, g4)
         return dqkv.reshape(-1, 3 * c.hd)
+
+    def _colsum_part(self, T: int, N: int) -> torch.Tensor:
+        """fp32 [ceil(T/32), N] block column sums of a GEMM epilogue (one buffer, reused
+        in stream order)."""
+        n = -(-T // 32) * N
+        if self._csum.numel() < n:
+            raise ValueError(f"colsum buffer holds {self._csum.numel()} < {n} floats")
+        return self._csum[:n]
 
     def _ln(self, x, w, b, resid=None):
         """libzinf LayerNorm (bf16); with resid the residual add is fused: returns
@@ -951,7 +968,15 @@ class GPTZeroEngine:
         ws = self.ws
         self._mm_dw("fc2.dW", dy, a, G["fc2_w"])
         du = torch.empty_like(u)
-        if self._zi("fc2.dx", dy, P["fc2_w"], du, u):  # du = (dy W2) * gelu'(u), then db1
+        if self._zi("fc2.dx", dy, P["fc2_w"], du, u) and self.epi_aux:
+            # du = (dy W2) * gelu'(u); the epilogue also sums du's columns per 32-row
+            # block, so db1 is one small fold instead of a pass over du
+            T, H4 = du.shape
+            part = self._colsum_part(T, H4)
+            kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u, colsum=part)
+            kernels.colsum_fold(part, -(-T // 32), H4, G["fc1_b"])
+            self.launches += 1
+        elif self._zi("fc2.dx", dy, P["fc2_w"], du, u):   # A/B: separate bias pass
             kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
             kernels.bias_grad(du, G["fc1_b"], ws)
             self.launches += 1
@@ -967,8 +992,19 @@ class GPTZeroEngine:
         kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy,
                        dres_sum=G["fc2_b"])
         self._mm_dw("proj.dW", dx2, o, G["proj_w"])
-        do = self._mm_dx("proj.dx", dx2, P["proj_w"])
-        dqkv = self._attn_bwd(do, att)
+        if self._zi("proj.dx", dx2, P["proj_w"], o) and self.epi_aux:
+            # dO = dx2 Wp; the epilogue also forms the attention backward's
+            # delta = rowsum(dO o O) per head, so zi_attn_bwd skips its delta pass
+            c = self.cfg
+            do = torch.empty(dx2.shape[0], P["proj_w"].shape[1], dtype=dx2.dtype, device=dx2.device)
+            delta = torch.empty(c.batch * c.heads * c.seq, dtype=torch.float32, device=dx2.device)
+            kernels.gemm_sk(dx2, P["proj_w"].t(), do, x=o, delta=delta,
+                            delta_shape=(c.seq, c.heads, c.head_dim))
+            self.launches += 1
+            dqkv = self._attn_bwd(do, att, delta=delta)
+        else:
+            do = self._mm_dx("proj.dx", dx2, P["proj_w"])
+            dqkv = self._attn_bwd(do, att)
         self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
         kernels.bias_grad(dqkv, G["qkv_b"], ws)
         dh1 = self._mm_dx("qkv.dx", dqkv, P["qkv_w"])

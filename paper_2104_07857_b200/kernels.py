@@ -285,13 +285,18 @@ def sk_workspace(stream=None) -> torch.Tensor:
 
 
 def gemm_sk(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi: str = "plain",
-            x=None, out2=None, split: bool = True, stream=None) -> torch.Tensor:
+            x=None, out2=None, split: bool = True, stream=None, colsum=None,
+            delta=None, delta_shape=None) -> torch.Tensor:
     """zi_gemm_sk: out = epi(a b^T) on the stream-K tcgen05 GEMM (include/zinf.h).
 
     ``a`` (M, K) and ``b`` (N, K) as in :func:`gemm` (either may be an MN-major
     transposed view). ``out`` is a row-major bf16 (M, N) view with the epilogues of
     :func:`gemm_ex`, or fp32 (epi "plain", no bias). ``split=False`` runs whole
-    tiles (no workspace)."""
+    tiles (no workspace). Side outputs (zi_gemm_sk_aux): ``colsum`` an fp32
+    [ceil(M/32), N] tensor receiving the 32-row block column sums of the bf16 output
+    (:func:`colsum_fold` finishes them); ``delta`` an fp32 [B*H*S] tensor receiving
+    rowsum(out o x) per (row, head) with ``delta_shape`` = (S, H, D), x = the attention
+    output."""
     M, K = a.shape
     N = b.shape[0]
     if b.shape[1] != K or out.shape != (M, N) or out.stride(1) != 1:
@@ -306,15 +311,31 @@ def gemm_sk(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi:
     pb, bmn, ldb = _operand(b, "b")
     s = stream if stream is not None else torch.cuda.current_stream()
     ws = sk_workspace(s) if split else None
-    _lib.call("zi_gemm_sk", pa, amn, lda, pb, bmn, ldb,
+    if colsum is not None and (colsum.dtype != torch.float32 or colsum.numel() < -(-M // 32) * N
+                               or not colsum.is_contiguous()):
+        raise ValueError("gemm_sk: colsum must be contiguous fp32 with ceil(M/32)*N elements")
+    dS, dH, dD = delta_shape if delta is not None else (0, 0, 0)
+    if delta is not None and (delta.dtype != torch.float32 or delta.numel() != M // max(dS, 1) * dH * dS):
+        raise ValueError("gemm_sk: delta must be fp32 [B*H*S]")
+    _lib.call("zi_gemm_sk_aux", pa, amn, lda, pb, bmn, ldb,
               _dev(bias, "bias") if bias is not None else None, out.data_ptr(), out.stride(0),
               int(f32), x.data_ptr() if x is not None else None,
               x.stride(0) if x is not None else 0,
               out2.data_ptr() if out2 is not None else None,
               out2.stride(0) if out2 is not None else 0, EPI[epi], M, N, K,
               ws.data_ptr() if ws is not None else None,
-              ws.numel() * 4 if ws is not None else 0, s.cuda_stream)
+              ws.numel() * 4 if ws is not None else 0,
+              colsum.data_ptr() if colsum is not None else None,
+              delta.data_ptr() if delta is not None else None, dS, dH, dD, s.cuda_stream)
     return out
+
+
+def colsum_fold(part: torch.Tensor, P: int, N: int, out: torch.Tensor, stream=None) -> None:
+    """zi_colsum_fold: out[c] = sum_p part[p, c] in p order (fp32 in; bf16 or fp32 out)."""
+    if part.dtype != torch.float32 or part.numel() < P * N or out.numel() != N:
+        raise ValueError("colsum_fold: part fp32 [P, N], out [N]")
+    _lib.call("zi_colsum_fold", part.data_ptr(), P, N, out.data_ptr(),
+              int(out.dtype == torch.float32), _stream(stream))
 
 
 class Workspace:
@@ -467,6 +488,8 @@ def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torc
     atomics); delta is an fp32 [B*H*S] workspace (rowsum of dout * out)."""
     S, D = _attn_shapes(qkv, batch, heads)
     for t, nm in ((out, "out"), (dout, "dout")):
+        if t is None and nm == "out":   # delta already holds rowsum(dout o out)
+            continue
         if t.dtype != torch.bfloat16 or t.shape != (qkv.shape[0], heads * D):
             raise ValueError(f"{nm} must be bf16 [B*S, H*D]")
     if dqkv.dtype != torch.bfloat16 or dqkv.shape != qkv.shape:
@@ -474,7 +497,8 @@ def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torc
     for t, nm in ((lse, "lse"), (delta, "delta")):
         if t.dtype != torch.float32 or t.numel() != batch * heads * S:
             raise ValueError(f"{nm} must be fp32 with B*H*S elements")
-    _lib.call("zi_attn_bwd", _dev(qkv, "qkv"), _dev(out, "out"), _dev(dout, "dout"),
+    _lib.call("zi_attn_bwd", _dev(qkv, "qkv"), _dev(out, "out") if out is not None else None,
+              _dev(dout, "dout"),
               _dev(lse, "lse"), _dev(delta, "delta"), _dev(dqkv, "dqkv"), batch, heads, S, D,
               _stream(stream))
 

@@ -61,3 +61,10 @@ def test_attention_matches_fp32_reference(B, H, S, D):
     out2 = torch.empty_like(out)
     kernels.attn_fwd(qkv, out2, lse, B, H)
     assert torch.equal(out.view(torch.int16), out2.view(torch.int16))
+    # out = None: delta is taken as given (rowsum(dout o out), here the kernel's own
+    # from the first call) and the backward is the same bit for bit
+    dqkv3 = torch.empty_like(qkv)
+    kernels.attn_bwd(qkv, None, dout, lse, delta, dqkv3, B, H)
+    assert torch.equal(dqkv.view(torch.int16), dqkv3.view(torch.int16))
+    ref_delta = (out.float() * dout.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).reshape(-1)
+    torch.testing.assert_close(delta, ref_delta, rtol=1e-5, atol=1e-4)

@@ -162,3 +162,57 @@ def test_rejects_bad_arguments():
         kernels.gemm_sk(a, b, y, epi="gelu", out2=y)
     with pytest.raises(ValueError):
         kernels.gemm_sk(a, b, y, bias=torch.zeros(256, device="cuda", dtype=bf))
+
+
+@pytest.mark.parametrize("M,N,K,epi", [(8192, 8192, 2048, "dgelu"), (300, 520, 200, "dgelu"),
+                                       (1000, 2056, 1024, "plain"), (8192, 2048, 2048, "plain")])
+@pytest.mark.parametrize("split", [True, False])
+def test_colsum_side_output(M, N, K, epi, split):
+    """32-row block column sums of the stored bf16 output, folded in block order: the
+    bias gradient of the fc1 layer from the fc2 input-gradient GEMM. Checked against
+    the fp32 sum of the kernel's own bf16 output (exact up to fp32 summation order),
+    bitwise repeatable; rows past M (bias-only epilogue values) never count."""
+    a, b = operands("dx", M, N, K, 21)
+    x = torch.randn(M, N, device="cuda").to(bf)
+    bias = torch.randn(N, device="cuda").to(bf) if epi == "plain" else None
+    y = torch.empty(M, N, device="cuda", dtype=bf)
+    P = -(-M // 32)
+    part = torch.full((P * N,), float("nan"), device="cuda")
+    kernels.gemm_sk(a, b, y, bias=bias, epi=epi, x=x if epi == "dgelu" else None,
+                    colsum=part, split=split)
+    out = torch.empty(N, device="cuda")
+    kernels.colsum_fold(part, P, N, out)
+    ob = torch.empty(N, device="cuda", dtype=bf)
+    kernels.colsum_fold(part, P, N, ob)
+    torch.cuda.synchronize()
+    ref = y.double().sum(0)
+    assert torch.isfinite(out).all()
+    torch.testing.assert_close(out.double(), ref, rtol=1e-5, atol=1e-5 * M ** 0.5)
+    assert torch.equal(ob, out.to(bf))
+    blk = y[:32 * (M // 32)].float().view(M // 32, 32, N).sum(1)
+    torch.testing.assert_close(part.view(P, N)[:M // 32], blk, rtol=1e-5, atol=1e-5)
+    part2 = torch.empty_like(part)
+    kernels.gemm_sk(a, b, torch.empty_like(y), bias=bias, epi=epi,
+                    x=x if epi == "dgelu" else None, colsum=part2, split=split)
+    torch.cuda.synchronize()
+    assert torch.equal(part, part2)
+
+
+@pytest.mark.parametrize("B,S,H,D", [(8, 1024, 16, 128), (2, 256, 4, 64), (1, 128, 3, 128)])
+def test_delta_side_output(B, S, H, D):
+    """proj.dx epilogue: dO = dx2 Wp^T and delta[b, h, s] = sum over the head's D
+    columns of bf16(dO) * O — the attention backward's rowsum(dO o O)."""
+    M, N, K = B * S, H * D, H * D
+    a, b = operands("dx", M, N, K, 5)
+    o = torch.randn(M, N, device="cuda").to(bf)
+    y = torch.empty(M, N, device="cuda", dtype=bf)
+    delta = torch.full((B * H * S,), float("nan"), device="cuda")
+    kernels.gemm_sk(a, b, y, x=o, delta=delta, delta_shape=(S, H, D))
+    torch.cuda.synchronize()
+    check(y, a.float() @ b.float().t(), K, name="dO")
+    ref = (y.float() * o.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).reshape(-1)
+    torch.testing.assert_close(delta, ref, rtol=1e-5, atol=1e-4)
+    d2 = torch.empty_like(delta)
+    kernels.gemm_sk(a, b, torch.empty_like(y), x=o, delta=d2, delta_shape=(S, H, D))
+    torch.cuda.synchronize()
+    assert torch.equal(delta, d2)
