@@ -767,6 +767,7 @@ def offload_leg(cfg, args) -> dict:
     out["config3_equiv"] = _safe(offload_equiv_leg, args)
     out["config5_equiv"] = _safe(offload_equiv_leg, args, batch=32, params_host=True)
     if not args.no_nvme:
+        out["nvme_params"] = _safe(nvme_params_leg, cfg, args, bs, steps)
         out["nvme_optimizer"] = _safe(nvme_leg, cfg, args, bs, steps)
         out["nvme_optimizer_direct"] = _safe(nvme_leg, cfg, args, bs, 1, direct=True)
     return out
@@ -1008,6 +1009,83 @@ def disk_peak(root: str, nbytes: int = 2 << 30) -> dict:
         if _os.path.exists(path):
             _os.unlink(path)
     return res
+
+
+def nvme_params_leg(cfg, args, bs, steps) -> dict:
+    """ZeRO-Infinity's defining placement (PAPER §6.2): the 1.3B step with the bf16
+    parameter shards as reference-format .shard files in the NVMe tier and the fp32
+    optimizer states in pinned host DRAM. Every fetch position runs the plan's three
+    stages: nc (NVMe -> pinned, store workers) issued 3 positions
+    ahead, cg (pinned -> HBM, H2D stream) 2 ahead, gg (gather) 1 ahead; updated bf16
+    params are written back to their files. Hidden fraction by SURVEY §8(d):
+    1 - (t_nvme - t_hbm) / t_transfer, t_transfer = the step's host-link bytes at the
+    measured duplex peak (the nc reads come from files the page cache holds on this
+    box, so PCIe, not the disk, carries the transfer)."""
+    import shutil
+    import tempfile
+    import torch
+    from paper_2104_07857_b200 import gpt as eg
+    from paper_2104_07857_b200.comm import LocalComm
+    from paper_2104_07857_b200.store import TierKind
+    peak = host_link_peak()
+    res = {}
+    root = tempfile.mkdtemp(prefix="zinf_nvme_params_", dir=args.nvme_dir)
+    try:
+        for name, pl in (("hbm", eg.Placement(TierKind.DEVICE, TierKind.DEVICE)),
+                         ("nvme", eg.Placement(TierKind.NVME, TierKind.HOST))):
+            eng = eg.GPTZeroEngine(cfg, LocalComm(1), seed=7, lr=1e-4, placement=pl,
+                                   nvme_root=root if name == "nvme" else None)
+            for w in range(2):
+                eng.step([bs[w % 2]])
+            eng.flush()
+            torch.cuda.synchronize()
+
+            def counters():
+                return (getattr(eng, "offload_bytes", 0) + getattr(eng, "fetch_bytes", 0),
+                        getattr(eng, "nc_bytes", 0))
+            h0, n0 = counters()
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t = time.perf_counter()
+            t0.record()
+            for s in range(steps):
+                loss = eng.step([bs[s % 2]])
+            eng.flush()
+            t1.record()
+            torch.cuda.synchronize()
+            wall = (time.perf_counter() - t) * 1e3 / steps
+            h1, n1 = counters()
+            res[name] = {"ms": t0.elapsed_time(t1) / steps, "wall_ms": wall,
+                         "host_bytes": (h1 - h0) / steps, "nc_bytes": (n1 - n0) / steps,
+                         "loss": float(loss.item())}
+            if name == "nvme":
+                eng.trace = True
+                eng.step([bs[0]])
+                eng.flush()
+                tl = eng.timeline()
+                res[name]["tl_hidden"] = tl.hidden_fraction(("pcie",))
+                eng.trace = False
+            eng.close()
+            del eng
+            torch.cuda.empty_cache()
+    finally:
+        shutil.rmtree(root, ignore_errors=True)
+    nv, hb = res["nvme"], res["hbm"]
+    t_xfer = nv["host_bytes"] / (peak["duplex_gbs"] * 1e9) * 1e3
+    exposed = nv["ms"] - hb["ms"]
+    return {"workload": "GPT-1.3B ZeRO-Infinity step: bf16 params as NVMe-tier .shard files "
+                        "(nc -> cg -> gg at plan depths 3 / 2 / 1), fp32 optimizer state in "
+                        "pinned host DRAM",
+            "ms_per_step_hbm": round(hb["ms"], 2), "ms_per_step_nvme": round(nv["ms"], 2),
+            "wall_ms_per_step_nvme": round(nv["wall_ms"], 2),
+            "tflops_nvme": round(eg.model_flops_per_step(cfg) / (nv["ms"] / 1e3) / 1e12, 1),
+            "nc_bytes_per_step": int(nv["nc_bytes"]),
+            "host_bytes_per_step": int(nv["host_bytes"]),
+            "transfer_ms_at_duplex_peak": round(t_xfer, 2),
+            "exposed_ms": round(exposed, 2),
+            "hidden_fraction": round(max(0.0, 1.0 - exposed / t_xfer), 4) if t_xfer > 0 else None,
+            "timeline_pcie_hidden_behind_compute": round(nv["tl_hidden"], 4),
+            "loss_hbm": hb["loss"], "loss_nvme": nv["loss"],
+            "losses_bitwise_equal": hb["loss"] == nv["loss"]}
 
 
 def nvme_leg(cfg, args, bs, steps, direct: bool = False) -> dict:
