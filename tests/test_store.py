@@ -163,14 +163,37 @@ def test_errors_and_visibility(tmp_path):
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not mounted")
 def test_differential_random_ops(tmp_path):
     """AC-11: 10^4 random write/read/range/move/delete ops, ours vs the reference."""
+    _differential(tmp_path, ["host", "nvme"], sync_io=True, seed=2024)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not installed")
+@pytest.mark.parametrize("sync_io", [True, False])
+def test_differential_random_ops_gpu_path(tmp_path, sync_io):
+    """AC-11 on the B200 code path: the DEVICE tier is HBM tensors on the store's CUDA
+    stream, HOST is pinned cudaHostAlloc memory with CUDA-event tickets and _settle, NVMe
+    goes through the native pinned pool; with sync_io=False the store's worker threads
+    and tickets are in play. Same 10^4-op differential against the unmodified reference
+    (baseline/_ref), results and per-tier stats equal."""
+    assert torch.cuda.is_available()
+    _differential(tmp_path, ["device", "host", "nvme"], sync_io=sync_io, seed=2025)
+
+
+def _host_bytes(v) -> bytes:
+    """Bytes of a read result: numpy (reference), or a torch tensor on any device (ours)."""
+    if isinstance(v, torch.Tensor):
+        v = v.cpu().numpy()
+    return np.asarray(v).tobytes()
+
+
+def _differential(tmp_path, tiers, sync_io: bool, seed: int):
     sys.path.insert(0, REF_SRC)
     import infinisim.store as R
-    rng = np.random.default_rng(2024)
+    rng = np.random.default_rng(seed)
     ours = S.TierStore(1 << 16, 1 << 15, nvme_root=str(tmp_path / "o"),
-                       pool=S.BufferPool(256, 4), sync_io=True)
+                       pool=S.BufferPool(256, 4), sync_io=sync_io)
     ref = R.TierStore(1 << 16, 1 << 15, nvme_root=str(tmp_path / "r"),
-                      pool=R.BufferPool(256, 4), sync_io=True)
-    tiers = ["host", "nvme"]
+                      pool=R.BufferPool(256, 4), sync_io=sync_io)
     keys = [f"k{i}" for i in range(24)]
     dts = ["<f2", "<f4", "<f8"]
 
@@ -184,11 +207,11 @@ def test_differential_random_ops(tmp_path):
             if op == "read":
                 k, t = args
                 v = store.read(k, T(t)).wait()
-                return ("val", np.asarray(v.numpy() if hasattr(v, "numpy") else v).tobytes())
+                return ("val", _host_bytes(v))
             if op == "range":
                 k, t, s, n = args
                 v = store.read_range(k, T(t), s, n).wait()
-                return ("val", np.asarray(v.numpy() if hasattr(v, "numpy") else v).tobytes())
+                return ("val", _host_bytes(v))
             if op == "wrange":
                 k, t, s, a = args
                 store.flush([store.write_range(k, T(t), s, a)])
@@ -224,7 +247,7 @@ def test_differential_random_ops(tmp_path):
         assert o1 == o2, (i, op, args[:2], o1[:2], o2[:2])
         if i % 500 == 0:
             s1, s2 = ours.stats(), ref.stats()
-            for t_ in ("host", "nvme"):
+            for t_ in tiers:
                 a_, b_ = s1.tiers[S.TierKind(t_)], s2.tiers[R.TierKind(t_)]
                 assert (a_.used, a_.peak_used, a_.bytes_read, a_.bytes_written) == \
                        (b_.used, b_.peak_used, b_.bytes_read, b_.bytes_written)
