@@ -43,10 +43,14 @@ def launches(path: str, top: int = 25) -> str:
            "", "| share | time (us) | launches | kernel |", "|---:|---:|---:|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1])[:top]:
         out.append(f"| {v / T * 100:.2f}% | {v:.0f} | {cnt[k]} | `{k}` |")
-    mine = sum(v for k, v in tot.items() if "zi::" in k or "fused::" in k or "gemm" in k or
+    mine = sum(v for k, v in tot.items()
+               if any(t in k for t in ("zi::", "fused::", "gemm", "gsk::", "attn::", "emb::")) or
                k.startswith(("rs_kernel", "adam_kernel", "gather_", "linear_fwd")))
+    lib = sum(v for k, v in tot.items() if "nvjet" in k or "cudnn" in k or "cutlass" in k)
+    other = T - mine - lib
     out.append("")
-    out.append(f"libzinf kernels: {mine / T * 100:.2f}% of device time")
+    out.append(f"libzinf kernels: {mine / T * 100:.2f}% of device time; cuBLAS / cuDNN: "
+               f"{lib / T * 100:.2f}%; other (torch elementwise glue): {other / T * 100:.2f}%")
     return "\n".join(out)
 
 
