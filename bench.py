@@ -775,6 +775,7 @@ def offload_leg(cfg, args) -> dict:
 
 def _safe(fn, *a, **kw) -> dict:
     """Run one bench sub-leg; a failure is reported in its slot, never loses the line."""
+    import gc
     import torch
     try:
         return fn(*a, **kw)
@@ -784,6 +785,8 @@ def _safe(fn, *a, **kw) -> dict:
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         return {"error": repr(e)[:300]}
+    finally:
+        gc.collect()     # free the leg's engines (and their pinned arenas) now
 
 
 def offload_equiv_leg(args, batch: int = 64, params_host: bool = False) -> dict:
@@ -970,7 +973,13 @@ def config3_real_leg(args) -> dict:
 def _leg_subprocess(name: str, args, timeout: int = 1200) -> dict:
     """Run one heavy leg in a fresh process (its pinned memory is the host's, and a
     failure cannot take the main line with it); the child prints one JSON object."""
+    import gc
     import subprocess
+    import torch
+    gc.collect()                 # engines of earlier legs hold pinned arenas through cycles
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    torch._C._host_emptyCache()  # and torch's pinned host cache (host_link_peak buffers)
     cmd = [sys.executable, os.path.abspath(__file__), "--leg", name,
            "--steps", str(args.steps), "--warmup", str(args.warmup)]
     try:

@@ -219,35 +219,41 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     mbar_wait(q_full, 0);
     unsigned long long* ms = (tr && blockIdx.x == 0 && lane == 0)
                                  ? trace + gridDim.x * 6 + 2 * 64 * 6 : nullptr;
-    for (int u = 0; u <= nsub; ++u) {
-      if (tr && lane == 0 && u == 1) tr[2] = gtimer();
-      if (ms) ms[u * 4 + 0] = clock64();
-      if (u < nsub) {                              // scores of sub-tile u
-        const int st = u % NST, g = u & 1;
-        mbar_wait(&kv_full[st], (u / NST) & 1);
-        if (ms) ms[u * 4 + 1] = clock64();
-        if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
-        if (ms) ms[u * 4 + 2] = clock64();
-        fence_after_sync();
-        if (elect_one()) {
-          mma_tile<64, false, D / 16>(tmem + g * 64, sQ, sKV + st * 2 * HB, id_s, false);
-          umma_commit(&s_full[g]);
-        }
-        __syncwarp();
+    // Order: S_0, S_1, then per v: S_{v+2}, PV_v. S_{v+2} goes into group g's score slot as
+    // soon as the group has loaded S_v (s_free), before its P_v exists, so the group finds
+    // its next scores ready when it publishes P_v (issuing S_{v+2} after PV_v instead left
+    // each group idle for a PV + S MMA latency per sub-tile: half the elementwise warps
+    // waited at any time). Stages in flight: v, v+1, v+2 <= NST.
+    auto issue_s = [&](int u) {                    // scores of sub-tile u
+      const int st = u % NST, g = u & 1;
+      mbar_wait(&kv_full[st], (u / NST) & 1);
+      if (ms) ms[u * 4 + 1] = clock64();
+      if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
+      if (ms) ms[u * 4 + 2] = clock64();
+      fence_after_sync();
+      if (elect_one()) {
+        mma_tile<64, false, D / 16>(tmem + g * 64, sQ, sKV + st * 2 * HB, id_s, false);
+        umma_commit(&s_full[g]);
       }
-      if (u >= 1) {                                // O_g += P V of sub-tile u-1
-        const int v = u - 1, st = v % NST, g = v & 1;
-        mbar_wait(&p_full[g], (v >> 1) & 1);
-        if (ms) ms[u * 4 + 3] = clock64();
-        fence_after_sync();
-        if (elect_one()) {
-          mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sKV + st * 2 * HB + HB,
-                                id_o, v >= 2);
-          umma_commit(&kv_empty[st]);
-          umma_commit(&pv_done[g]);
-        }
-        __syncwarp();
+      __syncwarp();
+    };
+    issue_s(0);
+    if (nsub > 1) issue_s(1);
+    for (int v = 0; v < nsub; ++v) {
+      if (tr && lane == 0 && v == 1) tr[2] = gtimer();
+      if (ms) ms[v * 4 + 0] = clock64();
+      if (v + 2 < nsub) issue_s(v + 2);
+      const int st = v % NST, g = v & 1;           // O_g += P V of sub-tile v
+      mbar_wait(&p_full[g], (v >> 1) & 1);
+      if (ms) ms[v * 4 + 3] = clock64();
+      fence_after_sync();
+      if (elect_one()) {
+        mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sKV + st * 2 * HB + HB,
+                              id_o, v >= 2);
+        umma_commit(&kv_empty[st]);
+        umma_commit(&pv_done[g]);
       }
+      __syncwarp();
     }
     if (tr && lane == 0) tr[3] = gtimer();
   } else {
@@ -445,33 +451,36 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
     constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     mbar_wait(kv_full, 0);
-    for (int u = 0; u <= nsub; ++u) {
-      if (u < nsub) {
-        const int st = u % NST, g = u & 1;
-        mbar_wait(&qd_full[st], (u / NST) & 1);
-        if (u >= 2) mbar_wait(&st_free[g], ((u - 2) >> 1) & 1);
-        fence_after_sync();
-        if (elect_one()) {
-          const uint8_t* q = sQD + st * 2 * HB;
-          mma_tile<64, false, D / 16>(tmem + g * 128, sK, q, id_s, false);
-          mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sV, q + HB, id_s, false);
-          umma_commit(&st_full[g]);
-        }
-        __syncwarp();
+    // S^T / dP^T of sub-tile v+2 are issued as soon as group g has loaded v's (st_free),
+    // before dV / dK of v (see the forward); stages v .. v+2 in flight (NST = 3).
+    auto issue_s = [&](int u) {
+      const int st = u % NST, g = u & 1;
+      mbar_wait(&qd_full[st], (u / NST) & 1);
+      if (u >= 2) mbar_wait(&st_free[g], ((u - 2) >> 1) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        const uint8_t* q = sQD + st * 2 * HB;
+        mma_tile<64, false, D / 16>(tmem + g * 128, sK, q, id_s, false);
+        mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sV, q + HB, id_s, false);
+        umma_commit(&st_full[g]);
       }
-      if (u >= 1) {
-        const int v = u - 1, st = v % NST, g = v & 1;
-        mbar_wait(&ps_full[g], (v >> 1) & 1);
-        fence_after_sync();
-        if (elect_one()) {
-          const uint8_t* q = sQD + st * 2 * HB;
-          mma_tile<64, true, 4>(tmem + 256, sPT + g * 16384, q + HB, id_d, v > 0);
-          mma_tile<64, true, 4>(tmem + 384, sdST + g * 16384, q, id_d, v > 0);
-          umma_commit(&qd_empty[st]);
-          umma_commit(&ps_empty[g]);
-        }
-        __syncwarp();
+      __syncwarp();
+    };
+    issue_s(0);
+    if (nsub > 1) issue_s(1);
+    for (int v = 0; v < nsub; ++v) {
+      if (v + 2 < nsub) issue_s(v + 2);
+      const int st = v % NST, g = v & 1;
+      mbar_wait(&ps_full[g], (v >> 1) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        const uint8_t* q = sQD + st * 2 * HB;
+        mma_tile<64, true, 4>(tmem + 256, sPT + g * 16384, q + HB, id_d, v > 0);
+        mma_tile<64, true, 4>(tmem + 384, sdST + g * 16384, q, id_d, v > 0);
+        umma_commit(&qd_empty[st]);
+        umma_commit(&ps_empty[g]);
       }
+      __syncwarp();
     }
     if (elect_one()) umma_commit(acc_done);
     __syncwarp();
@@ -613,31 +622,33 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
     constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     mbar_wait(qd_full, 0);
-    for (int u = 0; u <= nsub; ++u) {
-      if (u < nsub) {
-        const int st = u % NST, g = u & 1;
-        mbar_wait(&kv_full[st], (u / NST) & 1);
-        if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
-        fence_after_sync();
-        if (elect_one()) {
-          const uint8_t* kv = sKV + st * 2 * HB;
-          mma_tile<64, false, D / 16>(tmem + g * 128, sQ, kv, id_s, false);
-          mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sdO, kv + HB, id_s, false);
-          umma_commit(&s_full[g]);
-        }
-        __syncwarp();
+    // S / dP of sub-tile v+2 before dQ of v (see the forward); stages v .. v+2 (NST = 4)
+    auto issue_s = [&](int u) {
+      const int st = u % NST, g = u & 1;
+      mbar_wait(&kv_full[st], (u / NST) & 1);
+      if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        const uint8_t* kv = sKV + st * 2 * HB;
+        mma_tile<64, false, D / 16>(tmem + g * 128, sQ, kv, id_s, false);
+        mma_tile<64, false, D / 16>(tmem + g * 128 + 64, sdO, kv + HB, id_s, false);
+        umma_commit(&s_full[g]);
       }
-      if (u >= 1) {
-        const int v = u - 1, st = v % NST, g = v & 1;
-        mbar_wait(&ds_full[g], (v >> 1) & 1);
-        fence_after_sync();
-        if (elect_one()) {
-          mma_tile<64, true, 4>(tmem + 256, sdS + g * 16384, sKV + st * 2 * HB, id_d, v > 0);
-          umma_commit(&kv_empty[st]);
-          umma_commit(&ds_empty[g]);
-        }
-        __syncwarp();
+      __syncwarp();
+    };
+    issue_s(0);
+    if (nsub > 1) issue_s(1);
+    for (int v = 0; v < nsub; ++v) {
+      if (v + 2 < nsub) issue_s(v + 2);
+      const int st = v % NST, g = v & 1;
+      mbar_wait(&ds_full[g], (v >> 1) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        mma_tile<64, true, 4>(tmem + 256, sdS + g * 16384, sKV + st * 2 * HB, id_d, v > 0);
+        umma_commit(&kv_empty[st]);
+        umma_commit(&ds_empty[g]);
       }
+      __syncwarp();
     }
     if (elect_one()) umma_commit(acc_done);
     __syncwarp();
