@@ -26,6 +26,7 @@
 //             dQ += dS K_j in TMEM.
 // No atomics: each output row is produced by one CTA that sums its terms in a fixed
 // order, so the backward is bitwise reproducible run to run and across placements.
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -37,7 +38,12 @@ namespace attn {
 
 using namespace zi::tc;
 
-constexpr int THREADS = 320;                 // warp 0 TMA, warp 1 MMA, warps 2..9 elementwise
+// warp 0 TMA; warp 1 the score MMAs (and TMEM allocation); warps 2..9 elementwise;
+// warp 10 the accumulating MMAs (PV / dV-dK / dQ). Two issuing warps, so a score MMA
+// never waits in program order behind an accumulate that waits for the other group's
+// probabilities (one issuing thread serialised the two elementwise groups).
+constexpr int THREADS = 352;
+constexpr int ACC_WARP = 10;
 constexpr int GW = 4;                        // warps per elementwise group (one per lane quadrant)
 constexpr float LOG2E = 1.4426950408889634f;
 
@@ -96,6 +102,17 @@ __device__ __forceinline__ void mma_tile(uint32_t d, const uint8_t* a, const uin
   }
 }
 
+// CTA index -> (rank t of its tile, batch-head bh). CTAs run in groups of G batch-heads
+// (G * nq CTAs, about one wave for G = 16): inside a group rank-major (t = 0 is the
+// tile with the most causal work), so a wave holds every tile of its batch-heads and
+// their K / V tiles are read from HBM once and then hit in L2. G = B*H is one group.
+__device__ __forceinline__ void tile_order(int idx, int nq, int BH, int G, int& t, int& bh) {
+  const int per = G * nq, grp = idx / per, r = idx - grp * per;
+  const int g = min(G, BH - grp * G);              // the last group may be partial
+  t = r / g;
+  bh = grp * G + r % g;
+}
+
 // one lane of a converged warp (elect.sync): the tcgen05.mma issuer
 __device__ __forceinline__ bool elect_one() {
   uint32_t p = 0;
@@ -143,11 +160,15 @@ __device__ __forceinline__ void tmem_free512(uint32_t tmem) {
 // ============================================================================ forward
 // Two independent online softmaxes: group g folds the kv columns g*64..g*64+63 of every
 // kv tile into its own (m_g, l_g, O_g); the epilogue merges the two.
+// K and V half-tiles stream through separate rings: a K stage is released as soon as
+// its score MMA completed, a V stage after its PV MMA, so K is fetched up to NSK
+// sub-tiles ahead of the scores instead of waiting behind the PV of its stage (TMA
+// latency under load is ~2 us, several sub-tiles). The epilogue's (m, l) exchange
+// reuses the group's own P tile once its last PV completed.
 template <int D>
 struct Fwd {
-  static constexpr int QB = 128 * D * 2, HB = 64 * D * 2, NST = 4;   // kv half-tile stages
-  static constexpr int Q = 0, KV = QB, P = QB + NST * 2 * HB, XCH = P + 2 * 16384,
-                       BAR = XCH + 4 * 128 * 4;
+  static constexpr int QB = 128 * D * 2, HB = 64 * D * 2, NSK = 5, NSV = 5;
+  static constexpr int Q = 0, K = QB, V = K + NSK * HB, P = V + NSV * HB, BAR = P + 2 * 16384;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -155,7 +176,7 @@ template <int D>
 __global__ void __launch_bounds__(THREADS, 1)
 fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
            float* __restrict__ lse, int B, int H, int S, int hd, float sl2,
-           unsigned long long* __restrict__ trace) {
+           unsigned long long* __restrict__ trace, int grp) {
   // trace (diagnostics, normally null): per CTA {sm, entry, operands in, last MMA issued,
   // softmax done, exit} in globaltimer ns
   unsigned long long* tr = trace ? trace + blockIdx.x * 6 : nullptr;
@@ -166,25 +187,28 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     tr[1] = gtimer();
   }
   using L = Fwd<D>;
-  constexpr int HB = L::HB, NST = L::NST;
+  constexpr int HB = L::HB, NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sQ = sm + L::Q, *sKV = sm + L::KV, *sP = sm + L::P;
+  uint8_t *sQ = sm + L::Q, *sK = sm + L::K, *sV = sm + L::V, *sP = sm + L::P;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
-  uint64_t *q_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + NST,
-           *s_full = bar + 1 + 2 * NST, *s_free = s_full + 2, *p_full = s_full + 4,
-           *pv_done = s_full + 6;
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = k_full + NSK, *v_full = k_empty + NSK,
+           *v_empty = v_full + NSV, *s_full = v_empty + NSV, *s_free = s_full + 2,
+           *p_full = s_full + 4, *pv_done = s_full + 6;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 8);
 
   const int nq = S / 128, BH = B * H;
-  const int i = nq - 1 - (int)blockIdx.x / BH;     // long causal rows first
-  const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
+  int i, bh;                                       // long causal rows first
+  tile_order((int)blockIdx.x, nq, BH, grp, i, bh);
+  i = nq - 1 - i;
+  const int b = bh / H, h = bh % H;
   const int nkv = i + 1, nsub = 2 * nkv, row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < NST; ++s) { mbar_init(&kv_full[s], 1); mbar_init(&kv_empty[s], 1); }
+    for (int s = 0; s < NSK; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < NSV; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
     for (int g = 0; g < 2; ++g) {
       mbar_init(&s_full[g], 1); mbar_init(&s_free[g], GW);
       mbar_init(&p_full[g], GW); mbar_init(&pv_done[g], 1);
@@ -203,54 +227,62 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     if (lane == 0) {
       mbar_expect_tx(q_full, L::QB);
       load_rows<D, 128>(sQ, &tm, q_full, h * D, row0 + i * 128);
-      for (int u = 0; u < nsub; ++u) {
-        const int st = u % NST;
-        mbar_wait(&kv_empty[st], ((u / NST) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * HB);
-        const int r = row0 + u * 64;               // kv rows of sub-tile u
-        load_rows<D, 64>(sKV + st * 2 * HB, &tm, &kv_full[st], hd + h * D, r);
-        load_rows<D, 64>(sKV + st * 2 * HB + HB, &tm, &kv_full[st], 2 * hd + h * D, r);
+      // K runs up to 2 sub-tiles ahead of V in issue order (the scores lead the PVs)
+      int uk = 0, uv = 0;
+      while (uv < nsub) {
+        if (uk < nsub && uk < uv + 3) {
+          const int st = uk % NSK;
+          mbar_wait(&k_empty[st], ((uk / NSK) & 1) ^ 1);
+          mbar_expect_tx(&k_full[st], HB);
+          load_rows<D, 64>(sK + st * HB, &tm, &k_full[st], hd + h * D, row0 + uk * 64);
+          ++uk;
+        } else {
+          const int st = uv % NSV;
+          mbar_wait(&v_empty[st], ((uv / NSV) & 1) ^ 1);
+          mbar_expect_tx(&v_full[st], HB);
+          load_rows<D, 64>(sV + st * HB, &tm, &v_full[st], 2 * hd + h * D, row0 + uv * 64);
+          ++uv;
+        }
       }
     }
   } else if (warp == 1) {
-    // the whole warp waits; one elected lane issues each group of MMAs and commits
+    // scores: the whole warp waits; one elected lane issues each group of MMAs and commits.
+    // S_u goes into group g's slot as soon as the group has loaded S_{u-2} (s_free).
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
-    constexpr uint32_t id_o = idesc_bf16_f32(128, D, false, true);
     mbar_wait(q_full, 0);
     unsigned long long* ms = (tr && blockIdx.x == 0 && lane == 0)
                                  ? trace + gridDim.x * 6 + 2 * 64 * 6 : nullptr;
-    // Order: S_0, S_1, then per v: S_{v+2}, PV_v. S_{v+2} goes into group g's score slot as
-    // soon as the group has loaded S_v (s_free), before its P_v exists, so the group finds
-    // its next scores ready when it publishes P_v (issuing S_{v+2} after PV_v instead left
-    // each group idle for a PV + S MMA latency per sub-tile: half the elementwise warps
-    // waited at any time). Stages in flight: v, v+1, v+2 <= NST.
-    auto issue_s = [&](int u) {                    // scores of sub-tile u
-      const int st = u % NST, g = u & 1;
-      mbar_wait(&kv_full[st], (u / NST) & 1);
+    for (int u = 0; u < nsub; ++u) {
+      if (tr && lane == 0 && u == 1) tr[2] = gtimer();
+      if (ms) ms[u * 4 + 0] = clock64();
+      const int st = u % NSK, g = u & 1;
+      mbar_wait(&k_full[st], (u / NSK) & 1);
       if (ms) ms[u * 4 + 1] = clock64();
       if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
       if (ms) ms[u * 4 + 2] = clock64();
       fence_after_sync();
       if (elect_one()) {
-        mma_tile<64, false, D / 16>(tmem + g * 64, sQ, sKV + st * 2 * HB, id_s, false);
+        mma_tile<64, false, D / 16>(tmem + g * 64, sQ, sK + st * HB, id_s, false);
         umma_commit(&s_full[g]);
+        umma_commit(&k_empty[st]);
       }
       __syncwarp();
-    };
-    issue_s(0);
-    if (nsub > 1) issue_s(1);
+    }
+  } else if (warp == ACC_WARP) {
+    // O_g += P V of sub-tile v once group g published P_v; frees the kv stage (its S
+    // MMA completed before the group could load S_v)
+    constexpr uint32_t id_o = idesc_bf16_f32(128, D, false, true);
+    unsigned long long* ms = (tr && blockIdx.x == 0 && lane == 0)
+                                 ? trace + gridDim.x * 6 + 2 * 64 * 6 : nullptr;
     for (int v = 0; v < nsub; ++v) {
-      if (tr && lane == 0 && v == 1) tr[2] = gtimer();
-      if (ms) ms[v * 4 + 0] = clock64();
-      if (v + 2 < nsub) issue_s(v + 2);
-      const int st = v % NST, g = v & 1;           // O_g += P V of sub-tile v
+      const int st = v % NSV, g = v & 1;
+      mbar_wait(&v_full[st], (v / NSV) & 1);
       mbar_wait(&p_full[g], (v >> 1) & 1);
       if (ms) ms[v * 4 + 3] = clock64();
       fence_after_sync();
       if (elect_one()) {
-        mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sKV + st * 2 * HB + HB,
-                              id_o, v >= 2);
-        umma_commit(&kv_empty[st]);
+        mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sV + st * HB, id_o, v >= 2);
+        umma_commit(&v_empty[st]);
         umma_commit(&pv_done[g]);
       }
       __syncwarp();
@@ -339,12 +371,15 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
       if (fs) fs[jj * 6 + 5] = clock64();
     }
     // merge the two streams: O = (O_0 2^(m_0-M) + O_1 2^(m_1-M)) / (l_0 2^(m_0-M) + l_1 2^(m_1-M))
-    float* xch = reinterpret_cast<float*>(sm + L::XCH);
-    xch[g * 256 + r] = m;
-    xch[g * 256 + 128 + r] = l;
+    // (m, l) exchange in the group's own P tile, free once its last PV completed
     mbar_wait(&pv_done[g], (nkv - 1) & 1);
+    float* xg = reinterpret_cast<float*>(sP + g * 16384);
+    xg[r] = m;
+    xg[128 + r] = l;
     named_sync(1 + q4, 2 * 32);
-    const float m0 = xch[r], l0 = xch[128 + r], m1 = xch[256 + r], l1 = xch[384 + r];
+    const float* x0 = reinterpret_cast<const float*>(sP);
+    const float* x1 = reinterpret_cast<const float*>(sP + 16384);
+    const float m0 = x0[r], l0 = x0[128 + r], m1 = x1[r], l1 = x1[128 + r];
     const float M = fmaxf(m0, m1);
     const float a0 = ex2(m0 - M), a1 = (m1 == -INFINITY) ? 0.f : ex2(m1 - M);
     const float Lt = l0 * a0 + l1 * a1, inv = 1.f / Lt;
@@ -396,7 +431,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_do,
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
-                float scale) {
+                float scale, int grp) {
   using L = Bkv<D>;
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -410,8 +445,9 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   uint32_t* tslot = reinterpret_cast<uint32_t*>(st_full + 9);
 
   const int nq = S / 128, BH = B * H;
-  const int j = (int)blockIdx.x / BH;            // kv tile; small j = many q tiles, first
-  const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
+  int j, bh;                                     // kv tile; small j = many q tiles, first
+  tile_order((int)blockIdx.x, nq, BH, grp, j, bh);
+  const int b = bh / H, h = bh % H;
   const int nsub = 2 * (nq - j), row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -449,11 +485,9 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     }
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
-    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     mbar_wait(kv_full, 0);
-    // S^T / dP^T of sub-tile v+2 are issued as soon as group g has loaded v's (st_free),
-    // before dV / dK of v (see the forward); stages v .. v+2 in flight (NST = 3).
-    auto issue_s = [&](int u) {
+    // S^T / dP^T of sub-tile u as soon as group g has loaded u-2's (st_free)
+    for (int u = 0; u < nsub; ++u) {
       const int st = u % NST, g = u & 1;
       mbar_wait(&qd_full[st], (u / NST) & 1);
       if (u >= 2) mbar_wait(&st_free[g], ((u - 2) >> 1) & 1);
@@ -465,11 +499,11 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
         umma_commit(&st_full[g]);
       }
       __syncwarp();
-    };
-    issue_s(0);
-    if (nsub > 1) issue_s(1);
+    }
+  } else if (warp == ACC_WARP) {
+    // dV += P^T dO, dK += dS^T Q of sub-tile v once group g published them
+    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     for (int v = 0; v < nsub; ++v) {
-      if (v + 2 < nsub) issue_s(v + 2);
       const int st = v % NST, g = v & 1;
       mbar_wait(&ps_full[g], (v >> 1) & 1);
       fence_after_sync();
@@ -568,7 +602,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_do,
               const float* __restrict__ lse, const float* __restrict__ delta,
               __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
-              float scale) {
+              float scale, int grp) {
   using L = Bq<D>;
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -581,8 +615,10 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
   uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 9);
 
   const int nq = S / 128, BH = B * H;
-  const int i = nq - 1 - (int)blockIdx.x / BH;
-  const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
+  int i, bh;
+  tile_order((int)blockIdx.x, nq, BH, grp, i, bh);
+  i = nq - 1 - i;
+  const int b = bh / H, h = bh % H;
   const int nsub = 2 * (i + 1), row0 = b * S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -620,10 +656,9 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
     }
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
-    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     mbar_wait(qd_full, 0);
-    // S / dP of sub-tile v+2 before dQ of v (see the forward); stages v .. v+2 (NST = 4)
-    auto issue_s = [&](int u) {
+    // S / dP of sub-tile u as soon as group g has loaded u-2's (s_free)
+    for (int u = 0; u < nsub; ++u) {
       const int st = u % NST, g = u & 1;
       mbar_wait(&kv_full[st], (u / NST) & 1);
       if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
@@ -635,11 +670,11 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
         umma_commit(&s_full[g]);
       }
       __syncwarp();
-    };
-    issue_s(0);
-    if (nsub > 1) issue_s(1);
+    }
+  } else if (warp == ACC_WARP) {
+    // dQ += dS K of sub-tile v once group g published dS_v
+    constexpr uint32_t id_d = idesc_bf16_f32(128, D, false, true);
     for (int v = 0; v < nsub; ++v) {
-      if (v + 2 < nsub) issue_s(v + 2);
       const int st = v % NST, g = v & 1;
       mbar_wait(&ds_full[g], (v >> 1) & 1);
       fence_after_sync();
@@ -788,6 +823,18 @@ static int check(const void* qkv, int B, int H, int S, int D, const char* who) {
   return ZI_OK;
 }
 
+// batch-heads per CTA group (tile_order); default one group (rank-major over all
+// batch-heads: measured 1-8 % faster than groups of 1-32, the K / V re-reads are not the
+// bound); ZI_ATTN_GROUP=G for A/B
+static int attn_group(int BH) {
+  static int g = -1;
+  if (g < 0) {
+    const char* e = getenv("ZI_ATTN_GROUP");
+    g = e ? atoi(e) : 0;
+  }
+  return (g <= 0 || g > BH) ? BH : g;
+}
+
 template <int D>
 static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cudaStream_t st) {
   const int hd = H * D;
@@ -799,7 +846,8 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
   if ((rc = set_smem(fwd_kernel<D>, Fwd<D>::BYTES, attr)) != ZI_OK) return rc;
   const float sl2 = LOG2E / sqrtf((float)D);
   zi::launch_pdl(fwd_kernel<D>, dim3(B * H * (S / 128)), dim3(THREADS), Fwd<D>::BYTES, st,
-                 tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace);
+                 tm, static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace,
+                 attn_group(B * H));
   return launch_status("zi_attn_fwd");
 }
 
@@ -824,10 +872,10 @@ static int bwd(const void* qkv, const void* out, const void* dout, const float* 
   const int grid = B * H * (S / 128);
   auto* dq = static_cast<__nv_bfloat16*>(dqkv);
   zi::launch_pdl(bwd_dkdv_kernel<D>, dim3(grid), dim3(THREADS), Bkv<D>::BYTES, st, tm, tdo, lse,
-                 delta, dq, B, H, S, hd, sl2, scale);
+                 delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H));
   if ((rc = launch_status("zi_attn_bwd(dkdv)")) != ZI_OK) return rc;
   zi::launch_pdl(bwd_dq_kernel<D>, dim3(grid), dim3(THREADS), Bq<D>::BYTES, st, tm, tdo, lse,
-                 delta, dq, B, H, S, hd, sl2, scale);
+                 delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H));
   return launch_status("zi_attn_bwd(dq)");
 }
 
