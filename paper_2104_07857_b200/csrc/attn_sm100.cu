@@ -113,6 +113,18 @@ __device__ __forceinline__ void tile_order(int idx, int nq, int BH, int G, int& 
   bh = grp * G + r % g;
 }
 
+// D[128 x N] (+)= A B over KS 16-deep steps with A (128 x 16*KS bf16) in TMEM at column
+// a_tmem (8 columns per step) and B a BROWS-row MN-major tile in shared memory.
+template <int BROWS, int KS>
+__device__ __forceinline__ void mma_tile_ts(uint32_t d, uint32_t a_tmem, const uint8_t* b,
+                                            uint32_t idesc, bool accumulate) {
+  const uint64_t db = mndesc<BROWS>(b, 0);
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk)
+    umma_bf16_ts(d, a_tmem + kk * 8, db + (uint64_t)(kk * (2048 >> 4)), idesc,
+                 (accumulate || kk > 0) ? 1u : 0u);
+}
+
 // one lane of a converged warp (elect.sync): the tcgen05.mma issuer
 __device__ __forceinline__ bool elect_one() {
   uint32_t p = 0;
@@ -221,7 +233,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
   __syncthreads();
   fence_after_sync();
   zi::pdl_sync();   // setup above overlapped the previous kernel's tail
-  const uint32_t tmem = *tslot;        // S slot g at g*64; O_g at 256 + g*128
+  const uint32_t tmem = *tslot;        // S slot g at g*64; P_g (bf16) at 128 + g*32; O_g at 256 + g*128
 
   if (warp == 0) {
     if (lane == 0) {
@@ -281,7 +293,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
       if (ms) ms[v * 4 + 3] = clock64();
       fence_after_sync();
       if (elect_one()) {
-        mma_tile<64, true, 4>(tmem + 256 + g * 128, sP + g * 16384, sV + st * HB, id_o, v >= 2);
+        mma_tile_ts<64, 4>(tmem + 256 + g * 128, tmem + 128 + g * 32, sV + st * HB, id_o, v >= 2);
         umma_commit(&v_empty[st]);
         umma_commit(&pv_done[g]);
       }
@@ -292,7 +304,7 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tmem + g * 64 + lo, tO = tmem + 256 + g * 128 + lo;
-    uint8_t* sPg = sP + g * 16384;
+    const uint32_t tP = tmem + 128 + g * 32 + lo;    // this thread's row of P_g
     float m = -INFINITY, l = 0.f;
     unsigned long long* fs = (tr && blockIdx.x == 0 && lane == 0 && (warp == 2 || warp == 6))
                                  ? trace + gridDim.x * 6 + g * 64 * 6 : nullptr;
@@ -361,10 +373,10 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
         }
       }
       if (fs) fs[jj * 6 + 4] = clock64();
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        st_piece(sPg, r, q, make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
-      fence_proxy_async_smem();
+      // P_g (bf16, two per column) into TMEM columns 128 + g*32: the PV MMA reads its A
+      // operand from there, so P never touches shared memory (the forward is bound by
+      // shared-memory bandwidth: operand reads of the N = 64 score MMAs, K / V fills)
+      tmem_st32(tP, pk);
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[g]);
@@ -414,6 +426,216 @@ fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ o
     tmem_free512(tmem);
   }
   if (tr && threadIdx.x == 0) tr[5] = gtimer();
+}
+
+// ================================================================ forward, 2 Q tiles
+// CTA = two adjacent q tiles (qa = 2t, qb = 2t + 1) of one (batch, head) sharing every
+// K / V tile; 128-column kv tiles, so the score MMAs run at N = 128 (the N = 64 shape
+// reaches only 2/3 of the tensor rate, scripts/probes/mma_probe.cu). TMEM: S_a, S_b
+// (128 columns each; P_x, bf16, overwrites the first 64 columns of S_x once read), O_a,
+// O_b. One MMA thread issues, per kv tile j: PV_a(j), S_a(j+1), PV_b(j), S_b(j+1) — so
+// while softmax group x works on S_x(j) the tensor core runs the other tile's PV and S
+// (ping-pong); a tile's S_x(j+1) follows its own PV_x(j) in issue order, which is what
+// makes the P / S aliasing and the lazy O rescale safe (tcgen05 work of one thread
+// completes in order: S_x(j) complete implies PV_x(j-1) complete).
+template <int D>
+struct Fwd2 {
+  static constexpr int TB = 128 * D * 2, NSK = 3, NSV = 2;
+  static constexpr int QA = 0, QBo = TB, K = 2 * TB, V = K + NSK * TB, BAR = V + NSV * TB;
+  static constexpr int BYTES = BAR + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+            float* __restrict__ lse, int B, int H, int S, int hd, float sl2) {
+  using L = Fwd2<D>;
+  constexpr int TB = L::TB, NSK = L::NSK, NSV = L::NSV;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = align1024(smem_raw);
+  uint8_t *sQa = sm + L::QA, *sQb = sm + L::QBo, *sK = sm + L::K, *sV = sm + L::V;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
+  uint64_t *q_full = bar, *k_full = bar + 1, *k_empty = k_full + NSK, *v_full = k_empty + NSK,
+           *v_empty = v_full + NSV, *s_full = v_empty + NSV, *p_full = s_full + 2,
+           *pv_done = s_full + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(s_full + 6);
+
+  const int nq2 = S / 256, BH = B * H;
+  const int t = nq2 - 1 - (int)blockIdx.x / BH;    // most causal work first
+  const int bh = (int)blockIdx.x % BH, b = bh / H, h = bh % H;
+  const int qa = 2 * t, nkv_a = qa + 1, nkv_b = qa + 2, row0 = b * S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NSK; ++s) { mbar_init(&k_full[s], 1); mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < NSV; ++s) { mbar_init(&v_full[s], 1); mbar_init(&v_empty[s], 1); }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1); mbar_init(&p_full[x], GW); mbar_init(&pv_done[x], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&tm);
+  }
+  if (warp == 1) tmem_alloc512(tslot);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  zi::pdl_sync();
+  const uint32_t tmem = *tslot;        // S_x / P_x at x*128; O_x at 256 + x*128
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * TB);
+      load_rows<D, 128>(sQa, &tm, q_full, h * D, row0 + qa * 128);
+      load_rows<D, 128>(sQb, &tm, q_full, h * D, row0 + (qa + 1) * 128);
+      int uk = 0, uv = 0;                          // K runs one tile ahead of V
+      while (uv < nkv_b) {
+        if (uk < nkv_b && uk <= uv + 1) {
+          const int st = uk % NSK;
+          mbar_wait(&k_empty[st], ((uk / NSK) & 1) ^ 1);
+          mbar_expect_tx(&k_full[st], TB);
+          load_rows<D, 128>(sK + st * TB, &tm, &k_full[st], hd + h * D, row0 + uk * 128);
+          ++uk;
+        } else {
+          const int st = uv % NSV;
+          mbar_wait(&v_empty[st], ((uv / NSV) & 1) ^ 1);
+          mbar_expect_tx(&v_full[st], TB);
+          load_rows<D, 128>(sV + st * TB, &tm, &v_full[st], 2 * hd + h * D, row0 + uv * 128);
+          ++uv;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16_f32(128, 128, false, false);
+    constexpr uint32_t id_o = idesc_bf16_f32(128, D, false, true);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int x, int j) {             // S_x(j) = Q_x K_j^T
+      const int st = j % NSK;
+      mbar_wait(&k_full[st], (j / NSK) & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        mma_tile<128, false, D / 16>(tmem + x * 128, x ? sQb : sQa, sK + st * TB, id_s, false);
+        umma_commit(&s_full[x]);
+        if (x == 1) umma_commit(&k_empty[st]);     // both tiles' scores of K_j issued
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int x, int j) {            // O_x += P_x(j) V_j
+      const int st = j % NSV;
+      mbar_wait(&v_full[st], (j / NSV) & 1);
+      mbar_wait(&p_full[x], j & 1);
+      fence_after_sync();
+      if (elect_one()) {
+        mma_tile_ts<128, 8>(tmem + 256 + x * 128, tmem + x * 128, sV + st * TB, id_o, j > 0);
+        umma_commit(&pv_done[x]);
+        if (x == 1) umma_commit(&v_empty[st]);
+      }
+      __syncwarp();
+    };
+    issue_s(0, 0);
+    issue_s(1, 0);
+    for (int j = 0; j < nkv_b; ++j) {
+      if (j < nkv_a) {
+        issue_pv(0, j);
+        if (j + 1 < nkv_a) issue_s(0, j + 1);
+      }
+      issue_pv(1, j);
+      if (j + 1 < nkv_b) issue_s(1, j + 1);
+    }
+  } else {
+    // softmax group x = q tile qa + x; thread = row r of the tile (TMEM lane)
+    const int x = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t lo = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + x * 128 + lo, tO = tmem + 256 + x * 128 + lo;
+    const int qi = qa + x, nkv = nkv_a + x;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[x], j & 1);
+      fence_after_sync();
+      const bool diag = j == qi;                   // key index > query index masked
+      float mx[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx[k] = -INFINITY;
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t t0[32], t1[32];
+        tmem_ld32_nowait(tS + hh * 64, t0);
+        tmem_ld32_nowait(tS + hh * 64 + 32, t1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          float a = u2f(t0[c]), bb = u2f(t1[c]);
+          if (diag && hh * 64 + c > r) a = -INFINITY;
+          if (diag && hh * 64 + 32 + c > r) bb = -INFINITY;
+          mx[c & 7] = fmaxf(mx[c & 7], fmaxf(a, bb));
+        }
+      }
+      const float mrow = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
+      float alpha = 1.f;
+      if (mrow > m + 8.f) {                        // lazy rescale (FA4); first tile: alpha 0
+        alpha = ex2(m - mrow);
+        m = mrow;
+      }
+      if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        // S_x(j) complete => PV_x(j-1) complete (same issuing thread): O_x is stable
+#pragma unroll 1
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] = __float_as_uint(u2f(o[k]) * alpha);
+          tmem_st32(tO + cc * 32, o);
+        }
+      }
+      const float nm = (m == -INFINITY) ? 0.f : -m;
+      float rs[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) rs[k] = 0.f;
+#pragma unroll 1
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t t0[32], t1[32];
+        tmem_ld32_nowait(tS + hh * 64, t0);
+        tmem_ld32_nowait(tS + hh * 64 + 32, t1);
+        tmem_wait_ld();
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int c0 = hh * 64 + 2 * c;
+          float x0 = u2f(t0[2 * c]), x1 = u2f(t0[2 * c + 1]);
+          if (diag && c0 > r) x0 = -INFINITY;
+          if (diag && c0 + 1 > r) x1 = -INFINITY;
+          const float p0 = ex2(fmaf(x0, sl2, nm)), p1 = ex2(fmaf(x1, sl2, nm));
+          rs[c & 7] += p0 + p1;
+          pk[c] = pack_bf16(p0, p1);
+          float y0 = u2f(t1[2 * c]), y1 = u2f(t1[2 * c + 1]);
+          if (diag && c0 + 32 > r) y0 = -INFINITY;
+          if (diag && c0 + 33 > r) y1 = -INFINITY;
+          const float p2 = ex2(fmaf(y0, sl2, nm)), p3 = ex2(fmaf(y1, sl2, nm));
+          rs[(c + 4) & 7] += p2 + p3;
+          pk[16 + c] = pack_bf16(p2, p3);
+        }
+        // P columns hh*32 .. hh*32+31 (kv hh*64 .. hh*64+63) over S columns already read
+        tmem_st32(tS + hh * 32, pk);
+      }
+      l = l * alpha + (((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7])));
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[x]);
+    }
+    mbar_wait(&pv_done[x], (nkv - 1) & 1);
+    fence_after_sync();
+    const float inv = 1.f / l;
+    const size_t row = (size_t)row0 + qi * 128 + r;
+    store_row<D>(tO, inv, out + row * hd + h * D);
+    lse[(size_t)bh * S + qi * 128 + r] = m + __log2f(l);
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after_sync();
+    tmem_free512(tmem);
+  }
 }
 
 // =================================================================== backward: dK, dV
@@ -835,6 +1057,16 @@ static int attn_group(int BH) {
   return (g <= 0 || g > BH) ? BH : g;
 }
 
+// ZI_ATTN_FWD2=0: the one-Q-tile forward everywhere (A/B)
+static bool use_fwd2() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZI_ATTN_FWD2");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int D>
 static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cudaStream_t st) {
   const int hd = H * D;
@@ -842,6 +1074,14 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
   if (rc != ZI_OK) return rc;
   CUtensorMap tm;
   if ((rc = make_map(&tm, qkv, B * S, 3 * hd, 3 * hd)) != ZI_OK) return rc;
+  if (S % 256 == 0 && use_fwd2() && g_trace == nullptr) {   // two q tiles per CTA
+    static bool attr2 = false;
+    if ((rc = set_smem(fwd2_kernel<D>, Fwd2<D>::BYTES, attr2)) != ZI_OK) return rc;
+    const float sl2 = LOG2E / sqrtf((float)D);
+    zi::launch_pdl(fwd2_kernel<D>, dim3(B * H * (S / 256)), dim3(320), Fwd2<D>::BYTES, st, tm,
+                   static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2);
+    return launch_status("zi_attn_fwd");
+  }
   static bool attr = false;
   if ((rc = set_smem(fwd_kernel<D>, Fwd<D>::BYTES, attr)) != ZI_OK) return rc;
   const float sl2 = LOG2E / sqrtf((float)D);

@@ -28,7 +28,7 @@ def reference(qkv, B, H, S, D):
     return o, (q, k, v), torch.logsumexp(s.masked_fill(mask, float("-inf")), -1)
 
 
-@pytest.mark.parametrize("B,H,S,D", [(1, 1, 128, 64), (2, 3, 256, 64), (2, 2, 384, 128),
+@pytest.mark.parametrize("B,H,S,D", [(1, 1, 128, 64), (2, 3, 256, 64), (2, 2, 384, 128), (2, 2, 512, 128),
                                      (1, 16, 1024, 128), (4, 4, 128, 128)])
 def test_attention_matches_fp32_reference(B, H, S, D):
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + S + D)
