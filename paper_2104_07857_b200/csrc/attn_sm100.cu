@@ -448,7 +448,20 @@ struct Fwd2 {
 template <int D>
 __global__ void __launch_bounds__(320, 1)
 fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
-            float* __restrict__ lse, int B, int H, int S, int hd, float sl2) {
+            float* __restrict__ lse, int B, int H, int S, int hd, float sl2,
+            unsigned long long* __restrict__ trace) {
+  // trace (diagnostics, normally null): per CTA {sm, entry, operands in, last MMA issued,
+  // softmax done, exit} in globaltimer ns; CTA 0: per kv tile, group x's
+  // {wait start, S ready, max done, P published} and the MMA thread's
+  // {PV_a issued, S_a issued, PV_b issued, S_b issued} in clock64
+  unsigned long long* tr = trace ? trace + blockIdx.x * 6 : nullptr;
+  if (tr && threadIdx.x == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tr[0] = smid;
+    tr[1] = gtimer();
+  }
+  unsigned long long* fine = (trace && blockIdx.x == 0) ? trace + gridDim.x * 6 : nullptr;
   using L = Fwd2<D>;
   constexpr int TB = L::TB, NSK = L::NSK, NSV = L::NSV;
   extern __shared__ uint8_t smem_raw[];
@@ -532,44 +545,51 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
       }
       __syncwarp();
     };
+    unsigned long long* mf = (fine && lane == 0) ? fine + 2 * 16 * 4 : nullptr;
     issue_s(0, 0);
     issue_s(1, 0);
+    if (tr && lane == 0) tr[2] = gtimer();
     for (int j = 0; j < nkv_b; ++j) {
       if (j < nkv_a) {
         issue_pv(0, j);
+        if (mf) mf[j * 4 + 0] = clock64();
         if (j + 1 < nkv_a) issue_s(0, j + 1);
+        if (mf) mf[j * 4 + 1] = clock64();
       }
       issue_pv(1, j);
+      if (mf) mf[j * 4 + 2] = clock64();
       if (j + 1 < nkv_b) issue_s(1, j + 1);
+      if (mf) mf[j * 4 + 3] = clock64();
     }
+    if (tr && lane == 0) tr[3] = gtimer();
   } else {
     // softmax group x = q tile qa + x; thread = row r of the tile (TMEM lane)
     const int x = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tmem + x * 128 + lo, tO = tmem + 256 + x * 128 + lo;
     const int qi = qa + x, nkv = nkv_a + x;
+    unsigned long long* gf = (fine && lane == 0 && q4 == 0) ? fine + x * 16 * 4 : nullptr;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
+      if (gf) gf[j * 4 + 0] = clock64();
       mbar_wait(&s_full[x], j & 1);
+      if (gf) gf[j * 4 + 1] = clock64();
       fence_after_sync();
       const bool diag = j == qi;                   // key index > query index masked
+      uint32_t sv[128];                            // the row's 128 scores, loaded once
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) tmem_ld32_nowait(tS + hh * 32, sv + hh * 32);
+      tmem_wait_ld();
+      if (diag) {
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > r) sv[c] = __float_as_uint(-INFINITY);
+      }
       float mx[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) mx[k] = -INFINITY;
-#pragma unroll 1
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t t0[32], t1[32];
-        tmem_ld32_nowait(tS + hh * 64, t0);
-        tmem_ld32_nowait(tS + hh * 64 + 32, t1);
-        tmem_wait_ld();
+      for (int k = 0; k < 8; ++k) mx[k] = u2f(sv[k]);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          float a = u2f(t0[c]), bb = u2f(t1[c]);
-          if (diag && hh * 64 + c > r) a = -INFINITY;
-          if (diag && hh * 64 + 32 + c > r) bb = -INFINITY;
-          mx[c & 7] = fmaxf(mx[c & 7], fmaxf(a, bb));
-        }
-      }
+      for (int c = 8; c < 128; ++c) mx[c & 7] = fmaxf(mx[c & 7], u2f(sv[c]));
       const float mrow = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * sl2;
       float alpha = 1.f;
@@ -588,41 +608,33 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
           tmem_st32(tO + cc * 32, o);
         }
       }
+      if (gf) gf[j * 4 + 2] = clock64();
       const float nm = (m == -INFINITY) ? 0.f : -m;
       float rs[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) rs[k] = 0.f;
-#pragma unroll 1
+      // (exp2 on the FMA pipe for part of the row, FA4's trick, measured slower here: the
+      // polynomial costs ~10 issue slots per element against one MUFU slot)
+#pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
-        uint32_t t0[32], t1[32];
-        tmem_ld32_nowait(tS + hh * 64, t0);
-        tmem_ld32_nowait(tS + hh * 64 + 32, t1);
-        tmem_wait_ld();
         uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int c0 = hh * 64 + 2 * c;
-          float x0 = u2f(t0[2 * c]), x1 = u2f(t0[2 * c + 1]);
-          if (diag && c0 > r) x0 = -INFINITY;
-          if (diag && c0 + 1 > r) x1 = -INFINITY;
-          const float p0 = ex2(fmaf(x0, sl2, nm)), p1 = ex2(fmaf(x1, sl2, nm));
+        for (int c = 0; c < 32; ++c) {
+          const int k0 = hh * 64 + 2 * c;
+          const float p0 = ex2(fmaf(u2f(sv[k0]), sl2, nm));
+          const float p1 = ex2(fmaf(u2f(sv[k0 + 1]), sl2, nm));
           rs[c & 7] += p0 + p1;
           pk[c] = pack_bf16(p0, p1);
-          float y0 = u2f(t1[2 * c]), y1 = u2f(t1[2 * c + 1]);
-          if (diag && c0 + 32 > r) y0 = -INFINITY;
-          if (diag && c0 + 33 > r) y1 = -INFINITY;
-          const float p2 = ex2(fmaf(y0, sl2, nm)), p3 = ex2(fmaf(y1, sl2, nm));
-          rs[(c + 4) & 7] += p2 + p3;
-          pk[16 + c] = pack_bf16(p2, p3);
         }
-        // P columns hh*32 .. hh*32+31 (kv hh*64 .. hh*64+63) over S columns already read
-        tmem_st32(tS + hh * 32, pk);
+        tmem_st32(tS + hh * 32, pk);                 // P over S columns already read
       }
       l = l * alpha + (((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7])));
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[x]);
+      if (gf) gf[j * 4 + 3] = clock64();
     }
+    if (tr && x == 1 && warp == 6 && lane == 0) tr[4] = gtimer();
     mbar_wait(&pv_done[x], (nkv - 1) & 1);
     fence_after_sync();
     const float inv = 1.f / l;
@@ -636,6 +648,7 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
     fence_after_sync();
     tmem_free512(tmem);
   }
+  if (tr && threadIdx.x == 0) tr[5] = gtimer();
 }
 
 // =================================================================== backward: dK, dV
@@ -1074,12 +1087,12 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
   if (rc != ZI_OK) return rc;
   CUtensorMap tm;
   if ((rc = make_map(&tm, qkv, B * S, 3 * hd, 3 * hd)) != ZI_OK) return rc;
-  if (S % 256 == 0 && use_fwd2() && g_trace == nullptr) {   // two q tiles per CTA
+  if (S % 256 == 0 && use_fwd2()) {   // two q tiles per CTA
     static bool attr2 = false;
     if ((rc = set_smem(fwd2_kernel<D>, Fwd2<D>::BYTES, attr2)) != ZI_OK) return rc;
     const float sl2 = LOG2E / sqrtf((float)D);
     zi::launch_pdl(fwd2_kernel<D>, dim3(B * H * (S / 256)), dim3(320), Fwd2<D>::BYTES, st, tm,
-                   static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2);
+                   static_cast<__nv_bfloat16*>(out), lse, B, H, S, hd, sl2, g_trace);
     return launch_status("zi_attn_fwd");
   }
   static bool attr = false;

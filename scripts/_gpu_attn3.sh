@@ -1,3 +1,4 @@
 make -j16 >/dev/null 2>&1 || { echo build failed; exit 1; }
 timeout 900 python -m pytest tests/test_attn_gpu.py -m gpu -q -p no:cacheprovider -x 2>&1 | tail -3
 for f in 0 1; do echo "FWD2=$f"; ZI_ATTN_FWD2=$f timeout 300 python scripts/bench_attn.py 2>&1 | tail -3 | head -2; done
+timeout 300 python scripts/bench_attn.py 8 16 1024 128 --trace2 2>&1 | head -16

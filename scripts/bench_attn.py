@@ -37,6 +37,36 @@ def main():
     dout = torch.randn_like(out)
     dqkv = torch.empty_like(qkv)
     unit = 2.0 * B * H * S * S * D / 2      # one causal matmul
+    if "--trace2" in sys.argv:              # per-CTA timeline of the two-q-tile forward
+        from paper_2104_07857_b200 import _lib
+        nct = B * H * (S // 256)
+        tr = torch.zeros(nct * 6 + 3 * 16 * 4, dtype=torch.int64, device="cuda")
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        torch.cuda.synchronize()
+        _lib.call("zi_attn_set_trace", tr.data_ptr())
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        torch.cuda.synchronize()
+        _lib.call("zi_attn_set_trace", None)
+        t = tr[:nct * 6].view(nct, 6).cpu().double()
+        fine = tr[nct * 6:].view(3, 16, 4).cpu().double()
+        t0 = t[:, 1].min()
+        t[:, 1:] = (t[:, 1:] - t0) / 1000.0
+        print("kernel span us", float(t[:, 5].max()))
+        for name, a, b in (("entry->operands", 1, 2), ("operands->last mma", 2, 3),
+                           ("last mma->softmax b done", 3, 4), ("softmax b done->exit", 4, 5),
+                           ("cta total", 1, 5)):
+            d = t[:, b] - t[:, a]
+            print(f"{name:26s} mean {float(d.mean()):6.2f} us  max {float(d.max()):6.2f}")
+        base = fine[0, 0, 0]
+        nkvb = S // 128                       # CTA 0 = the last q tile pair
+        for x in range(2):
+            print(f"group {x}: [wait start, S ready, max done, P published] kcycles")
+            for j in range(nkvb - 1 + x):
+                print("   ", j, [round(float(v - base) / 1000, 2) for v in fine[x, j]])
+        print("MMA: [PV_a, S_a(j+1), PV_b, S_b(j+1)] issued, kcycles")
+        for j in range(nkvb):
+            print("   ", j, [round(float(v - base) / 1000, 2) if v > 0 else None for v in fine[2, j]])
+        return
     if "--trace" in sys.argv:               # per-CTA timeline of the forward
         from paper_2104_07857_b200 import _lib
         nct = B * H * (S // 128)
