@@ -1,3 +1,3 @@
 make -j16 >/dev/null 2>&1 || { echo build failed; exit 1; }
 timeout 900 python -m pytest tests/test_attn_gpu.py -m gpu -q -p no:cacheprovider -x 2>&1 | tail -3
-for f in 0 1; do echo "BWD2=$f"; ZI_ATTN_BWD2=$f timeout 300 python scripts/bench_attn.py 2>&1 | tail -3 | head -2; done
+for f in 0 1; do echo "DQ2=$f"; ZI_ATTN_DQ2=$f timeout 300 python scripts/bench_attn.py 2>&1 | tail -3 | head -2; done
