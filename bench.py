@@ -460,9 +460,12 @@ def run_ours(args):
 
     # ---------------- offload leg: fp32 optimizer state in pinned host DRAM
     offload = None
+    config3_real = None
     if world == 1 and not args.no_offload:
         del eng
         torch.cuda.empty_cache()
+        if not args.no_config3:   # first, while this process holds no pinned arenas
+            config3_real = _leg_subprocess("config3_real", args)
         try:
             offload = offload_leg(cfg, args)
         except Exception as e:  # noqa: BLE001 — report, never lose the main line
@@ -475,9 +478,8 @@ def run_ours(args):
     if world == 1 and not args.no_offload:
         store = _safe(store_leg)
         tiling = _safe(tiling_leg)
-        if offload is not None and not args.no_config3:
-            torch.cuda.empty_cache()   # the 10B leg's process needs ~90 GB of this GPU
-            offload["config3_real"] = _leg_subprocess("config3_real", args)
+        if offload is not None and config3_real is not None:
+            offload["config3_real"] = config3_real
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None

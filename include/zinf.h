@@ -356,7 +356,13 @@ int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int
                 void* stream);
 int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
                 void* dqkv, int B, int H, int S, int head_dim, void* stream);
-/* (out = NULL: delta already holds rowsum(dout o out), e.g. from zi_gemm_sk_aux.) */
+/* (out = NULL: delta already holds rowsum(dout o out), e.g. from zi_gemm_sk_aux.)
+ * zi_attn_bwd_colsum also writes the column sums of dqkv (as stored, bf16) per 32-row
+ * block into colsum_part, fp32 [B*S/32][3*H*D] — the qkv bias gradient's partials
+ * (zi_colsum_fold sums them in block order). */
+int zi_attn_bwd_colsum(const void* qkv, const void* out, const void* dout, const float* lse,
+                       float* delta, void* dqkv, int B, int H, int S, int head_dim,
+                       float* colsum_part, void* stream);
 /* Tied-embedding gradient in a fixed order (csrc/embed.cu): out[v] = half_RNE(acc[v] +
  * sum of dx[t] over the tokens t with id v, in sequence order). tokens int64 [T]; dx
  * [T, hd] bf16 (dx_f32 = 0) or fp32; acc fp32 [V, hd]; out half [V, hd]; work int32

@@ -135,6 +135,8 @@ SIGNATURES = {
                        c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int,
                        c_void_p, c_size_t, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p],
     "zi_colsum_fold": [c_void_p, c_int, c_int, c_void_p, c_int, c_void_p],
+    "zi_attn_bwd_colsum": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                           c_int, c_int, c_int, c_void_p, c_void_p],
     "zi_gemm_sk_workspace_bytes": [],
 }
 _RESTYPE = {"zi_last_error": ctypes.c_char_p, "zi_gemm_sk_workspace_bytes": c_size_t}

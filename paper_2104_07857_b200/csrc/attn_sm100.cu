@@ -153,6 +153,43 @@ __device__ __forceinline__ void store_row(uint32_t taddr, float scale, __nv_bflo
   }
 }
 
+// store_row plus the column sums of the stored (bf16-rounded) values over the warp's 32
+// rows: a transpose-reduce butterfly (31 shuffles per 32 columns) leaves column c's sum in
+// lane c, written to csum[c] (the 32-row block partial of a bias gradient). Fixed order.
+template <int NC>
+__device__ __forceinline__ void store_row_csum(uint32_t taddr, float scale, __nv_bfloat16* dst,
+                                               float* csum, int lane) {
+#pragma unroll 1
+  for (int cc = 0; cc < NC / 32; ++cc) {
+    uint32_t o[32];
+    tmem_ld32(taddr + cc * 32, o);
+    float v[32];
+    uint4* d4 = reinterpret_cast<uint4*>(dst + cc * 32);
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint32_t w[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w[k] = pack_bf16(u2f(o[8 * g + 2 * k]) * scale, u2f(o[8 * g + 2 * k + 1]) * scale);
+        v[8 * g + 2 * k] = __uint_as_float(w[k] << 16);
+        v[8 * g + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+      }
+      d4[g] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int k = 0; k < off; ++k) {
+        const float send = up ? v[k] : v[k + off];
+        const float keep = up ? v[k + off] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+      }
+    }
+    csum[cc * 32 + lane] = v[0];
+  }
+}
+
 __device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                ::"r"(smem_u32(slot)), "r"(512) : "memory");
@@ -666,7 +703,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_do,
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
-                float scale, int grp) {
+                float scale, int grp, float* __restrict__ csum) {
   using L = Bkv<D>;
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -812,8 +849,14 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     fence_after_sync();
     const size_t row = (size_t)row0 + j * 128 + r;
     __nv_bfloat16* d = dqkv + row * 3 * hd;
-    if (g == 0) store_row<D>(tmem + 256 + lo, 1.f, d + 2 * hd + h * D);
-    else store_row<D>(tmem + 384 + lo, scale, d + hd + h * D);
+    if (csum == nullptr) {
+      if (g == 0) store_row<D>(tmem + 256 + lo, 1.f, d + 2 * hd + h * D);
+      else store_row<D>(tmem + 384 + lo, scale, d + hd + h * D);
+    } else {   // + the qkv bias gradient's 32-row block partials of dV / dK
+      float* cp = csum + ((size_t)row0 + j * 128 + q4 * 32) / 32 * (3 * hd);
+      if (g == 0) store_row_csum<D>(tmem + 256 + lo, 1.f, d + 2 * hd + h * D, cp + 2 * hd + h * D, lane);
+      else store_row_csum<D>(tmem + 384 + lo, scale, d + hd + h * D, cp + hd + h * D, lane);
+    }
   }
   fence_before_sync();
   __syncthreads();
@@ -837,7 +880,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_do,
               const float* __restrict__ lse, const float* __restrict__ delta,
               __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
-              float scale, int grp) {
+              float scale, int grp, float* __restrict__ csum) {
   using L = Bq<D>;
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -967,8 +1010,14 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
     mbar_wait(acc_done, 0);
     fence_after_sync();
     const size_t row = (size_t)row0 + i * 128 + r;
-    store_row<D / 2>(tmem + 256 + lo + g * (D / 2), scale,
-                     dqkv + row * 3 * hd + h * D + g * (D / 2));
+    if (csum == nullptr)
+      store_row<D / 2>(tmem + 256 + lo + g * (D / 2), scale,
+                       dqkv + row * 3 * hd + h * D + g * (D / 2));
+    else
+      store_row_csum<D / 2>(tmem + 256 + lo + g * (D / 2), scale,
+                            dqkv + row * 3 * hd + h * D + g * (D / 2),
+                            csum + ((size_t)row0 + i * 128 + q4 * 32) / 32 * (3 * hd) + h * D +
+                                g * (D / 2), lane);
   }
   fence_before_sync();
   __syncthreads();
@@ -1106,7 +1155,7 @@ static int fwd(const void* qkv, void* out, float* lse, int B, int H, int S, cuda
 
 template <int D>
 static int bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
-               void* dqkv, int B, int H, int S, cudaStream_t st) {
+               void* dqkv, int B, int H, int S, float* csum, cudaStream_t st) {
   const int hd = H * D;
   int rc = encoder();
   if (rc != ZI_OK) return rc;
@@ -1128,12 +1177,12 @@ static int bwd(const void* qkv, const void* out, const void* dout, const float* 
   // no shared-memory round trip — measured 5 % slower: with TMEM full, the next q tile's
   // scores cannot overlap the elementwise work, so MMA and softmax serialise)
   zi::launch_pdl(bwd_dkdv_kernel<D>, dim3(grid), dim3(THREADS), Bkv<D>::BYTES, st, tm, tdo,
-                 lse, delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H));
+                 lse, delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H), csum);
   if ((rc = launch_status("zi_attn_bwd(dkdv)")) != ZI_OK) return rc;
   // (likewise a 128-column dQ variant with dS in TMEM, one score slot overlapped with the
   // previous tile's elementwise work: 4 % slower than the two 64-column groups)
   zi::launch_pdl(bwd_dq_kernel<D>, dim3(grid), dim3(THREADS), Bq<D>::BYTES, st, tm, tdo, lse,
-                 delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H));
+                 delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H), csum);
   return launch_status("zi_attn_bwd(dq)");
 }
 
@@ -1160,6 +1209,12 @@ int zi_attn_fwd(const void* qkv, void* out, float* lse, int B, int H, int S, int
 
 int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, float* delta,
                 void* dqkv, int B, int H, int S, int head_dim, void* stream) {
+  return zi_attn_bwd_colsum(qkv, out, dout, lse, delta, dqkv, B, H, S, head_dim, nullptr, stream);
+}
+
+int zi_attn_bwd_colsum(const void* qkv, const void* out, const void* dout, const float* lse,
+                       float* delta, void* dqkv, int B, int H, int S, int head_dim,
+                       float* colsum_part, void* stream) {
   int rc = zi::attn::check(qkv, B, H, S, head_dim, "zi_attn_bwd");
   if (rc != ZI_OK) return rc;
   // out == NULL: delta already holds rowsum(dout o out) (the proj.dx GEMM's epilogue)
@@ -1168,8 +1223,8 @@ int zi_attn_bwd(const void* qkv, const void* out, const void* dout, const float*
                "zi_attn_bwd: 16-byte alignment");
   ZI_CHECK_ARG(H * head_dim / 8 <= 1024, "zi_attn_bwd: hidden %d too wide", H * head_dim);
   cudaStream_t s = (cudaStream_t)stream;
-  return head_dim == 64 ? zi::attn::bwd<64>(qkv, out, dout, lse, delta, dqkv, B, H, S, s)
-                        : zi::attn::bwd<128>(qkv, out, dout, lse, delta, dqkv, B, H, S, s);
+  return head_dim == 64 ? zi::attn::bwd<64>(qkv, out, dout, lse, delta, dqkv, B, H, S, colsum_part, s)
+                        : zi::attn::bwd<128>(qkv, out, dout, lse, delta, dqkv, B, H, S, colsum_part, s);
 }
 
 }  // extern "C"

@@ -365,23 +365,27 @@ ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
 // One __syncthreads between the phases and one to release the stage: 2 per R rows,
 // against 5 per 2 rows for ln_bwd_kernel's CTA-wide row reductions. Deterministic: fixed
 // per-row summation order, the CTA's rows in order, CTA partials folded in order.
-constexpr int LNS_NT = 512;
-template <int H, bool DRES>
+// NT = 512: one CTA per SM with a 192 KB ring; NT = 256 (H <= 4096): two CTAs per SM
+// with 96 KB rings each.
+template <int H, bool DRES, int NT>
 struct Lns {
-  static constexpr int R = 8192 / H, W = H / 512, CPT = H / 512, NIN = DRES ? 3 : 2;
+  static constexpr int NW = NT / 32, W = H / 512, R = NW / W, CPT = H / NT;
+  static constexpr int NIN = DRES ? 3 : 2;
   static constexpr int STAGE = NIN * R * H;                 // bf16 elements per stage
-  static constexpr int NSTG = DRES ? 4 : 6;                 // 192 KB of ring
+  static constexpr int NSTG = DRES ? 4 : 6;
+  static constexpr int MINB = NT == 512 ? 1 : 2;
   static constexpr size_t SMEM = (size_t)NSTG * STAGE * 2 + NSTG * 8 + 16 * 16 + 64;
+  static_assert(R >= 1, "a stage holds at least one row");
 };
 
-template <int H, bool DRES, bool RSUM>
-__global__ void __launch_bounds__(LNS_NT, 1)
+template <int H, bool DRES, bool RSUM, int NT>
+__global__ void __launch_bounds__(NT, (Lns<H, DRES, NT>::MINB))
 ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
                     const uint16_t* __restrict__ w, const float* __restrict__ mean,
                     const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
                     uint16_t* __restrict__ dx, float* __restrict__ part, int T) {
   zi::pdl_sync();
-  using L = Lns<H, DRES>;
+  using L = Lns<H, DRES, NT>;
   constexpr int R = L::R, W = L::W, CPT = L::CPT, NS = RSUM ? 3 : 2;
   constexpr int VE = CPT < 8 ? CPT : 8;                     // elements per vector access
   constexpr int NV = CPT / VE;                              // accesses per row
@@ -419,7 +423,7 @@ ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict_
   // phase-2 role: columns a * 512 * VE + tid * VE + [0, VE), a < NV
   float g2[CPT];
 #pragma unroll
-  for (int a = 0; a < NV; ++a) ld_row<VE>(w + (a * LNS_NT + tid) * VE, g2 + a * VE);
+  for (int a = 0; a < NV; ++a) ld_row<VE>(w + (a * NT + tid) * VE, g2 + a * VE);
   float acc[NS][CPT];
 #pragma unroll
   for (int k = 0; k < NS; ++k)
@@ -475,7 +479,7 @@ ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict_
       const size_t grow = (size_t)(g * R + r) * H;
 #pragma unroll
       for (int a = 0; a < NV; ++a) {
-        const int col = (a * LNS_NT + tid) * VE;
+        const int col = (a * NT + tid) * VE;
         float yv[VE], xv[VE], rv[VE], o[VE];
         ld_row<VE>(st + r * H + col, yv);
         ld_row<VE>(st + R * H + r * H + col, xv);
@@ -502,7 +506,7 @@ ln_bwd_split_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict_
     for (int a = 0; a < NV; ++a)
 #pragma unroll
       for (int j = 0; j < VE; ++j)
-        part[((size_t)k * gridDim.x + blockIdx.x) * H + (a * LNS_NT + tid) * VE + j] = acc[k][a * VE + j];
+        part[((size_t)k * gridDim.x + blockIdx.x) * H + (a * NT + tid) * VE + j] = acc[k][a * VE + j];
 }
 
 // part[set][P][H] -> out_set[H] (bf16 RNE or fp32); per column, P is split into
@@ -894,31 +898,41 @@ static int launch_ln_bwd3(int grid, cudaStream_t s, const uint16_t* dy, const ui
   return ZI_OK;
 }
 
-template <int H, bool DRES, bool RSUM>
+template <int H, bool DRES, bool RSUM, int NT>
 static int launch_ln_split3(int grid, cudaStream_t s, const uint16_t* dy, const uint16_t* x,
                             const uint16_t* w, const float* mean, const float* rstd,
                             const uint16_t* dres, uint16_t* dx, float* part, int T) {
-  constexpr size_t smem = Lns<H, DRES>::SMEM;
+  constexpr size_t smem = Lns<H, DRES, NT>::SMEM;
   static bool attr = false;
   if (!attr) {
-    ZI_CUDA(cudaFuncSetAttribute(ln_bwd_split_kernel<H, DRES, RSUM>,
+    ZI_CUDA(cudaFuncSetAttribute(ln_bwd_split_kernel<H, DRES, RSUM, NT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
             "cudaFuncSetAttribute(ln_bwd_split)");
     attr = true;
   }
-  zi::launch_pdl(ln_bwd_split_kernel<H, DRES, RSUM>, dim3(grid), dim3(LNS_NT), smem, s, dy, x, w, mean, rstd, dres, dx,
-                                                                 part, T);
+  zi::launch_pdl(ln_bwd_split_kernel<H, DRES, RSUM, NT>, dim3(grid), dim3(NT), smem, s, dy, x, w,
+                 mean, rstd, dres, dx, part, T);
   return ZI_OK;
 }
 
-template <int H>
+template <int H, int NT>
 static int launch_ln_split(int grid, cudaStream_t s, bool rsum, const uint16_t* dy,
                            const uint16_t* x, const uint16_t* w, const float* mean,
                            const float* rstd, const uint16_t* dres, uint16_t* dx, float* part,
                            int T) {
-  if (rsum) return launch_ln_split3<H, true, true>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
-  if (dres) return launch_ln_split3<H, true, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
-  return launch_ln_split3<H, false, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  if (rsum) return launch_ln_split3<H, true, true, NT>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  if (dres) return launch_ln_split3<H, true, false, NT>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+  return launch_ln_split3<H, false, false, NT>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
+}
+
+// ZI_LNB_NT=256 / 512: threads per CTA of the split LayerNorm backward (A/B)
+static int lnb_nt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZI_LNB_NT");
+    v = e ? atoi(e) : 512;
+  }
+  return v;
 }
 
 template <int TPR>
@@ -1035,8 +1049,9 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
   cudaStream_t s = (cudaStream_t)stream;
   const int tpr = H / 8;
   const bool split = H >= 2048 && !ln_bwd_legacy();
-  const int rpc = split ? 8192 / H : (tpr >= LNB_NT ? 1 : LNB_NT / tpr);
-  int grid = (split || tpr > LNB_NT ? 1 : 2) * sm_count();
+  const int snt = (lnb_nt() == 256 && H <= 4096) ? 256 : 512;
+  const int rpc = split ? snt * 16 / H : (tpr >= LNB_NT ? 1 : LNB_NT / tpr);
+  int grid = (split ? (snt == 256 ? 2 : 1) : (tpr > LNB_NT ? 1 : 2)) * sm_count();
   if (grid > (T + rpc - 1) / rpc) grid = (T + rpc - 1) / rpc;
   const int sets = dres_sum ? 3 : 2;
   // work[0, 1024) holds the column-reduction counters (must stay zero); partials follow
@@ -1049,9 +1064,11 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
   auto DX = (uint16_t*)dx;
   int st = ZI_OK;
   if (split) {
-    if (H == 2048) st = launch_ln_split<2048>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
-    else if (H == 4096) st = launch_ln_split<4096>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
-    else st = launch_ln_split<8192>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    if (H == 2048 && snt == 256) st = launch_ln_split<2048, 256>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else if (H == 2048) st = launch_ln_split<2048, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else if (H == 4096 && snt == 256) st = launch_ln_split<4096, 256>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else if (H == 4096) st = launch_ln_split<4096, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else st = launch_ln_split<8192, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
   } else switch (tpr) {
     case 16: st = launch_ln_bwd<16>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
     case 32: st = launch_ln_bwd<32>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;

@@ -835,8 +835,9 @@ class GPTZeroEngine:
         o = o4.detach().transpose(1, 2).reshape(B * S, c.hd)
         return o, (leaf, o4)
 
-    def _attn_bwd(self, do, saved, delta=None):
-        """delta given: rowsum(do o o) was formed by the GEMM that produced do."""
+    def _attn_bwd(self, do, saved, delta=None, colsum=None):
+        """delta given: rowsum(do o o) was formed by the GEMM that produced do. colsum: fp32
+        [T/32, 3*hd] receiving dqkv's 32-row block column sums (the qkv bias gradient)."""
         c = self.cfg
         if self.cdt == torch.bfloat16:
             qkv, o, lse = saved
@@ -844,7 +845,8 @@ class GPTZeroEngine:
             given = delta is not None
             if not given:
                 delta = torch.empty_like(lse)
-            kernels.attn_bwd(qkv, None if given else o, do, lse, delta, dqkv, c.batch, c.heads)
+            kernels.attn_bwd(qkv, None if given else o, do, lse, delta, dqkv, c.batch, c.heads,
+                             colsum=colsum)
             self.launches += 2 if given else 3
             return dqkv
         leaf, o4 = saved
@@ -1001,12 +1003,19 @@ class GPTZeroEngine:
             kernels.gemm_sk(dx2, P["proj_w"].t(), do, x=o, delta=delta,
                             delta_shape=(c.seq, c.heads, c.head_dim))
             self.launches += 1
-            dqkv = self._attn_bwd(do, att, delta=delta)
+            # the attention backward's epilogues also sum dqkv's columns per 32-row block:
+            # the qkv bias gradient is one small fold instead of a pass over dqkv
+            dqkv_cols = 3 * c.hd
+            part = self._colsum_part(c.tokens, dqkv_cols)
+            dqkv = self._attn_bwd(do, att, delta=delta, colsum=part)
+            self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
+            kernels.colsum_fold(part, c.tokens // 32, dqkv_cols, G["qkv_b"])
+            self.launches += 1
         else:
             do = self._mm_dx("proj.dx", dx2, P["proj_w"])
             dqkv = self._attn_bwd(do, att)
-        self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
-        kernels.bias_grad(dqkv, G["qkv_b"], ws)
+            self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
+            kernels.bias_grad(dqkv, G["qkv_b"], ws)
         dh1 = self._mm_dx("qkv.dx", dqkv, P["qkv_w"])
         dx = torch.empty_like(dh1)
         # ... and LN1 backward sums dres = dx2: the proj bias gradient

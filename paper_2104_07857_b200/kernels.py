@@ -483,7 +483,8 @@ def attn_fwd(qkv: torch.Tensor, out: torch.Tensor, lse: torch.Tensor, batch: int
 
 
 def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torch.Tensor,
-             delta: torch.Tensor, dqkv: torch.Tensor, batch: int, heads: int, stream=None) -> None:
+             delta: torch.Tensor, dqkv: torch.Tensor, batch: int, heads: int, stream=None,
+             colsum=None) -> None:
     """zi_attn_bwd: dqkv of causal attention, deterministic (fixed-order sums, no
     atomics); delta is an fp32 [B*H*S] workspace (rowsum of dout * out)."""
     S, D = _attn_shapes(qkv, batch, heads)
@@ -497,10 +498,13 @@ def attn_bwd(qkv: torch.Tensor, out: torch.Tensor, dout: torch.Tensor, lse: torc
     for t, nm in ((lse, "lse"), (delta, "delta")):
         if t.dtype != torch.float32 or t.numel() != batch * heads * S:
             raise ValueError(f"{nm} must be fp32 with B*H*S elements")
-    _lib.call("zi_attn_bwd", _dev(qkv, "qkv"), _dev(out, "out") if out is not None else None,
-              _dev(dout, "dout"),
+    if colsum is not None and (colsum.dtype != torch.float32 or not colsum.is_contiguous()
+                               or colsum.numel() < qkv.shape[0] // 32 * qkv.shape[1]):
+        raise ValueError("colsum must be contiguous fp32 with B*S/32 * 3*H*D elements")
+    _lib.call("zi_attn_bwd_colsum", _dev(qkv, "qkv"),
+              _dev(out, "out") if out is not None else None, _dev(dout, "dout"),
               _dev(lse, "lse"), _dev(delta, "delta"), _dev(dqkv, "dqkv"), batch, heads, S, D,
-              _stream(stream))
+              colsum.data_ptr() if colsum is not None else None, _stream(stream))
 
 
 def embed_grad(tokens: torch.Tensor, dx: torch.Tensor, acc: torch.Tensor, out: torch.Tensor,

@@ -68,3 +68,13 @@ def test_attention_matches_fp32_reference(B, H, S, D):
     assert torch.equal(dqkv.view(torch.int16), dqkv3.view(torch.int16))
     ref_delta = (out.float() * dout.float()).view(B, S, H, D).sum(-1).permute(0, 2, 1).reshape(-1)
     torch.testing.assert_close(delta, ref_delta, rtol=1e-5, atol=1e-4)
+    # with the bias-gradient side output: dqkv unchanged bit for bit, and the 32-row block
+    # column sums fold to the column sums of dqkv as stored
+    part = torch.full(((B * S) // 32 * 3 * H * D,), float("nan"), device="cuda")
+    dqkv4 = torch.empty_like(qkv)
+    kernels.attn_bwd(qkv, out, dout, lse, delta, dqkv4, B, H, colsum=part)
+    assert torch.equal(dqkv.view(torch.int16), dqkv4.view(torch.int16))
+    db = torch.empty(3 * H * D, device="cuda")
+    kernels.colsum_fold(part, (B * S) // 32, 3 * H * D, db)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(db.double(), dqkv.double().sum(0), rtol=1e-5, atol=1e-4 * S ** 0.5)
