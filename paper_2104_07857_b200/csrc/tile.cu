@@ -1,7 +1,7 @@
 // Memory-centric tiling: one row-block tile of a tiled linear,
 // forward and backward, behind the names of SURVEY §8(b)
-// (zi_linear_tile_fwd / zi_linear_tile_bwd). The GEMMs are zi_gemm (tcgen05 +
-// TMEM, TMA-fed, 2-SM pair tiles); the tile's bias gradient is a deterministic
+// (zi_linear_tile_fwd / zi_linear_tile_bwd). The GEMMs are zi_gemm_sk / zi_gemm (tcgen05
+// + TMEM, TMA-fed, 2-SM pair tiles); the tile's bias gradient is a deterministic
 // fp32 column sum over the tile's strided column block of the upstream grad.
 #include "common.cuh"
 
@@ -45,8 +45,19 @@ tile_colsum_kernel(const __nv_bfloat16* __restrict__ dy, int M, int N, int ld,
 
 extern "C" {
 
+// Tiles whose shapes meet zi_gemm_sk's contract (16-byte rows: N, ld multiples of 8) run on
+// the stream-K kernel with whole tiles (no workspace: each output element is one K-ordered
+// accumulation, so results do not depend on the tile count); others on zi_gemm.
+static bool sk_ok(int N, int lda, int ldb, int ldd, const void* a, const void* b, const void* d) {
+  return N % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0 && ldd % 8 == 0 && zi::aligned(a, 16) &&
+         zi::aligned(b, 16) && zi::aligned(d, 16);
+}
+
 int zi_linear_tile_fwd(const void* x, const void* w_t, const void* b_t, void* y, int M, int K,
                        int N_t, int ldx, int ldw, int ldy, void* stream) {
+  if (sk_ok(N_t, ldx, ldw, ldy, x, w_t, y) && (!b_t || zi::aligned(b_t, 16)))
+    return zi_gemm_sk(x, 0, ldx, w_t, 0, ldw, b_t, y, ldy, 0, nullptr, 0, nullptr, 0, ZI_EPI_PLAIN,
+                      M, N_t, K, nullptr, 0, stream);
   return zi_gemm(x, 0, ldx, w_t, 0, ldw, b_t, y, 0, 0, ldy, M, N_t, K, stream);
 }
 
@@ -57,7 +68,11 @@ int zi_linear_tile_bwd(const void* x, int ldx, const void* w_t, int ldw, const v
                "zi_linear_tile_bwd: bad arguments");
   int st;
   if (dw_t) {   // dW_t[n, k] = sum_m dy_t[m, n] x[m, k]   (both operands MN-major)
-    st = zi_gemm(dy_t, 1, lddy, x, 1, ldx, nullptr, dw_t, 0, 0, lddw, N_t, K, M, stream);
+    if (sk_ok(K, lddy, ldx, lddw, dy_t, x, dw_t) && N_t % 8 == 0)
+      st = zi_gemm_sk(dy_t, 1, lddy, x, 1, ldx, nullptr, dw_t, lddw, 0, nullptr, 0, nullptr, 0,
+                      ZI_EPI_PLAIN, N_t, K, M, nullptr, 0, stream);
+    else
+      st = zi_gemm(dy_t, 1, lddy, x, 1, ldx, nullptr, dw_t, 0, 0, lddw, N_t, K, M, stream);
     if (st) return st;
   }
   if (dx_acc) { // dx[m, k] += sum_n dy_t[m, n] W_t[n, k]  (fp32, tiles accumulate in order)
