@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include "bulk.cuh"
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -693,8 +694,9 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
 template <int D>
 struct Bkv {
   static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 3;   // q / dO half stages
+  // LD: each stage's 64 lse and 64 delta values (bulk-copied with its q / dO halves)
   static constexpr int K = 0, V = TB, QD = 2 * TB, PT = QD + NST * 2 * HB, DST = PT + 2 * 16384,
-                       BAR = DST + 2 * 16384;
+                       LD = DST + 2 * 16384, BAR = LD + NST * 512;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -709,7 +711,7 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
   uint8_t *sK = sm + L::K, *sV = sm + L::V, *sQD = sm + L::QD, *sPT = sm + L::PT,
-          *sdST = sm + L::DST;
+          *sdST = sm + L::DST, *sLD = sm + L::LD;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 1 + NST,
            *st_full = bar + 1 + 2 * NST, *st_free = st_full + 2, *ps_full = st_full + 4,
@@ -750,9 +752,12 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
       for (int u = 0; u < nsub; ++u) {
         const int st = u % NST, r = row0 + j * 128 + u * 64;   // q rows of sub-tile u
         mbar_wait(&qd_empty[st], ((u / NST) & 1) ^ 1);
-        mbar_expect_tx(&qd_full[st], 2 * HB);
+        mbar_expect_tx(&qd_full[st], 2 * HB + 512);
         load_rows<D, 64>(sQD + st * 2 * HB, &tm, &qd_full[st], h * D, r);
         load_rows<D, 64>(sQD + st * 2 * HB + HB, &tm_do, &qd_full[st], h * D, r);
+        const size_t q0 = (size_t)bh * S + j * 128 + u * 64;
+        bulk::g2s(sLD + st * 512, lse + q0, 256, &qd_full[st]);
+        bulk::g2s(sLD + st * 512 + 256, delta + q0, 256, &qd_full[st]);
       }
     }
   } else if (warp == 1) {
@@ -798,11 +803,13 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     uint8_t *sPTg = sPT + g * 16384, *sdSTg = sdST + g * 16384;
     const int nit = nsub / 2;
     for (int it = 0; it < nit; ++it) {
-      // lse / delta of the sub-tile's 64 queries: warp-uniform read-only loads (broadcast)
-      const size_t q0 = (size_t)bh * S + (j + it) * 128 + g * 64;
-      const float4* lq = reinterpret_cast<const float4*>(lse + q0);
-      const float4* dq4 = reinterpret_cast<const float4*>(delta + q0);
+      // lse / delta of the sub-tile's 64 queries, bulk-copied into the stage with its q /
+      // dO halves (shared-memory broadcast reads instead of dependent global loads)
+      const int u = 2 * it + g, ust = u % L::NST;
+      const float4* lq = reinterpret_cast<const float4*>(sLD + ust * 512);
+      const float4* dq4 = reinterpret_cast<const float4*>(sLD + ust * 512 + 256);
       mbar_wait(&st_full[g], it & 1);
+      mbar_wait(&qd_full[ust], (u / L::NST) & 1);  // complete already (the MMA waited on it)
       fence_after_sync();
       if (it >= 1) mbar_wait(&ps_empty[g], (it - 1) & 1);
 #pragma unroll 1
@@ -813,7 +820,7 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
         float Ls[32], Ds[32];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const float4 a = __ldg(lq + c * 8 + k), d = __ldg(dq4 + c * 8 + k);
+          const float4 a = lq[c * 8 + k], d = dq4[c * 8 + k];
           Ls[4 * k] = a.x; Ls[4 * k + 1] = a.y; Ls[4 * k + 2] = a.z; Ls[4 * k + 3] = a.w;
           Ds[4 * k] = d.x; Ds[4 * k + 1] = d.y; Ds[4 * k + 2] = d.z; Ds[4 * k + 3] = d.w;
         }
