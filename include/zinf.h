@@ -311,9 +311,14 @@ int zi_gemm(const void* A, int a_mn_major, int lda, const void* B, int b_mn_majo
  *   ZI_EPI_GELU   D = u = bf16(acc + bias), D2 = bf16(gelu_tanh(u))   fc1 forward
  *   ZI_EPI_RESID  D = bf16(bf16(acc + bias) + X)                        fc2 forward + residual
  *   ZI_EPI_DGELU  D = bf16(bf16(acc) * gelu_tanh'(X)), X = u            fc2 dX -> fc1 du
+ * zi_gemm_sk only:
+ *   ZI_EPI_GELU_SAVE  u = bf16(acc + bias): D = bf16(gelu_tanh'(u)), D2 = bf16(gelu_tanh(u))
+ *                     (fc1 forward keeping GELU' for the backward instead of u)
+ *   ZI_EPI_MUL        D = bf16(bf16(acc) * X), X = the saved GELU'           fc2 dX -> fc1 du
  * X (ldx) and D2 (ldd2) are M x N bf16; N % 8 == 0 and all leading dimensions
  * multiples of 8. Operand majorness as zi_gemm. */
-enum { ZI_EPI_PLAIN = 0, ZI_EPI_GELU = 1, ZI_EPI_RESID = 2, ZI_EPI_DGELU = 3 };
+enum { ZI_EPI_PLAIN = 0, ZI_EPI_GELU = 1, ZI_EPI_RESID = 2, ZI_EPI_DGELU = 3,
+       ZI_EPI_GELU_SAVE = 4, ZI_EPI_MUL = 5 };
 int zi_gemm_ex(const void* A, int a_mn_major, int lda, const void* B, int b_mn_major, int ldb,
                const void* bias, void* D, int ldd, const void* X, int ldx, void* D2, int ldd2,
                int epi, int M, int N, int K, void* stream);

@@ -128,6 +128,13 @@ __device__ __forceinline__ float gelu_tanh(float z) {
   return 0.5f * z * (1.f + tanh_fast(GELU_C * (z + GELU_A * z * z * z)));
 }
 
+// gelu_tanh(z) and gelu_tanh'(z) from one tanh (the fc1 forward saving GELU')
+__device__ __forceinline__ void gelu_and_grad(float z, float& g, float& gp) {
+  const float th = tanh_fast(GELU_C * (z + GELU_A * z * z * z));
+  g = 0.5f * z * (1.f + th);
+  gp = 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * GELU_C * (1.f + 3.f * GELU_A * z * z);
+}
+
 __device__ __forceinline__ float gelu_tanh_grad(float z) {
   const float th = tanh_fast(GELU_C * (z + GELU_A * z * z * z));
   return 0.5f * (1.f + th) + 0.5f * z * (1.f - th * th) * GELU_C * (1.f + 3.f * GELU_A * z * z);

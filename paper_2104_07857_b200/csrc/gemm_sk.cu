@@ -57,7 +57,8 @@ constexpr int FLAG_BYTES = 1 << 16;         // flag area at the start of the wor
 constexpr int GROUP_M = 16;
 
 constexpr int EPI_PLAIN = ZI_EPI_PLAIN, EPI_GELU = ZI_EPI_GELU, EPI_RESID = ZI_EPI_RESID,
-              EPI_DGELU = ZI_EPI_DGELU, EPI_F32 = 4;
+              EPI_DGELU = ZI_EPI_DGELU, EPI_GELU_SAVE = ZI_EPI_GELU_SAVE, EPI_MUL = ZI_EPI_MUL,
+              EPI_F32 = 16;
 
 constexpr size_t smem_bytes(int NS, int EW, int BPW) {
   return (size_t)NS * STAGE_BYTES + (size_t)EW * BPW * BOX_BYTES + 1024 + 256;
@@ -165,7 +166,7 @@ __device__ __forceinline__ void epi_words(const uint32_t* v, int row, int col0, 
         f[2 * j + 1] += bf16f(bw[j] >> 16);
       }
     }
-    if (EPI == EPI_RESID || EPI == EPI_DGELU) {
+    if (EPI == EPI_RESID || EPI == EPI_DGELU || EPI == EPI_MUL) {
       uint4 xv = make_uint4(0, 0, 0, 0);
       if (in && row < M) xv = *reinterpret_cast<const uint4*>(X + (size_t)row * ldx + c);
       const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -175,6 +176,9 @@ __device__ __forceinline__ void epi_words(const uint32_t* v, int row, int col0, 
         if (EPI == EPI_RESID) {
           f[2 * j] = rbf(f[2 * j]) + x0;
           f[2 * j + 1] = rbf(f[2 * j + 1]) + x1;
+        } else if (EPI == EPI_MUL) {
+          f[2 * j] = rbf(f[2 * j]) * x0;
+          f[2 * j + 1] = rbf(f[2 * j + 1]) * x1;
         } else {
           f[2 * j] = rbf(f[2 * j]) * gelu_tanh_grad(x0);
           f[2 * j + 1] = rbf(f[2 * j + 1]) * gelu_tanh_grad(x1);
@@ -497,7 +501,19 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           } else {
             uint32_t wd[32];
             epi_words<EPI>(v, row, gcol, M, N, bias, X, ldx, wd);
+            uint32_t wg[EPI == EPI_GELU_SAVE ? 32 : 1];
+            if (EPI == EPI_GELU_SAVE) {   // D <- GELU'(u), D2 <- GELU(u), one tanh each
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                float g0, g1, d0, d1;
+                gelu_and_grad(bf16f(wd[i] & 0xFFFF), g0, d0);
+                gelu_and_grad(bf16f(wd[i] >> 16), g1, d1);
+                wg[i] = pack_bf16(g0, g1);
+                wd[i] = pack_bf16(d0, d1);
+              }
+            }
             const uint8_t* box = emit(&tmD, wd, gcol, r0);
+            if (EPI == EPI_GELU_SAVE) emit(&tmD2, wg, gcol, r0);
             if (aux.csum != nullptr && r0 < M) {
               // column pair (2 lane, 2 lane + 1) of the 32 staged rows, summed in row
               // order (the box is SW128: row r's 16-byte chunk j at (j ^ (r % 8)) * 16)
@@ -784,6 +800,8 @@ static int dispatch(int epi, const CUtensorMap& ma, const CUtensorMap& mb, const
     case EPI_GELU: return launch<A_MN, B_MN, EPI_GELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
     case EPI_RESID: return launch<A_MN, B_MN, EPI_RESID, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
     case EPI_DGELU: return launch<A_MN, B_MN, EPI_DGELU, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_GELU_SAVE: return launch<A_MN, B_MN, EPI_GELU_SAVE, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
+    case EPI_MUL: return launch<A_MN, B_MN, EPI_MUL, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
     case EPI_F32: return launch<A_MN, B_MN, EPI_F32, CL>(ma, mb, md, md2, bias, X, ldx, M, N, sc, part, flag, aux, s);
   }
   set_error("zi_gemm_sk: unknown epilogue %d", epi);
@@ -829,16 +847,17 @@ extern "C" int zi_gemm_sk_aux(const void* A, int a_mn_major, int lda, const void
   ZI_CHECK_ARG(zi::aligned(A, 16) && zi::aligned(B, 16) && zi::aligned(D, 16) &&
                (!bias || zi::aligned(bias, 16)), "zi_gemm_sk: 16-byte aligned buffers");
   ZI_CHECK_ARG(!(a_mn_major && !b_mn_major), "zi_gemm_sk: MN-major A needs MN-major B");
-  ZI_CHECK_ARG(epi >= ZI_EPI_PLAIN && epi <= ZI_EPI_DGELU, "zi_gemm_sk: unknown epilogue %d", epi);
+  ZI_CHECK_ARG(epi >= ZI_EPI_PLAIN && epi <= ZI_EPI_MUL, "zi_gemm_sk: unknown epilogue %d", epi);
   if (d_f32) {
     ZI_CHECK_ARG(epi == ZI_EPI_PLAIN && !bias, "zi_gemm_sk: fp32 output takes no epilogue");
     ZI_CHECK_ARG(ldd % 4 == 0 && N % 4 == 0, "zi_gemm_sk: fp32 output needs N, ldd % 4 == 0");
   } else {
     ZI_CHECK_ARG(ldd % 8 == 0 && N % 8 == 0, "zi_gemm_sk: bf16 output needs N, ldd % 8 == 0");
   }
-  ZI_CHECK_ARG(epi != ZI_EPI_GELU || (D2 && ldd2 % 8 == 0 && ldd2 >= N && zi::aligned(D2, 16)),
+  ZI_CHECK_ARG((epi != ZI_EPI_GELU && epi != ZI_EPI_GELU_SAVE) ||
+               (D2 && ldd2 % 8 == 0 && ldd2 >= N && zi::aligned(D2, 16)),
                "zi_gemm_sk: GELU epilogue needs D2");
-  ZI_CHECK_ARG((epi != ZI_EPI_RESID && epi != ZI_EPI_DGELU && !delta) ||
+  ZI_CHECK_ARG((epi != ZI_EPI_RESID && epi != ZI_EPI_DGELU && epi != ZI_EPI_MUL && !delta) ||
                (X && ldx % 8 == 0 && ldx >= N && zi::aligned(X, 16)),
                "zi_gemm_sk: epilogue needs X");
   ZI_CHECK_ARG(!ws || ws_bytes >= zi_gemm_sk_workspace_bytes(),

@@ -115,8 +115,10 @@ def tune_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
         sites[name] = tune((name, T, w.shape[0], hd),
                            lambda w=w, b=b, out=out: kernels.gemm_sk(x, w, out, bias=b),
                            lambda w=w, b=b, out=out: torch.addmm(b, x, w.t(), out=out))
+    # the product path's epilogues: fc1 keeps GELU' for the backward ("gelu_save"), fc2.dx
+    # multiplies by it and sums the fc1 bias gradient's 32-row blocks (+ the fold)
     sites["fc1.fwd"] = tune(("fc1.fwd+gelu", T, H4, hd),
-                            lambda: kernels.gemm_sk(x, w1, o4, bias=b1, epi="gelu", out2=a4),
+                            lambda: kernels.gemm_sk(x, w1, o4, bias=b1, epi="gelu_save", out2=a4),
                             lambda: (torch.addmm(b1, x, w1.t(), out=o4), kernels.gelu_fwd(o4, a4)))
     sites["fc2.fwd"] = tune(("fc2.fwd+resid", T, hd, H4),
                             lambda: kernels.gemm_sk(u, w2, oh, bias=bh, epi="resid", x=oh2),
@@ -127,9 +129,10 @@ def tune_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
         sites[name] = tune((name, T, gw.shape[0], gw.shape[1]),
                            lambda dy=dy, inp=inp, gw=gw: kernels.gemm_sk(dy.t(), inp.t(), gw),
                            lambda dy=dy, inp=inp, gw=gw: torch.mm(dy.t(), inp, out=gw))
+    part = torch.empty(-(-T // 32) * H4, dtype=torch.float32, device=device)
     sites["fc2.dx"] = tune(("fc2.dx+dgelu", T, H4, hd),
-                           lambda: (kernels.gemm_sk(x, w2.t(), a4, epi="dgelu", x=u),
-                                    kernels.bias_grad(a4, db, ws)),
+                           lambda: (kernels.gemm_sk(x, w2.t(), a4, epi="mul", x=u, colsum=part),
+                                    kernels.colsum_fold(part, -(-T // 32), H4, db)),
                            lambda: (torch.mm(x, w2, out=o4), kernels.bias_grad(o4, db, ws, u=u,
                                                                                 du=a4)))
     for name, dy, w, out in (("fc1.dx", dy4, w1, oh), ("proj.dx", x, wp, oh),
@@ -137,7 +140,7 @@ def tune_gpt(T: int, hd: int, vocab: int, ws, device) -> dict:
         sites[name] = tune((name, T, hd, dy.shape[1]),
                            lambda dy=dy, w=w, out=out: kernels.gemm_sk(dy, w.t(), out),
                            lambda dy=dy, w=w, out=out: torch.mm(dy, w, out=out))
-    del x, u, w3, w1, w2, wp, o3, o4, oh, oh2, a4, gw3, gw1, gw2, gwp, dy4, dy3
+    del x, u, w3, w1, w2, wp, o3, o4, oh, oh2, a4, gw3, gw1, gw2, gwp, dy4, dy3, part
     # tied head: logits, dW (fp32 accumulator), dx
     hf, wte = rnd(T, hd), rnd(vocab, hd)
     logits = torch.empty(T, vocab, dtype=bf, device=device)

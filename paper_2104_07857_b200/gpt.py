@@ -854,6 +854,12 @@ class GPTZeroEngine:
         (dqkv,) = torch.autograd.grad(o4, leaf, g4)
         return dqkv.reshape(-1, 3 * c.hd)
 
+    def _gelu_save(self) -> bool:
+        """fc1's forward epilogue stores GELU'(u) in place of u for fc2's input-gradient
+        epilogue (both sites on zi_gemm_sk, side outputs on)."""
+        return (self.epi_aux and self.gsel.get("fc1.fwd") == "zi"
+                and self.gsel.get("fc2.dx") == "zi")
+
     def _colsum_part(self, T: int, N: int) -> torch.Tensor:
         """fp32 [ceil(T/32), N] block column sums of a GEMM epilogue (one buffer, reused
         in stream order)."""
@@ -947,7 +953,10 @@ class GPTZeroEngine:
         u = torch.empty(T, H4, dtype=h2.dtype, device=h2.device)
         a = torch.empty_like(u)
         if self._zi("fc1.fwd", h2, P["fc1_w"], P["fc1_b"], u, a):
-            kernels.gemm_sk(h2, P["fc1_w"], u, bias=P["fc1_b"], epi="gelu", out2=a)
+            # with the GELU'-saving epilogue, "u" holds GELU'(u): the fc2 input-gradient
+            # GEMM then only multiplies (its epilogue no longer evaluates tanh)
+            kernels.gemm_sk(h2, P["fc1_w"], u, bias=P["fc1_b"],
+                            epi="gelu_save" if self._gelu_save() else "gelu", out2=a)
         else:
             torch.addmm(P["fc1_b"], h2, P["fc1_w"].t(), out=u)
             kernels.gelu_fwd(u, a)
@@ -975,7 +984,8 @@ class GPTZeroEngine:
             # block, so db1 is one small fold instead of a pass over du
             T, H4 = du.shape
             part = self._colsum_part(T, H4)
-            kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u, colsum=part)
+            kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="mul" if self._gelu_save() else "dgelu",
+                            x=u, colsum=part)
             kernels.colsum_fold(part, -(-T // 32), H4, G["fc1_b"])
             self.launches += 1
         elif self._zi("fc2.dx", dy, P["fc2_w"], du, u):   # A/B: separate bias pass

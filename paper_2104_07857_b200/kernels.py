@@ -239,7 +239,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, accumul
     return out
 
 
-EPI = {"plain": 0, "gelu": 1, "resid": 2, "dgelu": 3}
+EPI = {"plain": 0, "gelu": 1, "resid": 2, "dgelu": 3, "gelu_save": 4, "mul": 5}
 
 
 def gemm_ex(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, bias=None, epi: str = "plain",

@@ -21,7 +21,15 @@ cases = {
     "plain": lambda: kernels.gemm_sk(a, b, y),
     "dgelu": lambda: kernels.gemm_sk(a, b, y, epi="dgelu", x=u),
     "dgelu+colsum": lambda: kernels.gemm_sk(a, b, y, epi="dgelu", x=u, colsum=part),
+    "mul+colsum": lambda: kernels.gemm_sk(a, b, y, epi="mul", x=u, colsum=part),
 }
+# the fc1 forward site (8192 x 8192 x 2048, K-major B): GELU vs GELU'-saving epilogue
+h = torch.randn(M, K, device="cuda", dtype=bf)
+w1 = (torch.randn(N, K, device="cuda") * K ** -0.5).to(bf)
+b1 = torch.randn(N, device="cuda", dtype=bf)
+y2 = torch.empty(M, N, device="cuda", dtype=bf)
+cases["fwd gelu"] = lambda: kernels.gemm_sk(h, w1, y, bias=b1, epi="gelu", out2=y2)
+cases["fwd gelu_save"] = lambda: kernels.gemm_sk(h, w1, y, bias=b1, epi="gelu_save", out2=y2)
 
 
 def t(fn, n=20):

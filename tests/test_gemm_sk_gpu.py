@@ -117,6 +117,18 @@ def test_epilogues(M, N, K):
     torch.cuda.synchronize()
     ref = acc.to(bf).float() * gelu_grad(x.float())
     check(yd, ref, K, name="dgelu", extra=acc.abs() * (gelu_grad(x.float()).abs() * 2 ** -7 + 2 ** -9))
+    # GELU'-saving forward: D = GELU'(u), D2 = GELU(u) of the kernel's own bf16 u (the same
+    # GELU bits as the "gelu" epilogue); then the multiply-only backward epilogue
+    gp, ga = torch.empty(M, N, device="cuda", dtype=bf), torch.empty(M, N, device="cuda", dtype=bf)
+    kernels.gemm_sk(a, b, gp, bias=bias, epi="gelu_save", out2=ga)
+    torch.cuda.synchronize()
+    assert torch.equal(ga.view(torch.int16), y2.view(torch.int16))
+    check(gp, gelu_grad(y.float()), K, rel=2 ** -7, name="gelu_save.d",
+          extra=(y.float().abs() + 1) * 2 ** -9)
+    ym = torch.empty(M, N, device="cuda", dtype=bf)
+    kernels.gemm_sk(a, b, ym, epi="mul", x=gp)
+    torch.cuda.synchronize()
+    check(ym, acc.to(bf).float() * gp.float(), K, name="mul", extra=acc.abs() * gp.float().abs() * 2 ** -7)
 
 
 @pytest.mark.parametrize("M,N,K,kind", [(8192, 2048, 2048, "fwd"), (2048, 2048, 8192, "dw"),
