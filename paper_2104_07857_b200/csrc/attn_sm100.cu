@@ -693,10 +693,11 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
 // CTA = kv tile j; sub-tiles over the q columns (q halves of tiles i >= j).
 template <int D>
 struct Bkv {
-  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 3;   // q / dO half stages
+  // q / dO half-tile stages; P^T / dS^T live in TMEM, so the shared memory they took holds a
+  // fourth stage (the Q / dO loads of sub-tile u+4 wait only for dV / dK of u)
+  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 4;
   // LD: each stage's 64 lse and 64 delta values (bulk-copied with its q / dO halves)
-  static constexpr int K = 0, V = TB, QD = 2 * TB, PT = QD + NST * 2 * HB, DST = PT + 2 * 16384,
-                       LD = DST + 2 * 16384, BAR = LD + NST * 512;
+  static constexpr int K = 0, V = TB, QD = 2 * TB, LD = QD + NST * 2 * HB, BAR = LD + NST * 512;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -705,13 +706,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_do,
                 const float* __restrict__ lse, const float* __restrict__ delta,
                 __nv_bfloat16* __restrict__ dqkv, int B, int H, int S, int hd, float sl2,
-                float scale, int grp, float* __restrict__ csum) {
+                float scale, int grp, float* __restrict__ csum,
+                unsigned long long* __restrict__ trace) {
+  // trace (diagnostics, normally null), CTA 0 only, clock64 per sub-tile u:
+  // [S warp: qd landed, st_free passed, issued] [acc warp: ps_full passed]
+  // [group: st_full passed, ps_empty passed, published]
+  unsigned long long* tk = (trace && blockIdx.x == 0) ? trace : nullptr;
   using L = Bkv<D>;
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sK = sm + L::K, *sV = sm + L::V, *sQD = sm + L::QD, *sPT = sm + L::PT,
-          *sdST = sm + L::DST, *sLD = sm + L::LD;
+  uint8_t *sK = sm + L::K, *sV = sm + L::V, *sQD = sm + L::QD, *sLD = sm + L::LD;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t *kv_full = bar, *qd_full = bar + 1, *qd_empty = bar + 1 + NST,
            *st_full = bar + 1 + 2 * NST, *st_free = st_full + 2, *ps_full = st_full + 4,
@@ -763,11 +768,14 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
     mbar_wait(kv_full, 0);
-    // S^T / dP^T of sub-tile u as soon as group g has loaded u-2's (st_free)
+    // S^T / dP^T of sub-tile u into slot g once dV / dK of u-2 have read its P^T / dS^T
+    // (which overwrote S^T / dP^T u-2 in TMEM)
     for (int u = 0; u < nsub; ++u) {
       const int st = u % NST, g = u & 1;
       mbar_wait(&qd_full[st], (u / NST) & 1);
-      if (u >= 2) mbar_wait(&st_free[g], ((u - 2) >> 1) & 1);
+      if (tk && lane == 0) tk[u * 8 + 0] = clock64();
+      if (u >= 2) mbar_wait(&ps_empty[g], ((u - 2) >> 1) & 1);
+      if (tk && lane == 0) tk[u * 8 + 1] = clock64();
       fence_after_sync();
       if (elect_one()) {
         const uint8_t* q = sQD + st * 2 * HB;
@@ -776,6 +784,7 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
         umma_commit(&st_full[g]);
       }
       __syncwarp();
+      if (tk && lane == 0) tk[u * 8 + 2] = clock64();
     }
   } else if (warp == ACC_WARP) {
     // dV += P^T dO, dK += dS^T Q of sub-tile v once group g published them
@@ -783,11 +792,12 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     for (int v = 0; v < nsub; ++v) {
       const int st = v % NST, g = v & 1;
       mbar_wait(&ps_full[g], (v >> 1) & 1);
+      if (tk && lane == 0) tk[v * 8 + 3] = clock64();
       fence_after_sync();
       if (elect_one()) {
         const uint8_t* q = sQD + st * 2 * HB;
-        mma_tile<64, true, 4>(tmem + 256, sPT + g * 16384, q + HB, id_d, v > 0);
-        mma_tile<64, true, 4>(tmem + 384, sdST + g * 16384, q, id_d, v > 0);
+        mma_tile_ts<64, 4>(tmem + 256, tmem + g * 128, q + HB, id_d, v > 0);      // P^T
+        mma_tile_ts<64, 4>(tmem + 384, tmem + g * 128 + 64, q, id_d, v > 0);  // dS^T
         umma_commit(&qd_empty[st]);
         umma_commit(&ps_empty[g]);
       }
@@ -800,7 +810,6 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
     const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
     const uint32_t tST = tmem + g * 128 + lo, tdPT = tST + 64;
-    uint8_t *sPTg = sPT + g * 16384, *sdSTg = sdST + g * 16384;
     const int nit = nsub / 2;
     for (int it = 0; it < nit; ++it) {
       // lse / delta of the sub-tile's 64 queries, bulk-copied into the stage with its q /
@@ -810,8 +819,10 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
       const float4* dq4 = reinterpret_cast<const float4*>(sLD + ust * 512 + 256);
       mbar_wait(&st_full[g], it & 1);
       mbar_wait(&qd_full[ust], (u / L::NST) & 1);  // complete already (the MMA waited on it)
+      unsigned long long* tg = (tk && lane == 0 && q4 == 0) ? tk + u * 8 : nullptr;
+      if (tg) tg[4] = clock64();
       fence_after_sync();
-      if (it >= 1) mbar_wait(&ps_empty[g], (it - 1) & 1);
+      if (tg) tg[5] = clock64();
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t s32[32], p32[32];
@@ -838,19 +849,16 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
           pp[k >> 1] = pack_bf16(p0, p1);
           dd[k >> 1] = pack_bf16(p0 * (u2f(p32[k]) - Ds[k]), p1 * (u2f(p32[k + 1]) - Ds[k + 1]));
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          st_piece(sPTg, r, c * 4 + q, make_uint4(pp[4 * q], pp[4 * q + 1], pp[4 * q + 2], pp[4 * q + 3]));
-          st_piece(sdSTg, r, c * 4 + q, make_uint4(dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]));
-        }
+        // P^T / dS^T (bf16 pairs) over this thread's S^T / dP^T columns already read:
+        // chunk c writes columns c*16 .. c*16+15, read by chunk 0
+        tmem_st16_nowait(tST + c * 16, pp);
+        tmem_st16_nowait(tdPT + c * 16, dd);
       }
+      tmem_wait_st();
       fence_before_sync();
-      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&st_free[g]);
-        mbar_arrive(&ps_full[g]);
-      }
+      if (lane == 0) mbar_arrive(&ps_full[g]);
+      if (tg) tg[6] = clock64();
     }
     mbar_wait(acc_done, 0);
     fence_after_sync();
@@ -1184,7 +1192,7 @@ static int bwd(const void* qkv, const void* out, const void* dout, const float* 
   // no shared-memory round trip — measured 5 % slower: with TMEM full, the next q tile's
   // scores cannot overlap the elementwise work, so MMA and softmax serialise)
   zi::launch_pdl(bwd_dkdv_kernel<D>, dim3(grid), dim3(THREADS), Bkv<D>::BYTES, st, tm, tdo,
-                 lse, delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H), csum);
+                 lse, delta, dq, B, H, S, hd, sl2, scale, attn_group(B * H), csum, g_trace);
   if ((rc = launch_status("zi_attn_bwd(dkdv)")) != ZI_OK) return rc;
   // (likewise a 128-column dQ variant with dS in TMEM, one score slot overlapped with the
   // previous tile's elementwise work: 4 % slower than the two 64-column groups)

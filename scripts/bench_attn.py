@@ -37,6 +37,20 @@ def main():
     dout = torch.randn_like(out)
     dqkv = torch.empty_like(qkv)
     unit = 2.0 * B * H * S * S * D / 2      # one causal matmul
+    if "--trace-bwd" in sys.argv:           # CTA 0 of the dK / dV kernel (j = 0: 16 sub-tiles)
+        from paper_2104_07857_b200 import _lib
+        kernels.attn_fwd(qkv, out, lse, B, H)
+        tr = torch.zeros(64 * 8, dtype=torch.int64, device="cuda")
+        _lib.call("zi_attn_set_trace", tr.data_ptr())
+        kernels.attn_bwd(qkv, out, dout, lse, delta, dqkv, B, H)
+        torch.cuda.synchronize()
+        _lib.call("zi_attn_set_trace", None)
+        t = tr.view(64, 8).cpu().double()
+        base = t[0, 0]
+        print("u: [S qd landed, st_free, S issued | acc ps_full | group st_full, ps_empty, published] kcycles")
+        for u in range(2 * (S // 128)):
+            print("   ", u, [round(float(v - base) / 1000, 2) for v in t[u, :7]])
+        return
     if "--trace2" in sys.argv:              # per-CTA timeline of the two-q-tile forward
         from paper_2104_07857_b200 import _lib
         nct = B * H * (S // 256)
