@@ -885,8 +885,9 @@ bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ 
 // CTA = q tile i; sub-tiles over the kv columns (kv halves of tiles j <= i).
 template <int D>
 struct Bq {
-  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 4;   // kv half stages
-  static constexpr int Q = 0, DO = TB, KV = 2 * TB, DS = KV + NST * 2 * HB, BAR = DS + 2 * 16384;
+  // kv half stages; dS lives in TMEM (over S), so its former shared memory is a 5th stage
+  static constexpr int TB = 128 * D * 2, HB = 64 * D * 2, NST = 5;
+  static constexpr int Q = 0, DO = TB, KV = 2 * TB, BAR = KV + NST * 2 * HB;
   static constexpr int BYTES = BAR + 256 + 1024;
 };
 
@@ -900,7 +901,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
   constexpr int TB = L::TB, HB = L::HB, NST = L::NST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = align1024(smem_raw);
-  uint8_t *sQ = sm + L::Q, *sdO = sm + L::DO, *sKV = sm + L::KV, *sdS = sm + L::DS;
+  uint8_t *sQ = sm + L::Q, *sdO = sm + L::DO, *sKV = sm + L::KV;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L::BAR);
   uint64_t *qd_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + NST,
            *s_full = bar + 1 + 2 * NST, *s_free = s_full + 2, *ds_full = s_full + 4,
@@ -950,11 +951,11 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
   } else if (warp == 1) {
     constexpr uint32_t id_s = idesc_bf16_f32(128, 64, false, false);
     mbar_wait(qd_full, 0);
-    // S / dP of sub-tile u as soon as group g has loaded u-2's (s_free)
+    // S / dP of sub-tile u into slot g once dQ of u-2 has read its dS (over S u-2 in TMEM)
     for (int u = 0; u < nsub; ++u) {
       const int st = u % NST, g = u & 1;
       mbar_wait(&kv_full[st], (u / NST) & 1);
-      if (u >= 2) mbar_wait(&s_free[g], ((u - 2) >> 1) & 1);
+      if (u >= 2) mbar_wait(&ds_empty[g], ((u - 2) >> 1) & 1);
       fence_after_sync();
       if (elect_one()) {
         const uint8_t* kv = sKV + st * 2 * HB;
@@ -972,7 +973,7 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
       mbar_wait(&ds_full[g], (v >> 1) & 1);
       fence_after_sync();
       if (elect_one()) {
-        mma_tile<64, true, 4>(tmem + 256, sdS + g * 16384, sKV + st * 2 * HB, id_d, v > 0);
+        mma_tile_ts<64, 4>(tmem + 256, tmem + g * 128, sKV + st * 2 * HB, id_d, v > 0);
         umma_commit(&kv_empty[st]);
         umma_commit(&ds_empty[g]);
       }
@@ -984,14 +985,12 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
     const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane;
     const uint32_t lo = (uint32_t)(q4 * 32) << 16;
     const uint32_t tSg = tmem + g * 128 + lo, tdPg = tSg + 64;
-    uint8_t* sdSg = sdS + g * 16384;
     const float nl = -lse[(size_t)bh * S + i * 128 + r];
     const float del = delta[(size_t)bh * S + i * 128 + r];
     const int nit = nsub / 2;
     for (int jj = 0; jj < nit; ++jj) {
       mbar_wait(&s_full[g], jj & 1);
       fence_after_sync();
-      if (jj >= 1) mbar_wait(&ds_empty[g], (jj - 1) & 1);
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t s32[32], p32[32];
@@ -1010,17 +1009,12 @@ bwd_dq_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CU
           }
           dd[k >> 1] = pack_bf16(p0 * (u2f(p32[k]) - del), p1 * (u2f(p32[k + 1]) - del));
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          st_piece(sdSg, r, c * 4 + q, make_uint4(dd[4 * q], dd[4 * q + 1], dd[4 * q + 2], dd[4 * q + 3]));
+        tmem_st16_nowait(tSg + c * 16, dd);   // dS over S columns chunk 0 has read
       }
+      tmem_wait_st();
       fence_before_sync();
-      fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_free[g]);
-        mbar_arrive(&ds_full[g]);
-      }
+      if (lane == 0) mbar_arrive(&ds_full[g]);
     }
     mbar_wait(acc_done, 0);
     fence_after_sync();
