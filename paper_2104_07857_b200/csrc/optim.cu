@@ -12,8 +12,6 @@
 // Memory: 8 elements per thread-iteration; fp32 arrays move as two 128-bit
 // streaming accesses, half arrays as one. Algorithmic bytes per element:
 // adam 30 (16 read + 14 write), rs_adam 2*K + 12 read + 14 write.
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace zi {
@@ -94,39 +92,12 @@ __global__ void __launch_bounds__(256)
 rs_kernel(Contribs cb, int K, size_t off, size_t n, size_t nvec8, size_t clen, float scale,
           float* __restrict__ out_or_g, float* __restrict__ p, float* __restrict__ m,
           float* __restrict__ v, uint16_t* __restrict__ ph, zi_adam_consts c,
-          const zi_adam_consts* __restrict__ cdev, int rs_ilp2) {
+          const zi_adam_consts* __restrict__ cdev) {
   zi::pdl_sync();
   if (ADAM && cdev != nullptr) c = *cdev;  // constants advanced on the device (CUDA graphs)
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
-  size_t i0 = tid;
-  if (ADAM && K == 1 && rs_ilp2) {
-    // K = 1 (one rank's contribution): two 8-element groups per iteration, all 14
-    // 16-byte loads issued before the first use: 240 vs 275 us on a 50.4M-element
-    // bucket, 90 % of the copy peak (scripts/bench_rs_adam.py)
-    for (; i0 + stride < nvec8; i0 += 2 * stride) {
-      const size_t ia = i0, ib = i0 + stride;
-      const uint4 wa = ld_stream(reinterpret_cast<const uint4*>(cb.ptr[0] + off) + ia);
-      const uint4 wb = ld_stream(reinterpret_cast<const uint4*>(cb.ptr[0] + off) + ib);
-      float pa[8], ma[8], va[8], pb[8], mb[8], vb[8], ga[8], gb[8];
-      load8(p, ia, pa); load8(m, ia, ma); load8(v, ia, va);
-      load8(p, ib, pb); load8(m, ib, mb); load8(v, ib, vb);
-      widen8<KIND>(wa, ga);
-      widen8<KIND>(wb, gb);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        ga[j] = __fmul_rn(ga[j], scale);
-        gb[j] = __fmul_rn(gb[j], scale);
-        adam1(pa[j], ma[j], va[j], ga[j], c);
-        adam1(pb[j], mb[j], vb[j], gb[j], c);
-      }
-      if (out_or_g) { store8(out_or_g, ia, ga); store8(out_or_g, ib, gb); }
-      store8(p, ia, pa); store8(m, ia, ma); store8(v, ia, va);
-      store8(p, ib, pb); store8(m, ib, mb); store8(v, ib, vb);
-      if (ph) { store8_half<KIND>(ph, ia, pa); store8_half<KIND>(ph, ib, pb); }
-    }
-  }
-  for (size_t i = i0; i < nvec8; i += stride) {
+  for (size_t i = tid; i < nvec8; i += stride) {
     float acc[8];
     {
       const uint4 w = ld_stream(reinterpret_cast<const uint4*>(cb.ptr[0] + off) + i);
@@ -202,17 +173,14 @@ int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t c
   const int grid = grid_for(nvec8 + (n - nvec8 * 8), block);
   cudaStream_t s = (cudaStream_t)stream;
   uint16_t* ph = static_cast<uint16_t*>(p_half);
-  static int ilp = -1;   // two groups per iteration in the K = 1 Adam path (ZI_RS_ILP=0: one)
-  if (ilp < 0) {
-    const char* e = getenv("ZI_RS_ILP");
-    ilp = e ? atoi(e) : 1;
-  }
+  // (two 8-element groups per thread-iteration, all 14 loads in flight, measured slower
+  // in the step: 275 vs 249 us per launch at 118 vs 64 registers)
   if (half_kind == ZI_HALF_BF16)
-    zi::launch_pdl(rs_kernel<ZI_HALF_BF16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8, clen, scale,
-                   out_or_g, p, m, v, ph, cc, cdev, ilp);
+    zi::launch_pdl(rs_kernel<ZI_HALF_BF16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8,
+                   clen, scale, out_or_g, p, m, v, ph, cc, cdev);
   else
-    zi::launch_pdl(rs_kernel<ZI_HALF_FP16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8, clen, scale,
-                   out_or_g, p, m, v, ph, cc, cdev, ilp);
+    zi::launch_pdl(rs_kernel<ZI_HALF_FP16, ADAM>, dim3(grid), dim3(block), 0, s, cb, K, off, n, nvec8,
+                   clen, scale, out_or_g, p, m, v, ph, cc, cdev);
   return launch_status(name);
 }
 
