@@ -578,7 +578,7 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
       fence_after_sync();
       if (elect_one()) {
         mma_tile_ts<128, 8>(tmem + 256 + x * 128, tmem + x * 128, sV + st * TB, id_o, j > 0);
-        umma_commit(&pv_done[x]);
+        if (j == nkv_a - 1 + x) umma_commit(&pv_done[x]);   // the tile's last PV: O final
         if (x == 1) umma_commit(&v_empty[st]);
       }
       __syncwarp();
@@ -673,7 +673,7 @@ fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ 
       if (gf) gf[j * 4 + 3] = clock64();
     }
     if (tr && x == 1 && warp == 6 && lane == 0) tr[4] = gtimer();
-    mbar_wait(&pv_done[x], (nkv - 1) & 1);
+    mbar_wait(&pv_done[x], 0);                     // committed once, after the last PV
     fence_after_sync();
     const float inv = 1.f / l;
     const size_t row = (size_t)row0 + qi * 128 + r;
