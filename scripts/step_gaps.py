@@ -25,15 +25,19 @@ ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUD
 iv = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev if e.time_range.end > e.time_range.start)
 t0, t1 = iv[0][0], max(e for _, e, _ in iv)
 union, cur_s, cur_e = 0.0, None, None
-gaps = []
-for s, e, _ in iv:
+gaps, where = [], []
+prev_name = None
+for s, e, n in iv:
     if cur_e is None or s > cur_e:
         if cur_e is not None:
             union += cur_e - cur_s
             gaps.append(s - cur_e)
+            where.append((s - cur_e, prev_name, n, s - t0))
         cur_s, cur_e = s, e
     else:
         cur_e = max(cur_e, e)
+    if e >= cur_e:
+        prev_name = n
 union += cur_e - cur_s
 tot = sum(e - s for s, e, _ in iv)
 by = {}
@@ -47,3 +51,5 @@ print(json.dumps({"span_ms": round((t1 - t0) / 1e3 / 2, 3), "busy_union_ms": rou
                   "gaps_over_5us": sum(1 for g in gaps if g > 5) // 2}))
 for k, v in top:
     print(f"{v / 1e3 / 2:8.3f} ms  {k}")
+for g, a, b, at in sorted(where, key=lambda w: -w[0])[:6]:
+    print(f"gap {g:8.1f} us at {at / 1e3:8.3f} ms: after {str(a)[:50]} | before {str(b)[:50]}")

@@ -134,6 +134,13 @@ def test_1p3b_block_shape_matches_oracle():
     run_vs_oracle(c, 1, 1, 1e-4, (1e-4, 3e-2, 2e-2, 0.25))
 
 
+def test_two_q_tile_attention_steps_match_oracle():
+    """S = 256 runs the two-Q-tile attention forward (and the TMEM-resident P^T / dS^T / dS
+    backward) inside the step: 3 partitioned steps at world 2 against the oracle."""
+    c = eg.GPTConfig(nl=2, hd=256, heads=2, seq=256, vocab=512, batch=2)
+    run_vs_oracle(c, 2, 3, 1e-3, TOL_BF16)
+
+
 @pytest.mark.parametrize("world", [1, 2])
 def test_cuda_graph_step_matches_eager(world):
     """The captured step replays the same math: device Adam counter + static inputs."""
