@@ -26,14 +26,23 @@ __global__ void count_kernel(const int64_t* __restrict__ tok, int T, int V, int*
   }
 }
 
-// exclusive scan of counts[0..V) into offsets[0..V] (offsets[V] = T); one CTA of 1024
-__global__ void scan_kernel(const int* __restrict__ counts, int V, int* __restrict__ offsets) {
+// exclusive scan of counts[0..V) into offsets[0..V] (offsets[V] = T); one CTA of 1024.
+// Each thread's contiguous range is read 8 counts at a time, the 8 loads in flight together
+// (not one dependent L2 round trip per element).
+__global__ void __launch_bounds__(1024)
+scan_kernel(const int* __restrict__ counts, int V, int* __restrict__ offsets) {
   zi::pdl_sync();
   __shared__ int part[1024];
   const int tid = threadIdx.x, per = (V + 1023) / 1024;
   const int lo = min(V, tid * per), hi = min(V, lo + per);
   int s = 0;
-  for (int i = lo; i < hi; ++i) s += counts[i];
+  for (int i = lo; i < hi; i += 8) {
+    int c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = i + k < hi ? counts[i + k] : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k];
+  }
   part[tid] = s;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {           // Hillis-Steele inclusive scan
@@ -43,33 +52,52 @@ __global__ void scan_kernel(const int* __restrict__ counts, int V, int* __restri
     __syncthreads();
   }
   int run = tid ? part[tid - 1] : 0;
-  for (int i = lo; i < hi; ++i) {
-    offsets[i] = run;
-    run += counts[i];
+  for (int i = lo; i < hi; i += 8) {
+    int c[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c[k] = i + k < hi ? counts[i + k] : 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i + k < hi) offsets[i + k] = run;
+      run += c[k];
+    }
   }
   if (tid == 1023) offsets[V] = part[1023];
 }
 
-// stable placement; earlier tokens stream through shared memory in tiles of int32 ids
-constexpr int PLACE_TILE = 8192;
+// stable placement; earlier tokens stream through shared memory in tiles of int32 ids.
+// A CTA of 256 threads places 64 tokens, 4 threads per token each counting the equal ids
+// in one quarter of the earlier range (integer sums: order-free), so T / 64 CTAs share
+// the O(T^2 / 2) comparisons.
+constexpr int PLACE_TILE = 8192, PLACE_TOK = 64, PLACE_SPLIT = 4;
 
-__global__ void place_kernel(const int64_t* __restrict__ tok, int T, int V,
-                             const int* __restrict__ offsets, int* __restrict__ order) {
+__global__ void __launch_bounds__(PLACE_TOK * PLACE_SPLIT)
+place_kernel(const int64_t* __restrict__ tok, int T, int V, const int* __restrict__ offsets,
+             int* __restrict__ order) {
   zi::pdl_sync();
   __shared__ int st[PLACE_TILE];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ int cnt[PLACE_SPLIT][PLACE_TOK];
+  const int j = threadIdx.x % PLACE_TOK, q = threadIdx.x / PLACE_TOK;
+  const int t = blockIdx.x * PLACE_TOK + j;
   const int v = t < T ? (int)tok[t] : -1;
-  const int tmax = min(T, (int)((blockIdx.x + 1) * blockDim.x));   // the block's last t + 1
+  const int tmax = min(T, (int)((blockIdx.x + 1) * PLACE_TOK));   // the block's last t + 1
   int rank = 0;
   for (int k0 = 0; k0 < tmax; k0 += PLACE_TILE) {
     const int n = min(PLACE_TILE, T - k0);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) st[i] = (int)tok[k0 + i];
     __syncthreads();
-    const int kend = min(n, t - k0);
-    for (int k = 0; k < kend; ++k) rank += (st[k] == v);
+    const int kend = max(0, min(n, t - k0));
+    const int qlen = (kend + PLACE_SPLIT - 1) / PLACE_SPLIT;
+    const int a = min(kend, q * qlen), b = min(kend, a + qlen);
+    for (int k = a; k < b; ++k) rank += (st[k] == v);
   }
-  if (t < T && v >= 0 && v < V) order[offsets[v] + rank] = t;
+  cnt[q][j] = rank;
+  __syncthreads();
+  if (q == 0) {
+    rank = cnt[0][j] + cnt[1][j] + cnt[2][j] + cnt[3][j];
+    if (t < T && v >= 0 && v < V) order[offsets[v] + rank] = t;
+  }
 }
 
 __device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
@@ -137,7 +165,8 @@ int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, cons
   ZI_CUDA(cudaMemsetAsync(counts, 0, (size_t)V * sizeof(int), s), "zi_embed_grad: memset");
   zi::launch_pdl(zi::emb::count_kernel, dim3((T + 255) / 256), dim3(256), 0, s, tokens, T, V, counts);
   zi::launch_pdl(zi::emb::scan_kernel, dim3(1), dim3(1024), 0, s, counts, V, offsets);
-  zi::launch_pdl(zi::emb::place_kernel, dim3((T + 255) / 256), dim3(256), 0, s, tokens, T, V, offsets, order);
+  zi::launch_pdl(zi::emb::place_kernel, dim3((T + zi::emb::PLACE_TOK - 1) / zi::emb::PLACE_TOK),
+                 dim3(zi::emb::PLACE_TOK * zi::emb::PLACE_SPLIT), 0, s, tokens, T, V, offsets, order);
   const int threads = ((hd / 8 + 31) / 32) * 32;
   auto* o = static_cast<uint16_t*>(out);
   const auto* xb = static_cast<const __nv_bfloat16*>(dx);
