@@ -169,6 +169,10 @@ int zi_bias_grad(const void* dy, const void* u, void* du, void* db, int db_f32, 
 int zi_softmax_ce(void* logits, const int64_t* targets, float* loss_rows, float* loss, int T,
                   int V, float scale, void* stream);
 
+/* Kernels libzinf has launched in this process (every entry point counts its launches,
+ * including launches recorded into a CUDA graph during capture). Diagnostics. */
+long long zi_launch_count(void);
+
 /* ---- offload engine (tier-store host tier, store.py:81-153) -------------- */
 int zi_host_alloc(size_t bytes, void** out);          /* pinned, portable */
 int zi_host_free(void* p);

@@ -138,8 +138,10 @@ SIGNATURES = {
     "zi_attn_bwd_colsum": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
                            c_int, c_int, c_int, c_void_p, c_void_p],
     "zi_gemm_sk_workspace_bytes": [],
+    "zi_launch_count": [],
 }
-_RESTYPE = {"zi_last_error": ctypes.c_char_p, "zi_gemm_sk_workspace_bytes": c_size_t}
+_RESTYPE = {"zi_last_error": ctypes.c_char_p, "zi_gemm_sk_workspace_bytes": c_size_t,
+            "zi_launch_count": ctypes.c_longlong}
 
 _lib = None
 _lock = threading.Lock()
@@ -215,3 +217,8 @@ def adam_consts(lr: float, beta1: float, beta2: float, eps: float, step: int) ->
 
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
+
+
+def launch_count() -> int:
+    """Kernels libzinf has launched in this process (zi_launch_count)."""
+    return int(load().zi_launch_count())

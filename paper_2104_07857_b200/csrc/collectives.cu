@@ -140,6 +140,7 @@ int zi_allgather(const void* const* shards, int world, size_t shard_elems, size_
     zi::gather_elem<uint32_t><<<grid, block, 0, s>>>(t, static_cast<uint32_t*>(full), shard_elems, full_elems);
   } else {
     zi::gather_elem<uint64_t><<<grid, block, 0, s>>>(t, static_cast<uint64_t*>(full), shard_elems, full_elems);
+  zi::count_launches();
   }
   return zi::launch_status("zi_allgather");
 }
@@ -155,6 +156,7 @@ int zi_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void
     f.ptr[k] = flags[k];
   }
   zi::barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, rank, epoch, nullptr);
+  zi::count_launches();
   return zi::launch_status("zi_barrier");
 }
 
@@ -170,6 +172,7 @@ int zi_barrier_dev(uint32_t* const* flags, int world, int rank, uint32_t* epoch_
     f.ptr[k] = flags[k];
   }
   zi::barrier_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, rank, 0u, epoch_ctr);
+  zi::count_launches();
   return zi::launch_status("zi_barrier_dev");
 }
 

@@ -38,6 +38,9 @@ __device__ __forceinline__ void pdl_sync() {
 
 bool pdl_enabled();
 
+// every libzinf kernel launch is counted (zi_launch_count: the engine's launches per step)
+void count_launches(int n = 1);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args&&... args) {
@@ -51,6 +54,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  count_launches();
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

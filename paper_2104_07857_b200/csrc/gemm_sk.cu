@@ -774,6 +774,7 @@ static int launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     at[2].val.preferredClusterDim.z = 1;
     cfg.numAttrs = 3;
   }
+  zi::count_launches();
   ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, md, md2, static_cast<const __nv_bfloat16*>(bias),
                              static_cast<const uint16_t*>(X), ldx, M, N, sc, part, flag, aux),
           "cudaLaunchKernelEx(zi_gemm_sk)");

@@ -1082,6 +1082,7 @@ static int launch(const CUtensorMap& ma, const CUtensorMap& mb, const void* bias
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  zi::count_launches();
   ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mb, static_cast<const __nv_bfloat16*>(bias), D, M, N,
                              K, ldd), "cudaLaunchKernelEx(zi_gemm)");
   return launch_status("zi_gemm");
@@ -1159,6 +1160,7 @@ static int launch_wide_cfg(const CUtensorMap& ma, const CUtensorMap& mb, const v
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  zi::count_launches();
   ZI_CUDA(cudaLaunchKernelEx(&cfg, kern, ma, mbp, md, md2, static_cast<const __nv_bfloat16*>(bias),
                              static_cast<const uint16_t*>(X), ldx, M, N, K, g_prof),
           "cudaLaunchKernelEx(zi_gemm wide)");

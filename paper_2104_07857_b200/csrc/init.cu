@@ -62,6 +62,7 @@ half_to_f32_kernel(const uint16_t* __restrict__ src, float* __restrict__ dst, si
 
 #define ZI_DISPATCH_HALF(kind, KERNEL, ...)                                 \
   do {                                                                     \
+    zi::count_launches();                                                   \
     if ((kind) == ZI_HALF_BF16) KERNEL<ZI_HALF_BF16><<<grid, 256, 0, s>>>(__VA_ARGS__); \
     else KERNEL<ZI_HALF_FP16><<<grid, 256, 0, s>>>(__VA_ARGS__);           \
   } while (0)

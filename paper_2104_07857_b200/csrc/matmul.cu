@@ -49,6 +49,7 @@ int zi_matmul_fixed(const void* A, int64_t sam, int64_t sak, const void* B, int6
   const int64_t total = (int64_t)M * N;
   const int grid = (int)((total + 255) / 256);
   cudaStream_t s = (cudaStream_t)stream;
+  zi::count_launches();
   if (dtype == ZI_DT_F32)
     zi::matmul_fixed_kernel<float><<<grid, 256, 0, s>>>(
         (const float*)A, sam, sak, (const float*)B, sbk, sbn, (const float*)bias, (float*)C, scm,

@@ -2,6 +2,7 @@
 // Host tier of the offload engine (reference BufferPool / IoTicket,
 // store.py:81-153): pinned cudaHostAlloc buffers + copy-engine transfers;
 // tickets are CUDA events.
+#include <atomic>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
@@ -12,6 +13,9 @@
 namespace zi {
 
 static thread_local char g_err[1024] = "";
+
+static std::atomic<long long> g_launch_count{0};
+void count_launches(int n) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
 
 bool pdl_enabled() {   // ZI_PDL=0: plain stream serialisation (A/B)
   static int v = -1;
@@ -39,6 +43,9 @@ int cuda_status(cudaError_t e, const char* what) {
 }  // namespace zi
 
 extern "C" {
+
+long long zi_launch_count(void) { return zi::g_launch_count.load(std::memory_order_relaxed); }
+
 
 const char* zi_last_error(void) { return zi::g_err; }
 

@@ -79,6 +79,7 @@ int zi_linear_tile_bwd(const void* x, int ldx, const void* w_t, int ldw, const v
     if (st) return st;
   }
   if (db_t) {
+    zi::count_launches();
     zi::tile_colsum_kernel<<<(N_t + 63) / 64, 256, 0, (cudaStream_t)stream>>>(
         (const __nv_bfloat16*)dy_t, M, N_t, lddy, db_t);
     return zi::launch_status("zi_linear_tile_bwd(db)");

@@ -656,17 +656,14 @@ class GPTZeroEngine:
                 self.comm.device_barrier(stream, channel=1)
                 kernels.allgather(self.peer_pstage[k], b.shard, dst, b.numel,
                                   use_copy_engine=self.copy_engine_gather)
-                self.launches += 1
             else:
                 base = b.arena_off * self.p16.element_size()
                 ptrs = [p + base for p in self.peer_p16]
                 kernels.allgather(ptrs, b.shard, dst, b.numel,
                                   use_copy_engine=self.copy_engine_gather)
-            self.launches += 1
             if self.cdt != self.half:
                 wide = self.wide_embed if b.key == "embed" else self.wide_slots[slot]
                 kernels.cast_half_to_f32(dst[:b.numel], wide[:b.numel])
-                self.launches += 1
             self._tspan(b.op, "cg" if (self.host_params and not staged) else "gg",
                         t0, self._tmark(stream))
             ev = torch.cuda.Event()
@@ -825,7 +822,6 @@ class GPTZeroEngine:
             o = torch.empty(B * S, c.hd, dtype=qkv.dtype, device=qkv.device)
             lse = torch.empty(B * H * S, dtype=torch.float32, device=qkv.device)
             kernels.attn_fwd(qkv, o, lse, B, H)
-            self.launches += 1
             return o, (qkv, o, lse)
         leaf = qkv.detach().requires_grad_(True)
         with torch.enable_grad():
@@ -847,7 +843,6 @@ class GPTZeroEngine:
                 delta = torch.empty_like(lse)
             kernels.attn_bwd(qkv, None if given else o, do, lse, delta, dqkv, c.batch, c.heads,
                              colsum=colsum)
-            self.launches += 2 if given else 3
             return dqkv
         leaf, o4 = saved
         g4 = do.view(c.batch, c.seq, c.heads, c.head_dim).transpose(1, 2)
@@ -877,7 +872,6 @@ class GPTZeroEngine:
         rstd = torch.empty(T, dtype=torch.float32, device=x.device)
         xs = torch.empty_like(x) if resid is not None else None
         kernels.ln_fwd(x, w, b, y, mean, rstd, LN_EPS, resid=resid, xsum=xs)
-        self.launches += 1
         return xs, y, mean, rstd
 
     def _block_fwd(self, x, P):
@@ -912,7 +906,6 @@ class GPTZeroEngine:
             out = torch.empty(x.shape[0], w.shape[0], dtype=x.dtype, device=x.device)
         if self._zi(site, x, w, b, out):
             kernels.gemm_sk(x, w, out, bias=b)
-            self.launches += 1
         else:
             torch.addmm(b, x, w.t(), out=out)
         return out
@@ -921,7 +914,6 @@ class GPTZeroEngine:
         """out = dy^T inp (a weight gradient, written into its grad-bucket view)."""
         if self._zi(site, dy, inp, out):
             kernels.gemm_sk(dy.t(), inp.t(), out)
-            self.launches += 1
         elif out.dtype == dy.dtype:
             torch.mm(dy.t(), inp, out=out)
         else:
@@ -933,7 +925,6 @@ class GPTZeroEngine:
         out = torch.empty(dy.shape[0], w.shape[1], dtype=dy.dtype, device=dy.device)
         if self._zi(site, dy, w, out):
             kernels.gemm_sk(dy, w.t(), out)
-            self.launches += 1
         else:
             torch.mm(dy, w, out=out)
         return out
@@ -963,11 +954,9 @@ class GPTZeroEngine:
         y = torch.empty_like(x2)
         if self._zi("fc2.fwd", a, P["fc2_w"], P["fc2_b"], y, x2):
             kernels.gemm_sk(a, P["fc2_w"], y, bias=P["fc2_b"], epi="resid", x=x2)
-            self.launches += 1
         else:
             torch.addmm(P["fc2_b"], a, P["fc2_w"].t(), out=y)
             y += x2
-        self.launches += 1
         return y, (x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a)
 
     def _block_bwd_fused(self, dy, cache, P, G):
@@ -987,11 +976,9 @@ class GPTZeroEngine:
             kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="mul" if self._gelu_save() else "dgelu",
                             x=u, colsum=part)
             kernels.colsum_fold(part, -(-T // 32), H4, G["fc1_b"])
-            self.launches += 1
         elif self._zi("fc2.dx", dy, P["fc2_w"], du, u):   # A/B: separate bias pass
             kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
             kernels.bias_grad(du, G["fc1_b"], ws)
-            self.launches += 1
         else:
             da = torch.mm(dy, P["fc2_w"])
             kernels.bias_grad(da, G["fc1_b"], ws, u=u, du=du)
@@ -1012,7 +999,6 @@ class GPTZeroEngine:
             delta = torch.empty(c.batch * c.heads * c.seq, dtype=torch.float32, device=dx2.device)
             kernels.gemm_sk(dx2, P["proj_w"].t(), do, x=o, delta=delta,
                             delta_shape=(c.seq, c.heads, c.head_dim))
-            self.launches += 1
             # the attention backward's epilogues also sum dqkv's columns per 32-row block:
             # the qkv bias gradient is one small fold instead of a pass over dqkv
             dqkv_cols = 3 * c.hd
@@ -1020,7 +1006,6 @@ class GPTZeroEngine:
             dqkv = self._attn_bwd(do, att, delta=delta, colsum=part)
             self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
             kernels.colsum_fold(part, c.tokens // 32, dqkv_cols, G["qkv_b"])
-            self.launches += 1
         else:
             do = self._mm_dx("proj.dx", dx2, P["proj_w"])
             dqkv = self._attn_bwd(do, att)
@@ -1031,7 +1016,6 @@ class GPTZeroEngine:
         # ... and LN1 backward sums dres = dx2: the proj bias gradient
         kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2,
                        dres_sum=G["proj_b"])
-        self.launches += 8
         return dx
 
     def _block_bwd(self, dy, cache, P, G):
@@ -1099,7 +1083,6 @@ class GPTZeroEngine:
         logits = torch.empty(hf.shape[0], PE["wte"].shape[0], dtype=hf.dtype, device=hf.device)
         if self._zi("head.fwd", hf, PE["wte"], logits):
             kernels.gemm_sk(hf, PE["wte"], logits)
-            self.launches += 1
         else:
             torch.mm(hf, PE["wte"].t(), out=logits)
         tgt = targets.reshape(-1)
@@ -1113,7 +1096,6 @@ class GPTZeroEngine:
         del logits, dlog
         dx = torch.empty_like(dhf)
         kernels.ln_bwd(dhf, x, PF["lnf_w"], mf, rf, dx, G["lnf_w"], G["lnf_b"], self.ws)
-        self.launches += 2
         return loss, dx
 
     # ------------------------------------------------------------------- reduce
@@ -1133,7 +1115,6 @@ class GPTZeroEngine:
         dst = self._contrib(li, b, slot)
         if flat.data_ptr() != dst.data_ptr():
             kernels.cast_f32_to_half(flat[:b.numel].contiguous(), dst[:b.numel])
-            self.launches += 1
         if b.shard * self.N > b.numel:
             dst[b.numel:b.shard * self.N].zero_()
 
@@ -1156,7 +1137,6 @@ class GPTZeroEngine:
             contribs = [self._contrib(li, b, slot) for li in range(len(self.ranks))]
         else:
             self.comm.device_barrier(os_, channel=2)
-            self.launches += 1
             if self._pending_free is not None:   # peers are done with the previous slot
                 ev = torch.cuda.Event()
                 ev.record(os_)
@@ -1188,7 +1168,6 @@ class GPTZeroEngine:
                                    self.adam, g_out=self._gout(li, b))
                 if host_params:  # updated bf16 shard back to its pinned home (D2H)
                     p16.copy_(ph, non_blocking=True)
-                self.launches += 1
             self._tspan(b.op, "reduce_scatter", t0, self._tmark(os_))
             if self.comm.is_local and os_ is not cur:
                 ev = torch.cuda.Event()
@@ -1257,7 +1236,6 @@ class GPTZeroEngine:
                 go = gouts[li]
                 kernels.rs_adam_dc(contribs, r * L + s, n, b.numel, scale, sp, sm, sv, ph,
                                    self.adam, g_out=go[s:s + n] if go is not None else None)
-                self.launches += 1
                 ev_c = torch.cuda.Event()
                 ev_c.record(opt)
             if host_params:   # bf16 write-back on its own lane: the next fetch waits on it only
@@ -1378,19 +1356,24 @@ class GPTZeroEngine:
     def step(self, batches) -> torch.Tensor:
         """One partitioned training step; ``batches[li] = (tokens, targets)``
         (int64 [batch, seq] CUDA tensors) for each local rank. Returns the
-        mean loss over all ranks as a 0-d fp32 CUDA tensor."""
+        mean loss over all ranks as a 0-d fp32 CUDA tensor. ``self.launches`` counts the
+        libzinf kernels the step launched (the library's own counter, zi_launch_count)."""
+        n0 = _lib.launch_count()
+        loss = self._step(batches)
+        self.launches += _lib.launch_count() - n0
+        return loss
+
+    def _step(self, batches) -> torch.Tensor:
         c = self.cfg
         self.t += 1
         consts = None                 # Adam constants live on the device (self.adam)
         self.grad_shards = {}
         cur = torch.cuda.current_stream()
         self.adam.advance()           # t += 1 and this step's bias corrections, on the GPU
-        self.launches += 1
         gs = self.gather_stream if self.prefetch else cur
         nloc = len(self.ranks)
         if not self.comm.is_local and self.N > 1:
             self.comm.device_barrier()  # peers' previous-step Adam writes are done
-            self.launches += 1
         if self.offload:
             # the cg lane follows this step's start (under capture: joins the graph)
             self.h2d_stream.wait_stream(cur)
@@ -1537,12 +1520,10 @@ class GPTZeroEngine:
                 kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], wte16, self.emb_work)
                 kernels.cast_half_to_f32(wte16.view(-1), G["wte"].view(-1))
                 G["wpe"].copy_(dwpe)
-                self.launches += 2
             else:  # fp32 accumulators -> RNE half contributions
                 kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], G["wte"],
                                    self.emb_work)
                 kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
-                self.launches += 5
             self._finish_grad(li, E, 0, flat)
         self._tspan(E.op, "compute", c0, self._tmark(cur))
         self._reduce_update(E, 0, consts)
