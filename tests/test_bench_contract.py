@@ -7,6 +7,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -32,3 +34,31 @@ def test_reference_arm_other_ranks_exit_quietly():
                         "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
                        timeout=120, cwd=ROOT, env=env)
     assert r.returncode == 0 and not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+@pytest.mark.gpu
+def test_main_arm_json_line():
+    """The product arm on the GPU (short run, no offload legs / CPU sample): the driver's
+    keys, a tensor roofline of zi_gemm_sk and the HBM roofline of the fused RS + Adam,
+    e2e with the step's host transfers counted, and a positive launch count."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3",
+                        "--warmup", "3", "--no-offload", "--no-cpu"], capture_output=True,
+                       text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "data", "config", "e2e", "gpu_launches",
+              "roofline", "roofline_hbm", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["value"] > 0
+    assert d["gpu_launches"] > 0 and d["gpu_launches"] % 3 == 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    roof = d["roofline"]
+    assert roof["bound"] == "tensor" and roof["unit"] == "TFLOP/s", roof
+    assert 0 < roof["frac"] < 1.3 and roof["launches_per_step"] > 0
+    assert roof["flops_per_step"] > 0.9 * 64e12    # the 1.3B step's GEMM flops (64.4 TF)
+    hb = d["roofline_hbm"]
+    assert hb["bound"] == "hbm" and 0 < hb["frac"] < 1.05
