@@ -67,6 +67,9 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        import threading
+        self.lines = []
+        first = threading.Event()
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
@@ -74,6 +77,18 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:  # noqa: BLE001
             self.proc = None
+            return self
+
+        def read():
+            for line in self.proc.stdout:
+                self.lines.append(line)
+                first.set()
+
+        self.reader = threading.Thread(target=read, daemon=True)
+        self.reader.start()
+        # nvidia-smi takes a few hundred ms to start on some boxes: the timed region
+        # begins only once it is sampling
+        first.wait(timeout=5.0)
         return self
 
     def __exit__(self, *exc):
@@ -82,9 +97,11 @@ class ClockSampler:
             time.sleep(0.25)
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:  # noqa: BLE001
                 self.proc.kill()
+            self.reader.join(timeout=5)
+            self.out = "".join(self.lines)
         return False
 
     def summary(self):
@@ -1244,7 +1261,7 @@ def main():
     ap.add_argument("--no-nvme", action="store_true", help="skip the NVMe optimizer-state leg")
     ap.add_argument("--nvme-dir", default=None, help="directory for the NVMe leg's shard files")
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
