@@ -19,7 +19,7 @@
 //   * two 256-column fp32 accumulators in TMEM, so the epilogue of item j runs while
 //     the MMA works on item j + 1;
 //   * hybrid stream-K schedule: with P pairs and T tiles of nk k-blocks, the first S
-//     tiles (S = P + T mod P, or all T when T < P) are cut into S*nk k-block units
+//     tiles (S = T mod P, or all T when T < P) are cut into S*nk k-block units
 //     dealt out evenly, unit range [q*U/P, (q+1)*U/P) to pair q; the remaining T - S
 //     tiles (a multiple of P) are whole tiles round-robin. Every pair does the same
 //     work to within one k-block;
@@ -676,12 +676,21 @@ static Sched make_sched(int M, int N, int K, int clusters, int CL, bool split) {
   // (the tied head's dx, K = 50304) the extra DRAM reads cost more than the wave
   // quantization they remove.
   if (s.nk > 256 || s.T < clusters) split = false;
+  // Stream-K over the last partial wave only (S = T mod P tiles, each cut across ~2-3
+  // pairs) rather than P + T mod P tiles (each pair ~1.5 tiles): fewer tiles run at
+  // staggered k offsets. In the 1.3B step +0.35 % (3 of 3 same-box interleaved rounds,
+  // profiles/r2_gemm_power.md); ZI_SK_TAIL=0 restores P + T mod P.
+  static int sk_tail = -1;
+  if (sk_tail < 0) {
+    const char* e = getenv("ZI_SK_TAIL");
+    sk_tail = e ? atoi(e) : 1;
+  }
   if (!split || s.T % clusters == 0) {
     s.P = s.T < clusters ? s.T : clusters;
     s.S = 0;
   } else {
     s.P = clusters;
-    s.S = s.T < clusters ? s.T : clusters + s.T % clusters;
+    s.S = s.T < clusters ? s.T : (sk_tail ? 0 : clusters) + s.T % clusters;
   }
   return s;
 }
