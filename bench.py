@@ -464,8 +464,10 @@ def run_ours(args):
     # the step). Separate from the headline: the step is re-captured with CUDA events
     # around each GEMM launch (event nodes cost the GEMMs their PDL overlap, so this
     # under-states them slightly), replayed `gsteps` times; 2*M*N*K flops per launch.
+    # N=1 only: the re-capture runs host barriers across ranks, and an error on one rank
+    # inside it would leave the others waiting; at N>1 `roofline` is the RS + Adam kernel.
     gemm_roof = None
-    if not args.no_graph:
+    if not args.no_graph and world == 1:
         try:
             gemm_roof = gemm_roofline(eng, step, dev_batches, tc, min(args.steps, 5))
         except Exception as e:  # noqa: BLE001 — report, never lose the main line
@@ -569,7 +571,8 @@ def run_ours(args):
             line["roofline"] = gemm_roof
         else:
             line["roofline"] = line["roofline_hbm"]
-            line["roofline_gemm_error"] = gemm_roof
+            if gemm_roof is not None:
+                line["roofline_gemm_error"] = gemm_roof
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
