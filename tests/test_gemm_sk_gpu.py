@@ -50,13 +50,17 @@ def operands(kind, M, N, K, seed):
     return dy.t(), x.t()
 
 
+# (cluster tiles of 256 x 512 on 37 preferred clusters of 4; stream-K over the T mod 37
+# tiles of the last partial wave)
 SHAPES = [
     (256, 256, 64),        # one tile
     (300, 520, 200),       # ragged M / N / K
-    (2048, 2048, 8192),    # 64 tiles < 74 pairs: every tile split
-    (8192, 2048, 2048),    # 256 tiles: 2 whole waves + stream-K region
-    (1000, 4104, 1024),    # ragged, split
-    (8192, 6144, 2048),    # qkv
+    (2048, 2048, 8192),    # 32 tiles < 37 clusters: whole tiles
+    (8192, 2048, 2048),    # 128 tiles: 3 whole waves + 17 tiles cut across 2-3 clusters
+    (1000, 4104, 1024),    # ragged
+    (8192, 6144, 2048),    # qkv: 384 tiles, 14 cut
+    (8192, 2048, 128),     # 17 cut tiles x 2 k-blocks over 37 clusters: empty ranges
+    (4096, 4608, 64),      # one k-block: 33 tail tiles, whole, 4 clusters idle
 ]
 
 
