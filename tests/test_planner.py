@@ -124,3 +124,35 @@ def test_cli_plan(capsys):
     assert cli.main(["plan", "--profile", "dgx2", "--nl", "128", "--hd", "25600"]) == 0
     out = capsys.readouterr().out.splitlines()
     assert out[1].startswith("strategy,fits") and out[2].startswith("ZeroInfNvme,1,")
+
+
+# --------------------------------------------------------------- pinned to the reference
+def _planner_ref():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "planner_ref.json")) as f:
+        return json.load(f)
+
+
+def test_formulas_match_reference_memory_and_efficiency():
+    """Every sizing / bandwidth formula the planner restates equals the reference's own
+    output (infinisim memory.py:83-121, efficiency.py:38-90) on 560 shapes, recorded by
+    tests/golden/make_planner_golden.py."""
+    g = _planner_ref()
+    assert P.STATE_BYTES == g["model_state_bytes_per_param"]
+    for row in g["shapes"]:
+        s = P.ModelShape(**row["shape"])
+        assert s.params == row["params"], row["shape"]
+        assert P.STATE_BYTES * s.params == row["model_state_bytes"]
+        assert P.mswm_bytes(s.hd) == row["mswm_bytes"]
+        assert math.ceil(P.awm_bytes(s)) == row["awm_bytes"], row["shape"]
+        for k in P.AitKind:
+            assert P.ait(k, s) == row["ait"][k.value], (row["shape"], k)
+            # the AIT definition: iteration flops over the category's bytes moved
+            assert row["flops_per_iter"] == 8 * s.bsz * s.seq * s.params
+    for e in g["efficiency"]:
+        bw = math.inf if e["bw"] == "inf" else e["bw"]
+        assert P.efficiency(e["ait"], bw, e["peak"]) == e["eff"], e
+    for r in g["required_bandwidth"]:
+        assert P.required_bandwidth(r["ait"], r["peak"], r["target"]) == pytest.approx(
+            r["bw"], rel=1e-15), r
