@@ -378,6 +378,18 @@ int zi_attn_bwd_colsum(const void* qkv, const void* out, const void* dout, const
  * [2*V + 1 + T]. Deterministic: counting sort with stable ranks, no float atomics. */
 int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, const float* acc, int V,
                   int hd, void* out, int half_kind, int* work, void* stream);
+/* Embedding lookup of the GPT forward (csrc/embed.cu), replacing torch's
+ * F.embedding(tokens, wte) + wpe (the train_step forward): x[t] =
+ * bf16_RNE(wte[tokens[t]] + wpe[t % S]) summed in fp32. tokens int64 [T]; wte bf16 [V, hd];
+ * wpe bf16 [S, hd]; x bf16 [T, hd]. Ids outside [0, V) contribute no wte row. */
+int zi_embed_fwd(const int64_t* tokens, int T, int S, const void* wte, const void* wpe, int V,
+                 int hd, void* x, void* stream);
+/* Position-embedding gradient in a fixed order: out[s] = sum over b = 0..B-1 (ascending)
+ * of dx[b*S + s] in fp32; dx [B*S, hd] fp32 (dx_kind = -1) or half (ZI_HALF_*); out [S, hd] fp32
+ * (out_kind = -1) or half RNE (ZI_HALF_BF16 / ZI_HALF_FP16) — the wpe gradient
+ * contribution before the reduce-scatter. */
+int zi_pos_grad(const void* dx, int dx_kind, int B, int S, int hd, void* out, int out_kind,
+                void* stream);
 /* Diagnostics: per-CTA globaltimer records of zi_attn_fwd into buf (6 u64 per CTA: sm,
  * entry, operands in, last MMA issued, softmax done, exit); NULL turns it off. */
 int zi_attn_set_trace(void* buf);

@@ -123,6 +123,8 @@ SIGNATURES = {
     "zi_attn_set_trace": [c_void_p],
     "zi_embed_grad": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_int,
                       c_void_p, c_void_p],
+    "zi_embed_fwd": [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p],
+    "zi_pos_grad": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p],
     "zi_attn_fwd": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
     "zi_attn_bwd": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
                     c_int, c_void_p],

@@ -110,6 +110,16 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
     f[2 * q + 1] = x.y;
   }
 }
+__device__ __forceinline__ void load8(const __half* p, float* f) {
+  const uint4 g = *reinterpret_cast<const uint4*>(p);
+  const __half2* g2 = reinterpret_cast<const __half2*>(&g);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 x = __half22float2(g2[q]);
+    f[2 * q] = x.x;
+    f[2 * q + 1] = x.y;
+  }
+}
 __device__ __forceinline__ void load8(const float* p, float* f) {
   const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
@@ -142,6 +152,63 @@ __global__ void rows_kernel(const TX* __restrict__ dx, const float* __restrict__
   o.z = (uint32_t)Half<KIND>::narrow(r[4]) | ((uint32_t)Half<KIND>::narrow(r[5]) << 16);
   o.w = (uint32_t)Half<KIND>::narrow(r[6]) | ((uint32_t)Half<KIND>::narrow(r[7]) << 16);
   *reinterpret_cast<uint4*>(out + base) = o;
+}
+
+// Embedding lookup of the step's forward: x[t, :] = RNE(wte[tokens[t], :] + wpe[t % S, :]),
+// bf16 in and out, the sum in fp32 (torch's bf16 add: F.embedding(tok, wte) + wpe, bit
+// for bit). One thread per 8 consecutive elements of a row; out-of-range ids read no wte
+// row (their x row is wpe alone, like count_kernel skipping them).
+__global__ void __launch_bounds__(256)
+fwd_kernel(const int64_t* __restrict__ tok, int T, int S, const __nv_bfloat16* __restrict__ wte,
+           const __nv_bfloat16* __restrict__ wpe, int V, int hd, uint16_t* __restrict__ x) {
+  zi::pdl_sync();
+  const int per_row = hd / 8;
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)T * per_row) return;
+  const int t = (int)(i / per_row), e = (int)(i % per_row) * 8;
+  const int64_t v = tok[t];
+  float a[8], b[8];
+  load8(wpe + (size_t)(t % S) * hd + e, b);
+  if (v >= 0 && v < V) load8(wte + (size_t)v * hd + e, a);
+  else for (int q = 0; q < 8; ++q) a[q] = 0.f;
+  uint4 o;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    w[q] = (uint32_t)Half<ZI_HALF_BF16>::narrow(a[2 * q] + b[2 * q]) |
+           ((uint32_t)Half<ZI_HALF_BF16>::narrow(a[2 * q + 1] + b[2 * q + 1]) << 16);
+  *reinterpret_cast<uint4*>(x + (size_t)t * hd + e) = o;
+}
+
+// Position-embedding gradient: out[s, :] = sum_{b ascending} dx[b * S + s, :] in fp32,
+// stored as fp32 (OUT = -1) or rounded RNE to half (OUT = half kind). Fixed order.
+template <typename TX, int OUT>
+__global__ void __launch_bounds__(256)
+pos_grad_kernel(const TX* __restrict__ dx, int B, int S, int hd, void* __restrict__ out) {
+  zi::pdl_sync();
+  const int per_row = hd / 8;
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= (size_t)S * per_row) return;
+  const size_t off = (i / per_row) * (size_t)hd + (i % per_row) * 8;
+  float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int b = 0; b < B; ++b) {
+    float f[8];
+    load8(dx + (size_t)b * S * hd + off, f);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] += f[q];
+  }
+  if constexpr (OUT < 0) {
+    float* o = static_cast<float*>(out) + off;
+    *reinterpret_cast<float4*>(o) = make_float4(s[0], s[1], s[2], s[3]);
+    *reinterpret_cast<float4*>(o + 4) = make_float4(s[4], s[5], s[6], s[7]);
+  } else {
+    uint4 o;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      w[q] = (uint32_t)Half<OUT>::narrow(s[2 * q]) | ((uint32_t)Half<OUT>::narrow(s[2 * q + 1]) << 16);
+    *reinterpret_cast<uint4*>(static_cast<uint16_t*>(out) + off) = o;
+  }
 }
 
 }  // namespace emb
@@ -179,6 +246,53 @@ int zi_embed_grad(const int64_t* tokens, int T, const void* dx, int dx_f32, cons
     else zi::launch_pdl(zi::emb::rows_kernel<ZI_HALF_FP16, __nv_bfloat16>, dim3(V), dim3(threads), 0, s, xb, acc, offsets, order, hd, o);
   }
   return zi::launch_status("zi_embed_grad");
+}
+
+int zi_embed_fwd(const int64_t* tokens, int T, int S, const void* wte, const void* wpe, int V,
+                 int hd, void* x, void* stream) {
+  ZI_CHECK_ARG(tokens && wte && wpe && x, "zi_embed_fwd: NULL argument");
+  ZI_CHECK_ARG(T >= 1 && S >= 1 && V >= 1 && hd >= 8 && hd % 8 == 0,
+               "zi_embed_fwd: bad T/S/V/hd %d/%d/%d/%d", T, S, V, hd);
+  ZI_CHECK_ARG(zi::aligned(wte, 16) && zi::aligned(wpe, 16) && zi::aligned(x, 16),
+               "zi_embed_fwd: 16-byte alignment");
+  const size_t n = (size_t)T * (hd / 8);
+  zi::launch_pdl(zi::emb::fwd_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0,
+                 (cudaStream_t)stream, tokens, T, S, static_cast<const __nv_bfloat16*>(wte),
+                 static_cast<const __nv_bfloat16*>(wpe), V, hd, static_cast<uint16_t*>(x));
+  return zi::launch_status("zi_embed_fwd");
+}
+
+int zi_pos_grad(const void* dx, int dx_kind, int B, int S, int hd, void* out, int out_kind,
+                void* stream) {
+  ZI_CHECK_ARG(dx && out, "zi_pos_grad: NULL argument");
+  ZI_CHECK_ARG(B >= 1 && S >= 1 && hd >= 8 && hd % 8 == 0, "zi_pos_grad: bad B/S/hd %d/%d/%d",
+               B, S, hd);
+  ZI_CHECK_ARG(out_kind == -1 || out_kind == ZI_HALF_BF16 || out_kind == ZI_HALF_FP16,
+               "zi_pos_grad: out_kind must be -1 (fp32) or a half kind, got %d", out_kind);
+  ZI_CHECK_ARG(zi::aligned(dx, 16) && zi::aligned(out, 16), "zi_pos_grad: 16-byte alignment");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t n = (size_t)S * (hd / 8);
+  const dim3 g((unsigned)((n + 255) / 256)), b(256);
+  ZI_CHECK_ARG(dx_kind == -1 || dx_kind == ZI_HALF_BF16 || dx_kind == ZI_HALF_FP16,
+               "zi_pos_grad: dx_kind must be -1 (fp32) or a half kind, got %d", dx_kind);
+  const auto* xb = static_cast<const __nv_bfloat16*>(dx);
+  const auto* xh = static_cast<const __half*>(dx);
+  const auto* xf = static_cast<const float*>(dx);
+  using namespace zi::emb;
+  if (dx_kind == ZI_HALF_FP16) {
+    if (out_kind < 0) zi::launch_pdl(pos_grad_kernel<__half, -1>, g, b, 0, s, xh, B, S, hd, out);
+    else if (out_kind == ZI_HALF_BF16) zi::launch_pdl(pos_grad_kernel<__half, ZI_HALF_BF16>, g, b, 0, s, xh, B, S, hd, out);
+    else zi::launch_pdl(pos_grad_kernel<__half, ZI_HALF_FP16>, g, b, 0, s, xh, B, S, hd, out);
+  } else if (dx_kind < 0) {
+    if (out_kind < 0) zi::launch_pdl(pos_grad_kernel<float, -1>, g, b, 0, s, xf, B, S, hd, out);
+    else if (out_kind == ZI_HALF_BF16) zi::launch_pdl(pos_grad_kernel<float, ZI_HALF_BF16>, g, b, 0, s, xf, B, S, hd, out);
+    else zi::launch_pdl(pos_grad_kernel<float, ZI_HALF_FP16>, g, b, 0, s, xf, B, S, hd, out);
+  } else {
+    if (out_kind < 0) zi::launch_pdl(pos_grad_kernel<__nv_bfloat16, -1>, g, b, 0, s, xb, B, S, hd, out);
+    else if (out_kind == ZI_HALF_BF16) zi::launch_pdl(pos_grad_kernel<__nv_bfloat16, ZI_HALF_BF16>, g, b, 0, s, xb, B, S, hd, out);
+    else zi::launch_pdl(pos_grad_kernel<__nv_bfloat16, ZI_HALF_FP16>, g, b, 0, s, xb, B, S, hd, out);
+  }
+  return zi::launch_status("zi_pos_grad");
 }
 
 }  // extern "C"

@@ -809,6 +809,10 @@ class GPTZeroEngine:
     # ------------------------------------------------------------------ compute
     def _embed_fwd(self, P, tokens):
         c = self.cfg
+        if self.fused:   # one libzinf pass: token row + position row, rounded once
+            x = torch.empty(tokens.numel(), c.hd, dtype=P["wte"].dtype, device=self.dev)
+            kernels.embed_fwd(tokens.contiguous(), P["wte"], P["wpe"][: tokens.shape[1]], x)
+            return x
         x = F.embedding(tokens, P["wte"]) + P["wpe"][: tokens.shape[1]]
         return x.reshape(-1, c.hd)
 
@@ -1512,18 +1516,17 @@ class GPTZeroEngine:
         for li in range(nloc):
             G, flat = self._grad_views(li, E, 0)
             tok = batches[li][0].reshape(-1)
-            dwpe = xs[li].view(c.batch, c.seq, c.hd).sum(0, dtype=torch.float32)
             # tied wte: head contribution + the lookup's gradient rows, summed per vocabulary
             # row in sequence order (zi_embed_grad: no float atomics) and rounded to half
             if G["wte"].dtype == torch.float32:
                 wte16 = torch.empty(c.vocab, c.hd, dtype=self.half, device=self.dev)
                 kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], wte16, self.emb_work)
                 kernels.cast_half_to_f32(wte16.view(-1), G["wte"].view(-1))
-                G["wpe"].copy_(dwpe)
             else:  # fp32 accumulators -> RNE half contributions
                 kernels.embed_grad(tok, xs[li].contiguous(), self.wte_acc[li], G["wte"],
                                    self.emb_work)
-                kernels.cast_f32_to_half(dwpe.view(-1), G["wpe"].view(-1))
+            # wpe: fixed-order fp32 batch sum, stored in the gradient's dtype (one pass)
+            kernels.pos_grad(xs[li].contiguous().view(-1, c.hd), c.batch, G["wpe"])
             self._finish_grad(li, E, 0, flat)
         self._tspan(E.op, "compute", c0, self._tmark(cur))
         self._reduce_update(E, 0, consts)

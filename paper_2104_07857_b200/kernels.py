@@ -522,3 +522,28 @@ def embed_grad(tokens: torch.Tensor, dx: torch.Tensor, acc: torch.Tensor, out: t
     _lib.call("zi_embed_grad", _dev(tokens.reshape(-1), "tokens"), T, _dev(dx, "dx"),
               int(dx.dtype == torch.float32), _dev(acc, "acc"), V, hd, _dev(out, "out"),
               half_kind(out.dtype), _dev(work, "work"), _stream(stream))
+
+
+def embed_fwd(tokens: torch.Tensor, wte: torch.Tensor, wpe: torch.Tensor, x: torch.Tensor,
+              stream=None) -> None:
+    """zi_embed_fwd: x[t] = RNE(wte[tokens[t]] + wpe[t % S]) (bf16; torch's
+    F.embedding(tokens, wte) + wpe bit for bit). tokens int64 [B, S] or [T] with S rows of
+    wpe; x bf16 [T, hd]."""
+    S, hd = wpe.shape
+    T = tokens.numel()
+    if tokens.dtype != torch.int64 or x.shape != (T, hd) or wte.shape[1] != hd:
+        raise ValueError("tokens int64 [T]; wte [V, hd], wpe [S, hd], x [T, hd] bf16")
+    _lib.call("zi_embed_fwd", _dev(tokens, "tokens"), T, S, _bf16_2d(wte, "wte"),
+              _bf16_2d(wpe, "wpe"), wte.shape[0], hd, _bf16_2d(x, "x"), _stream(stream))
+
+
+def pos_grad(dx: torch.Tensor, B: int, out: torch.Tensor, stream=None) -> None:
+    """zi_pos_grad: out[s] = sum over b ascending of dx[b*S + s] (fp32 sum), stored fp32 or
+    rounded RNE to out's half dtype."""
+    S, hd = out.shape
+    if dx.shape != (B * S, hd) or dx.dtype not in (torch.bfloat16, torch.float16, torch.float32):
+        raise ValueError("dx bf16 / fp16 / fp32 [B*S, hd]")
+    kind = -1 if out.dtype == torch.float32 else half_kind(out.dtype)
+    dkind = -1 if dx.dtype == torch.float32 else half_kind(dx.dtype)
+    _lib.call("zi_pos_grad", _dev(dx, "dx"), dkind, B, S, hd,
+              _dev(out, "out"), kind, _stream(stream))
