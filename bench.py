@@ -644,7 +644,7 @@ def gemm_roofline(eng, step, batches, peak_tflops, gsteps: int) -> dict:
             "frac_of_burst_peak": round(achieved / burst, 4) if burst else None,
             "algorithmic_bytes_per_step": alg_b,
             "traffic": traffic,
-            "traffic_note": "ncu DRAM read+write per step (profiles/r2_gemm_step_ncu.md) vs the "
+            "traffic_note": "ncu DRAM read+write per step (profiles/r2_gemm_step_ncu_s5.md) vs the "
                             "operand/output bytes: re-reads, but ~2 TB/s average, tensor-bound"}
 
 
