@@ -352,6 +352,23 @@ int zi_gemm_sk_aux(const void* A, int a_mn_major, int lda, const void* B, int b_
                    void* stream);
 /* out[c] = sum over p < P of part[p][c] in p order (fp32 in; bf16 RNE or fp32 out). */
 int zi_colsum_fold(const float* part, int P, int N, void* out, int out_f32, void* stream);
+/* Deferred column folds (csrc/fused.cu). zi_ln_bwd_partials is zi_ln_bwd's row pass
+ * alone: dx, and the per-CTA partials of dgamma, dbeta (and, with dres_sum != 0, of the
+ * column sums of dres) as part fp32 [sets][P][H], P returned in *nparts (sets = 2 or 3).
+ * zi_fold_sets then sums up to ZI_FOLD_MAX_SETS partial sets in one launch, each
+ * out[c] = sum_p part[p * N + c] in the order zi_ln_bwd / zi_colsum_fold use (bitwise the
+ * same results), so a block's four bias / LayerNorm gradient folds cost one launch. */
+#define ZI_FOLD_MAX_SETS 8
+typedef struct zi_fold_set {
+  const float* part;   /* fp32 [P][N] */
+  int P;
+  int N;
+  void* out;           /* [N], bf16 or fp32 (out_f32) */
+} zi_fold_set;
+int zi_ln_bwd_partials(const void* dy, const void* x, const void* w, const float* mean,
+                       const float* rstd, const void* dres, void* dx, int dres_sum, float* part,
+                       size_t part_elems, int T, int H, int* nparts, void* stream);
+int zi_fold_sets(const zi_fold_set* sets, int n, int out_f32, void* stream);
 /* Diagnostics: a device buffer of >= 148*16*8 u64 receiving clock64() stamps of the
  * wide-tile GEMM's pipeline (NULL turns it off). Not for production use. */
 int zi_gemm_set_profile(void* buf);

@@ -123,6 +123,9 @@ SIGNATURES = {
     "zi_attn_set_trace": [c_void_p],
     "zi_embed_grad": [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_int,
                       c_void_p, c_void_p],
+    "zi_ln_bwd_partials": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                           c_int, c_void_p, c_size_t, c_int, c_int, c_void_p, c_void_p],
+    "zi_fold_sets": [c_void_p, c_int, c_int, c_void_p],
     "zi_embed_fwd": [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p],
     "zi_pos_grad": [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p],
     "zi_attn_fwd": [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p],
@@ -196,6 +199,14 @@ def check(status: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+class FoldSetC(ctypes.Structure):
+    """include/zinf.h zi_fold_set."""
+    _fields_ = [("part", c_void_p), ("P", c_int), ("N", c_int), ("out", c_void_p)]
+
+
+FOLD_MAX_SETS = 8
 
 
 def ptr_array(ptrs) -> "ctypes.Array":

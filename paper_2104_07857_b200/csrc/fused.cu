@@ -547,6 +547,38 @@ ln_fold_kernel(const float* __restrict__ part, int P, int H, void* __restrict__ 
   }
 }
 
+// zi_fold_sets: up to ZI_FOLD_MAX_SETS independent folds in one launch (blockIdx.y = set),
+// each exactly ln_fold_kernel's order: FOLD_SUB ordered runs, combined in run order.
+struct FoldSets {
+  zi_fold_set s[ZI_FOLD_MAX_SETS];
+  int out_f32;
+};
+__global__ void __launch_bounds__(32 * FOLD_SUB)
+fold_sets_kernel(const __grid_constant__ FoldSets f) {
+  zi::pdl_sync();
+  __shared__ float sm[FOLD_SUB][33];
+  const zi_fold_set& d = f.s[blockIdx.y];
+  const int lane = threadIdx.x & 31, sub = threadIdx.x >> 5;
+  const int col = blockIdx.x * 32 + lane;
+  if (blockIdx.x * 32 >= d.N) return;            // whole CTA past this set's columns
+  float s = 0.f;
+  if (col < d.N) {
+    const int per = (d.P + FOLD_SUB - 1) / FOLD_SUB, p0 = sub * per, p1 = min(d.P, p0 + per);
+    const float* src = d.part + col;
+#pragma unroll 4
+    for (int p = p0; p < p1; ++p) s += __ldcg(src + (size_t)p * d.N);
+  }
+  sm[sub][lane] = s;
+  __syncthreads();
+  if (sub == 0 && col < d.N) {
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < FOLD_SUB; ++k) t += sm[k][lane];
+    if (f.out_f32) static_cast<float*>(d.out)[col] = t;
+    else static_cast<uint16_t*>(d.out)[col] = tobf(t);
+  }
+}
+
 // y = gelu_tanh(u), 8 bf16 per thread per step (n % 8 == 0), grid-stride.
 __global__ void __launch_bounds__(256)
 gelu_fwd_kernel(const uint16_t* __restrict__ u, uint16_t* __restrict__ y, size_t n8) {
@@ -943,6 +975,47 @@ static int launch_ln_bwd(int grid, cudaStream_t s, bool rsum, const uint16_t* dy
   return launch_ln_bwd3<TPR, false, false>(grid, s, dy, x, w, mean, rstd, dres, dx, part, T);
 }
 
+// The row pass of zi_ln_bwd: dx, and the CTA partials of dgamma / dbeta (/ sum dres)
+// as part[set][P][H]; returns P (the grid) through *nparts.
+static int ln_bwd_rows(const void* dy, const void* x, const void* w, const float* mean,
+                       const float* rstd, const void* dres, void* dx, bool rs, float* part,
+                       size_t part_elems, int T, int H, int* nparts, cudaStream_t s) {
+  ZI_CHECK_ARG(zi::aligned(dy, 16) && zi::aligned(x, 16) && zi::aligned(dx, 16) &&
+               (!dres || zi::aligned(dres, 16)), "zi_ln_bwd: rows must be 16-byte aligned");
+  ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..8192, power of 2");
+  const int tpr = H / 8;
+  const bool split = H >= 2048 && !ln_bwd_legacy();
+  // (256-thread CTAs, two per SM with 96 KB rings, measured 9 % slower than one 512-thread
+  // CTA with a 192 KB ring: 40.6 vs 37.2 us on 8192 x 2048)
+  const int snt = 512;
+  const int rpc = split ? snt * 16 / H : (tpr >= LNB_NT ? 1 : LNB_NT / tpr);
+  int grid = (split ? (snt == 256 ? 2 : 1) : (tpr > LNB_NT ? 1 : 2)) * sm_count();
+  if (grid > (T + rpc - 1) / rpc) grid = (T + rpc - 1) / rpc;
+  const int sets = rs ? 3 : 2;
+  ZI_CHECK_ARG(part_elems >= (size_t)sets * grid * H, "zi_ln_bwd: partials need %zu floats",
+               (size_t)sets * grid * H);
+  auto DY = (const uint16_t*)dy, X = (const uint16_t*)x, W = (const uint16_t*)w,
+       DR = (const uint16_t*)dres;
+  auto DX = (uint16_t*)dx;
+  int st = ZI_OK;
+  if (split) {
+    if (H == 2048) st = launch_ln_split<2048, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else if (H == 4096) st = launch_ln_split<4096, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+    else st = launch_ln_split<8192, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
+  } else switch (tpr) {
+    case 16: st = launch_ln_bwd<16>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 32: st = launch_ln_bwd<32>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 64: st = launch_ln_bwd<64>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 128: st = launch_ln_bwd<128>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 256: st = launch_ln_bwd<256>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 512: st = launch_ln_bwd<512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+    case 1024: st = launch_ln_bwd<1024>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
+  }
+  if (st) return st;
+  *nparts = grid;
+  return zi::launch_status("zi_ln_bwd(dx)");
+}
+
 extern "C" {
 
 int zi_ln_fwd(const void* x, const void* resid, void* xsum, const void* w, const void* b, void* y,
@@ -1041,46 +1114,43 @@ int zi_ln_bwd(const void* dy, const void* x, const void* w, const float* mean, c
               float* work, size_t work_elems, int T, int H, void* stream) {
   ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && dgamma && dbeta && work, "zi_ln_bwd: NULL");
   ZI_CHECK_ARG(!dres_sum || dres, "zi_ln_bwd: dres_sum needs dres");
-  ZI_CHECK_ARG(zi::aligned(dy, 16) && zi::aligned(x, 16) && zi::aligned(dx, 16) &&
-               (!dres || zi::aligned(dres, 16)), "zi_ln_bwd: rows must be 16-byte aligned");
-  ZI_CHECK_ARG(H >= 128 && H <= 8192 && (H & (H - 1)) == 0, "zi_ln_bwd: H must be 128..8192, power of 2");
+  ZI_CHECK_ARG(work_elems > 1024, "zi_ln_bwd: work too small");
   cudaStream_t s = (cudaStream_t)stream;
-  const int tpr = H / 8;
-  const bool split = H >= 2048 && !ln_bwd_legacy();
-  // (256-thread CTAs, two per SM with 96 KB rings, measured 9 % slower than one 512-thread
-  // CTA with a 192 KB ring: 40.6 vs 37.2 us on 8192 x 2048)
-  const int snt = 512;
-  const int rpc = split ? snt * 16 / H : (tpr >= LNB_NT ? 1 : LNB_NT / tpr);
-  int grid = (split ? (snt == 256 ? 2 : 1) : (tpr > LNB_NT ? 1 : 2)) * sm_count();
-  if (grid > (T + rpc - 1) / rpc) grid = (T + rpc - 1) / rpc;
-  const int sets = dres_sum ? 3 : 2;
   // work[0, 1024) holds the column-reduction counters (must stay zero); partials follow
-  ZI_CHECK_ARG(work_elems >= 1024 + (size_t)sets * grid * H, "zi_ln_bwd: work needs %zu floats",
-               1024 + (size_t)sets * grid * H);
   float* part = work + 1024;
-  const bool rs = dres_sum != nullptr;
-  auto DY = (const uint16_t*)dy, X = (const uint16_t*)x, W = (const uint16_t*)w,
-       DR = (const uint16_t*)dres;
-  auto DX = (uint16_t*)dx;
-  int st = ZI_OK;
-  if (split) {
-    if (H == 2048) st = launch_ln_split<2048, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
-    else if (H == 4096) st = launch_ln_split<4096, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
-    else st = launch_ln_split<8192, 512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T);
-  } else switch (tpr) {
-    case 16: st = launch_ln_bwd<16>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 32: st = launch_ln_bwd<32>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 64: st = launch_ln_bwd<64>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 128: st = launch_ln_bwd<128>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 256: st = launch_ln_bwd<256>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 512: st = launch_ln_bwd<512>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-    case 1024: st = launch_ln_bwd<1024>(grid, s, rs, DY, X, W, mean, rstd, DR, DX, part, T); break;
-  }
+  const int sets = dres_sum ? 3 : 2;
+  int grid = 0;
+  int st = ln_bwd_rows(dy, x, w, mean, rstd, dres, dx, dres_sum != nullptr, part, work_elems - 1024,
+                       T, H, &grid, s);
   if (st) return st;
-  if ((st = zi::launch_status("zi_ln_bwd(dx)"))) return st;
   zi::launch_pdl(ln_fold_kernel, dim3(dim3((H + 31) / 32, sets)), dim3(32 * FOLD_SUB), 0, s, part, grid, H, dgamma, dbeta, dres_sum,
                                                           grads_f32);
   return zi::launch_status("zi_ln_bwd(fold)");
+}
+
+int zi_ln_bwd_partials(const void* dy, const void* x, const void* w, const float* mean,
+                       const float* rstd, const void* dres, void* dx, int dres_sum, float* part,
+                       size_t part_elems, int T, int H, int* nparts, void* stream) {
+  ZI_CHECK_ARG(dy && x && w && mean && rstd && dx && part && nparts, "zi_ln_bwd_partials: NULL");
+  ZI_CHECK_ARG(!dres_sum || dres, "zi_ln_bwd_partials: dres_sum needs dres");
+  return ln_bwd_rows(dy, x, w, mean, rstd, dres, dx, dres_sum != 0, part, part_elems, T, H, nparts,
+                     (cudaStream_t)stream);
+}
+
+int zi_fold_sets(const zi_fold_set* sets, int n, int out_f32, void* stream) {
+  ZI_CHECK_ARG(sets && n >= 1 && n <= ZI_FOLD_MAX_SETS, "zi_fold_sets: 1..%d sets", ZI_FOLD_MAX_SETS);
+  FoldSets f = {};
+  int maxn = 0;
+  for (int i = 0; i < n; ++i) {
+    ZI_CHECK_ARG(sets[i].part && sets[i].out && sets[i].P > 0 && sets[i].N > 0,
+                 "zi_fold_sets: bad set %d", i);
+    f.s[i] = sets[i];
+    if (sets[i].N > maxn) maxn = sets[i].N;
+  }
+  f.out_f32 = out_f32;
+  zi::launch_pdl(fold_sets_kernel, dim3((maxn + 31) / 32, n), dim3(32 * FOLD_SUB), 0,
+                 (cudaStream_t)stream, f);
+  return zi::launch_status("zi_fold_sets");
 }
 
 int zi_colsum_fold(const float* part, int P, int N, void* out, int out_f32, void* stream) {

@@ -278,6 +278,17 @@ class GPTZeroEngine:
         # fc2.dx epilogue's 32-row block column sums of du (the fc1 bias gradient)
         self._csum = torch.empty(-(-cfg.tokens // 32) * 4 * cfg.hd if self.fused else 0,
                                  dtype=torch.float32, device=self.dev)
+        # Deferred folds: the block backward's four column folds (fc1 / qkv bias, LN2 / LN1
+        # gamma, beta and the residual-sum bias) as one zi_fold_sets launch at the end of the
+        # block instead of four (the same order, bitwise the same gradients). ZI_FOLD_DEFER=0
+        # folds after each producer (A/B only).
+        self.fold_defer = self.fused and os.environ.get("ZI_FOLD_DEFER", "1") != "0"
+        if self.fold_defer:
+            sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+            lnp = 3 * 2 * sms * cfg.hd
+            self._csum_qkv = torch.empty(-(-cfg.tokens // 32) * 3 * cfg.hd, dtype=torch.float32,
+                                         device=self.dev)
+            self._lnpart = [torch.empty(lnp, dtype=torch.float32, device=self.dev) for _ in range(2)]
         # Every linear of the block and the head runs on zi_gemm_sk (tcgen05 stream-K,
         # the neighbouring elementwise pass folded into its epilogue where the site has
         # one): "zi", the default. "cublas" (cuBLAS + a separate pass) and "auto" (time
@@ -970,6 +981,7 @@ class GPTZeroEngine:
         libzinf; GEMMs on zi_gemm_sk, attention on zi_attn (tcgen05)."""
         x, h1, m1, r1, att, o, x2, h2, m2, r2, u, a = cache
         ws = self.ws
+        folds = []     # (part, P, N, out) sets folded in one launch at the end (fold_defer)
         self._mm_dw("fc2.dW", dy, a, G["fc2_w"])
         du = torch.empty_like(u)
         if self._zi("fc2.dx", dy, P["fc2_w"], du, u) and self.epi_aux:
@@ -979,7 +991,10 @@ class GPTZeroEngine:
             part = self._colsum_part(T, H4)
             kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="mul" if self._gelu_save() else "dgelu",
                             x=u, colsum=part)
-            kernels.colsum_fold(part, -(-T // 32), H4, G["fc1_b"])
+            if self.fold_defer:
+                folds.append((part, -(-T // 32), H4, G["fc1_b"]))
+            else:
+                kernels.colsum_fold(part, -(-T // 32), H4, G["fc1_b"])
         elif self._zi("fc2.dx", dy, P["fc2_w"], du, u):   # A/B: separate bias pass
             kernels.gemm_sk(dy, P["fc2_w"].t(), du, epi="dgelu", x=u)
             kernels.bias_grad(du, G["fc1_b"], ws)
@@ -992,8 +1007,8 @@ class GPTZeroEngine:
         del du
         dx2 = torch.empty_like(dh2)
         # LN2 backward also sums dres = dy: the fc2 bias gradient, no extra pass
-        kernels.ln_bwd(dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"], ws, dres=dy,
-                       dres_sum=G["fc2_b"])
+        self._ln_bwd_fold(folds, 0, dh2, x2, P["ln2_w"], m2, r2, dx2, G["ln2_w"], G["ln2_b"],
+                          dres=dy, dres_sum=G["fc2_b"])
         self._mm_dw("proj.dW", dx2, o, G["proj_w"])
         if self._zi("proj.dx", dx2, P["proj_w"], o) and self.epi_aux:
             # dO = dx2 Wp; the epilogue also forms the attention backward's
@@ -1006,10 +1021,14 @@ class GPTZeroEngine:
             # the attention backward's epilogues also sum dqkv's columns per 32-row block:
             # the qkv bias gradient is one small fold instead of a pass over dqkv
             dqkv_cols = 3 * c.hd
-            part = self._colsum_part(c.tokens, dqkv_cols)
+            part = (self._csum_qkv[:c.tokens // 32 * dqkv_cols] if self.fold_defer
+                    else self._colsum_part(c.tokens, dqkv_cols))
             dqkv = self._attn_bwd(do, att, delta=delta, colsum=part)
             self._mm_dw("qkv.dW", dqkv, h1, G["qkv_w"])
-            kernels.colsum_fold(part, c.tokens // 32, dqkv_cols, G["qkv_b"])
+            if self.fold_defer:
+                folds.append((part, c.tokens // 32, dqkv_cols, G["qkv_b"]))
+            else:
+                kernels.colsum_fold(part, c.tokens // 32, dqkv_cols, G["qkv_b"])
         else:
             do = self._mm_dx("proj.dx", dx2, P["proj_w"])
             dqkv = self._attn_bwd(do, att)
@@ -1018,9 +1037,24 @@ class GPTZeroEngine:
         dh1 = self._mm_dx("qkv.dx", dqkv, P["qkv_w"])
         dx = torch.empty_like(dh1)
         # ... and LN1 backward sums dres = dx2: the proj bias gradient
-        kernels.ln_bwd(dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"], ws, dres=dx2,
-                       dres_sum=G["proj_b"])
+        self._ln_bwd_fold(folds, 1, dh1, x, P["ln1_w"], m1, r1, dx, G["ln1_w"], G["ln1_b"],
+                          dres=dx2, dres_sum=G["proj_b"])
+        if folds:
+            kernels.fold_sets(folds)
         return dx
+
+    def _ln_bwd_fold(self, folds, k, dy, x, w, mean, rstd, dx, dgamma, dbeta, dres, dres_sum):
+        """LayerNorm backward; with fold_defer its dgamma / dbeta / dres-sum folds join the
+        block's fold list (partials in the k-th LN partial buffer) instead of launching."""
+        if not self.fold_defer:
+            kernels.ln_bwd(dy, x, w, mean, rstd, dx, dgamma, dbeta, self.ws, dres=dres,
+                           dres_sum=dres_sum)
+            return
+        part = self._lnpart[k]
+        P = kernels.ln_bwd_partials(dy, x, w, mean, rstd, dx, part, dres=dres, dres_sum=True)
+        H = x.shape[-1]
+        for i, out in enumerate((dgamma, dbeta, dres_sum)):
+            folds.append((part[i * P * H:(i + 1) * P * H], P, H, out))
 
     def _block_bwd(self, dy, cache, P, G):
         if self.fused:

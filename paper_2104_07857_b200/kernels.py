@@ -547,3 +547,38 @@ def pos_grad(dx: torch.Tensor, B: int, out: torch.Tensor, stream=None) -> None:
     dkind = -1 if dx.dtype == torch.float32 else half_kind(dx.dtype)
     _lib.call("zi_pos_grad", _dev(dx, "dx"), dkind, B, S, hd,
               _dev(out, "out"), kind, _stream(stream))
+
+
+def ln_bwd_partials(dy, x, w, mean, rstd, dx, part: torch.Tensor, dres=None, dres_sum=False,
+                    stream=None) -> int:
+    """zi_ln_bwd_partials: zi_ln_bwd's row pass alone — dx (+ dres), and the CTA partials
+    of dgamma, dbeta (and the column sums of dres with dres_sum) as part[sets][P][H].
+    Returns P; :func:`fold_sets` folds them (bitwise zi_ln_bwd's gradients)."""
+    import ctypes
+    H = x.shape[-1]
+    T = x.numel() // H
+    if part.dtype != torch.float32 or not part.is_cuda:
+        raise ValueError("part: fp32 CUDA tensor")
+    n = ctypes.c_int(0)
+    _lib.call("zi_ln_bwd_partials", _bf16_2d(dy, "dy"), _bf16_2d(x, "x"), _bf16_2d(w, "w"),
+              _dev(mean, "mean"), _dev(rstd, "rstd"),
+              _bf16_2d(dres, "dres") if dres is not None else None, _bf16_2d(dx, "dx"),
+              int(bool(dres_sum)), _dev(part, "part"), part.numel(), T, H, ctypes.byref(n),
+              _stream(stream))
+    return n.value
+
+
+def fold_sets(sets, stream=None) -> None:
+    """zi_fold_sets: out[c] = sum_p part[p, c] in p order for every (part, P, N, out) set,
+    one launch (at most 8 sets; outputs all bf16 or all fp32)."""
+    if not 1 <= len(sets) <= _lib.FOLD_MAX_SETS:
+        raise ValueError(f"fold_sets: 1..{_lib.FOLD_MAX_SETS} sets")
+    f32 = {o.dtype == torch.float32 for _, _, _, o in sets}
+    if len(f32) != 1:
+        raise ValueError("fold_sets: outputs must share a dtype")
+    arr = (_lib.FoldSetC * len(sets))()
+    for i, (part, P, N, out) in enumerate(sets):
+        if part.dtype != torch.float32 or part.numel() < P * N or out.numel() != N:
+            raise ValueError(f"fold_sets: set {i}: part fp32 [P, N], out [N]")
+        arr[i] = _lib.FoldSetC(part.data_ptr(), P, N, _dev(out, "out"))
+    _lib.call("zi_fold_sets", arr, len(sets), int(f32.pop()), _stream(stream))

@@ -135,3 +135,40 @@ def test_softmax_ce(T, V):
     K.softmax_ce(work, tgt, rows, loss, 1.0 / T)
     assert abs(loss.item() - ref_loss.item()) < 1e-4 * max(1.0, abs(ref_loss.item()))
     close(work, lf.grad, atol=1e-4 / T)
+
+
+@pytest.mark.parametrize("T,H,dres", [(8192, 2048, True), (300, 4096, True), (513, 1024, False),
+                                      (17, 8192, True), (3, 128, False)])
+def test_ln_bwd_partials_and_fold_sets_equal_ln_bwd(T, H, dres):
+    """zi_ln_bwd_partials + zi_fold_sets (the deferred folds) == zi_ln_bwd, bit for bit,
+    with a colsum fold riding in the same zi_fold_sets launch == zi_colsum_fold."""
+    g = torch.Generator(device="cuda").manual_seed(T * 7 + H)
+    x = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    w = (1 + 0.1 * torch.randn(H, device="cuda", generator=g)).bfloat16()
+    dy = torch.randn(T, H, device="cuda", generator=g).bfloat16()
+    dr = torch.randn(T, H, device="cuda", generator=g).bfloat16() if dres else None
+    y, mean, rstd = torch.empty_like(x), torch.empty(T, device="cuda"), torch.empty(T, device="cuda")
+    K.ln_fwd(x, w, torch.zeros_like(w), y, mean, rstd)
+    outs = []
+    for deferred in (False, True):
+        dx = torch.empty_like(x)
+        dg, db, ds = (torch.empty(H, device="cuda").bfloat16() for _ in range(3))
+        if deferred:
+            part = torch.empty(3 * 2 * 148 * H + 1000, device="cuda")
+            P = K.ln_bwd_partials(dy, x, w, mean, rstd, dx, part, dres=dr, dres_sum=dres)
+            sets = [(part[i * P * H:], P, H, o) for i, o in enumerate((dg, db, ds)[:3 if dres else 2])]
+            K.fold_sets(sets)
+        else:
+            K.ln_bwd(dy, x, w, mean, rstd, dx, dg, db, K.Workspace(), dres=dr, dres_sum=ds if dres else None)
+        outs.append((dx, dg, db, ds if dres else dg))
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    # column partials of another producer folded in the same launch, fp32 outputs
+    cp = torch.randn(37, 611, device="cuda", generator=g)
+    o1 = torch.empty(611, device="cuda")
+    o2 = torch.empty(611, device="cuda")
+    o3 = torch.empty(5, device="cuda")
+    K.colsum_fold(cp, 37, 611, o1)
+    K.fold_sets([(cp, 37, 611, o2), (cp, 2, 5, o3)])
+    assert torch.equal(o1, o2)
+    assert torch.equal(o3, cp.view(-1)[:5] + cp.view(-1)[5:10])   # part[p * N + c], N = 5

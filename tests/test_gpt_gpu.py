@@ -389,3 +389,20 @@ def test_step_bitwise_reproducible():
     for k in runs[0][1]:
         for r in range(2):
             assert torch.equal(runs[0][1][k][r], runs[1][1][k][r]), k
+
+
+def test_deferred_folds_bitwise_equal(monkeypatch):
+    """The block backward's folds as one zi_fold_sets launch (default) == one fold per
+    producer (ZI_FOLD_DEFER=0): same losses and master shards bit for bit."""
+    runs = []
+    for defer in ("1", "0"):
+        monkeypatch.setenv("ZI_FOLD_DEFER", defer)
+        e = eg.GPTZeroEngine(eg.TINY, LocalComm(2), lr=1e-3)
+        assert e.fold_defer == (defer == "1")
+        losses = [e.step(batches_for(eg.TINY, 2, s)).item() for s in range(2)]
+        runs.append((losses, {k: [e.shard(k, r)["p32"].cpu() for r in range(2)] for k in e.by_key}))
+        del e
+    assert runs[0][0] == runs[1][0]
+    for k in runs[0][1]:
+        for r in range(2):
+            assert torch.equal(runs[0][1][k][r], runs[1][1][k][r]), k
