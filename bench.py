@@ -550,14 +550,15 @@ def run_ours(args):
                     "d2h_bytes_per_step": 4},
             "gpu_launches": launches,
             "gemm_sites": gemm_sites,
-            "roofline_hbm": {"kernel": "zi_rs_adam_dc (fused RS + cast + Adam, 50.4M-element block "
-                                   "bucket, 28 B/elem)",
+            "roofline_hbm": {"kernel": "zi_rs_adam_dc (fused RS + cast + Adam over a block bucket's "
+                                   "shard: 2 B per contribution + 26 B per shard element)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4),
                          "bytes_per_launch": big, "avg_launch_ms": round(avg_ms, 4),
                          "share_of_step": round(rs_share, 4),
-                         "traffic": _ncu_traffic("zi_rs_adam_dc")},
+                         # the ncu capture is of the N=1 launch (50.4M elements, 1 contribution)
+                         "traffic": _ncu_traffic("zi_rs_adam_dc") if world == 1 else None},
             "clocks": clocks.summary(),
             "offload": offload,
             "collectives": collectives,
