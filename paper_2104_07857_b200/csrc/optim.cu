@@ -145,6 +145,17 @@ rs_kernel(Contribs cb, int K, size_t off, size_t n, size_t nvec8, size_t clen, f
   }
 }
 
+// ZI_RS_WAVES (A/B): grid = that many waves of resident CTAs (default 1)
+static int rs_waves() {
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("ZI_RS_WAVES");
+    w = e ? atoi(e) : 1;
+    if (w < 1) w = 1;
+  }
+  return w;
+}
+
 template <bool ADAM>
 int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t clen,
               float scale, int half_kind, float* out_or_g, float* p, float* m, float* v,
@@ -170,7 +181,19 @@ int launch_rs(const void* const* contribs, int K, size_t off, size_t n, size_t c
   const size_t nvec8 = vec ? valid / 8 : 0;
   const zi_adam_consts cc = c ? *c : zi_adam_consts{};
   const int block = 256;
-  const int grid = grid_for(nvec8 + (n - nvec8 * 8), block);
+  // one wave of resident CTAs (64 registers: 4 per SM), each grid-striding: a grid of
+  // 8 per SM ran as two waves with a ragged hand-over between them
+  static int per_sm[2] = {0, 0};
+  int& ps = per_sm[half_kind == ZI_HALF_BF16];
+  if (ps == 0) {
+    int b = 0;
+    if (half_kind == ZI_HALF_BF16)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_kernel<ZI_HALF_BF16, ADAM>, block, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, rs_kernel<ZI_HALF_FP16, ADAM>, block, 0);
+    ps = b > 0 ? b : 8;
+  }
+  const int grid = grid_for(nvec8 + (n - nvec8 * 8), block, rs_waves() * ps);
   cudaStream_t s = (cudaStream_t)stream;
   uint16_t* ph = static_cast<uint16_t*>(p_half);
   // (two 8-element groups per thread-iteration, all 14 loads in flight, measured slower
